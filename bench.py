@@ -1,0 +1,421 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 oil-paint filter hot path (one JSON line on rank 0).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl b200|reference]
+
+Workload (config.workload): BASELINE.json's large-radius configuration, the one
+the north-star target is quoted on -- config 4, 16384x16384 uniform-noise RGB8,
+r=15, L=20, CopyInput (the other four configs are parity-test cases;
+--config selects them for manual runs).  A "step" is one pass of the filter over
+the whole image.  N>1 (torchrun, one process per GPU): the image's rows are
+split into N contiguous bands with r-row halos; every rank filters
+its band; no collective on the data path (NCCL is used only for the barrier and
+the max-over-ranks timing).
+
+Reported:
+  value     output MP/s of the whole job, device-resident inputs, timed with CUDA
+            events on the launching stream, max over ranks; the 805 MB input is
+            larger than the 126 MB L2, so no flush is needed between steps.
+  e2e       the same metric through the C-ABI host-pointer call (pinned host
+            buffers, H2D + kernels + D2H inside the timed region).
+  roofline  issue-rate bound: colhist model ops/px x interior
+            pixels / kernel time vs 148 SMs x 4 warp-instr/clk x 32 lanes x
+            1965 MHz; the HBM side (6 B/px at 6548.5 GB/s measured) is reported
+            beside it.
+  cpu_baseline  the unmodified reference library (oracle/_ref, apply_parallel's
+            row-band engine) on all host cores of the box, on a bounded band of
+            the same image.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}
+NUM_SMS_B200 = 148
+
+
+def load_peaks() -> tuple[dict, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text()), "measured"
+    return dict(PEAKS_FALLBACK), "fallback"
+
+
+def colhist_ops_per_px(bins: int) -> int:
+    # colhist (Perreault-Hebert, O(B)) = 7*2 + 8*B + 3*B + 12 lane-ops
+    return 7 * 2 + 8 * bins + 3 * bins + 12
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self._t.join(timeout=2)
+
+    def summary(self) -> dict:
+        mhz, max_mhz, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                mhz.append(float(f[1]))
+                max_mhz = max(max_mhz, float(f[2]))
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(mhz) if mhz else None,
+                "sm_max_mhz": max_mhz or None, "reasons": sorted(reasons),
+                "samples": len(mhz)}
+
+
+# ----------------------------------------------------------------------------
+# CPU legs: the reference library (oracle/_ref) or, if it was not built, the
+# C restatement (oracle/).  Used only for cpu_baseline and --impl reference.
+# ----------------------------------------------------------------------------
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+class CpuEngine:
+    def __init__(self):
+        sys.path.insert(0, str(ROOT / "tests"))
+        import oracle_lib
+        self.kind = "reference"
+        try:
+            self.ref = oracle_lib.load_ref()
+        except (FileNotFoundError, OSError):
+            self.ref = None
+            self.kind = "port"
+            self.oracle = oracle_lib.oracle()
+
+    def band(self, img: np.ndarray, out: np.ndarray, radius: int, levels: int, y0: int, y1: int,
+             threads: int) -> None:
+        h, w, _ = img.shape
+        if self.ref is not None:
+            rc = self.ref.ref_filter_band(img.ctypes.data, out.ctypes.data, w, h, radius, levels,
+                                          y0, y1, threads)
+            assert rc == 0
+        else:  # C port: filter a sub-image holding the band plus halos
+            sub = np.ascontiguousarray(img[y0 - radius:y1 + radius])
+            tmp = np.empty_like(sub)
+            rc = self.oracle.oracle_filter_mt(sub.ctypes.data, tmp.ctypes.data, w, sub.shape[0],
+                                              radius, levels, 0, threads)
+            assert rc == 0
+            out[y0:y1] = tmp[radius:radius + (y1 - y0)]
+
+    def calibrate_rows(self, img, out, cfg, threads, target_s) -> tuple[int, float]:
+        r = cfg.radius
+        y0 = r
+        rows = max(1, min(8, cfg.height - 2 * r))
+        t = time.perf_counter()
+        self.band(img, out, r, cfg.levels, y0, y0 + rows, threads)
+        dt = time.perf_counter() - t
+        rate = rows / max(dt, 1e-6)
+        want = int(max(1, min(cfg.height - 2 * r, rate * target_s)))
+        return want, rate
+
+
+def cpu_sample_run(cfg, img, threads: int, target_s: float, steps: int = 1, warmup: int = 0):
+    """Times the reference engine on a bounded band of rows of the bench image."""
+    eng = CpuEngine()
+    out = np.zeros_like(img)
+    rows, _ = eng.calibrate_rows(img, out, cfg, threads, target_s)
+    y0 = cfg.radius
+    for _ in range(warmup):
+        eng.band(img, out, cfg.radius, cfg.levels, y0, y0 + rows, threads)
+    times = []
+    for _ in range(steps):
+        t = time.perf_counter()
+        eng.band(img, out, cfg.radius, cfg.levels, y0, y0 + rows, threads)
+        times.append(time.perf_counter() - t)
+    mp = rows * cfg.width / 1e6  # output megapixels of the sample (rows x full width)
+    return eng.kind, rows, mp, times
+
+
+def reference_arm(args, cfg) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    img = cfg.generate(0)
+    threads = host_threads()
+    step_s = float(os.environ.get("OILPAINT_REF_STEP_S", "4"))
+    kind, rows, mp, times = cpu_sample_run(cfg, img, threads, step_s, args.steps, args.warmup)
+    total = sum(times)
+    value = mp * len(times) / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "MP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1000 * total / len(times), 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": workload_config(cfg, args.gpus),
+        "cpu_baseline": {"value": round(value, 4), "unit": "MP/s", "cores": threads, "kind": kind,
+                         "sample": f"rows [{cfg.radius}, {cfg.radius + rows}) x {cfg.width} cols "
+                                   f"of the {cfg.name} image per step ({mp:.2f} MP), "
+                                   f"{'apply_parallel row-band engine (parallel_for_rows + filter_pixel)' if kind == 'reference' else 'C port'}, "
+                                   f"{threads} threads, {cpu_model()}"},
+        "e2e": {"value": round(value, 4), "unit": "MP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "output megapixels/sec at radius r, levels L (1/2/4/8 B200) and % of roofline"
+
+
+def workload_config(cfg, n: int) -> dict:
+    return {"workload": f"{cfg.name}: {cfg.description}", "width": cfg.width,
+            "height": cfg.height, "frames": cfg.frames, "radius": cfg.radius,
+            "levels": cfg.levels, "border": "CopyInput", "partition":
+            ("frames" if cfg.frames > 1 else "row bands with r-row halos") + f" over {n} GPU(s)",
+            "l2": "input 805 MB > 126 MB L2 (no flush needed)" if cfg.name == "c4" else
+                  "inputs re-read each step; L2 not flushed (small config)"}
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    from paper_1405_1020_b200.patterns import CONFIGS
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        reference_arm(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_1405_1020_b200 as opc
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    W, H, F = cfg.width, cfg.height, cfg.frames
+    r, L = cfg.radius, cfg.levels
+    params = opc.FilterParams(r, L, opc.BorderPolicy.CopyInput)
+    stream = torch.cuda.Stream()
+    ccfg = opc.CudaConfig(device=local, stream=stream.cuda_stream,
+                          allow_levels_256=(L == 256))
+
+    # ---- this rank's share: row band (single image) or frames (batch) ----
+    if F == 1:
+        y0, y1 = H * rank // world, H * (rank + 1) // world
+        lo, hi = opc.band_input_rows(H, y0, y1, r)
+        full = cfg.generate(0)
+        host_in = torch.from_numpy(np.ascontiguousarray(full[lo:hi])).pin_memory()
+        out_shape = (y1 - y0, W, 3)
+        my_frames = 1
+        out_pixels = (y1 - y0) * W
+        interior = max(0, min(y1, H - r) - max(y0, r)) * (W - 2 * r)
+    else:
+        f0, f1 = F * rank // world, F * (rank + 1) // world
+        my_frames = f1 - f0
+        host_in = torch.empty((my_frames, H, W, 3), dtype=torch.uint8).pin_memory()
+        for i in range(my_frames):
+            cfg.generate(f0 + i, out=host_in[i].numpy())
+        out_shape = (my_frames, H, W, 3)
+        full = host_in[0].numpy()
+        out_pixels = my_frames * H * W
+        interior = my_frames * (H - 2 * r) * (W - 2 * r)
+    dev_in = host_in.to(f"cuda:{local}")
+    dev_out = torch.empty(out_shape, dtype=torch.uint8, device=f"cuda:{local}")
+
+    def step_device():
+        if F == 1:
+            opc.apply_cuda_band_device(dev_in.data_ptr(), dev_out.data_ptr(), W, H, y0, y1,
+                                       params, ccfg)
+        else:
+            opc.apply_cuda_device(dev_in.data_ptr(), dev_out.data_ptr(), W, H, params, ccfg,
+                                  frames=my_frames)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step_device()
+    stream.synchronize()
+
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    launches0 = opc.kernel_launches()
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        with torch.cuda.stream(stream):
+            ev[0].record(stream)
+            for i in range(args.steps):
+                step_device()
+                ev[i + 1].record(stream)
+        stream.synchronize()
+    torch.cuda.synchronize()
+    barrier()
+    launches = opc.kernel_launches() - launches0
+    step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    total_ms = ev[0].elapsed_time(ev[args.steps])
+    t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    job_pixels = F * W * H
+    value = job_pixels / (ms_per_step / 1e3) / 1e6
+
+    # ---- end to end through the public C-ABI with pinned host buffers ----
+    host_out = torch.empty(out_shape, dtype=torch.uint8).pin_memory()
+    e2e_cfg = opc.CudaConfig(device=local, allow_levels_256=(L == 256))
+    import ctypes as _ct
+    from paper_1405_1020_b200._lib import LIB
+    c_e2e = e2e_cfg.to_c()
+
+    def step_e2e():
+        if F == 1:
+            rc = LIB.opc_filter_rgb8_band(host_in.data_ptr(), host_out.data_ptr(), W, H, y0, y1,
+                                          r, L, 0, _ct.byref(c_e2e))
+        else:
+            rc = LIB.opc_filter_rgb8_batch(host_in.data_ptr(), host_out.data_ptr(), my_frames, W,
+                                           H, r, L, 0, _ct.byref(c_e2e))
+        assert rc == 0, LIB.opc_last_error()
+
+    step_e2e()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        step_e2e()
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = job_pixels * args.e2e_steps / float(te.item()) / 1e6
+    # the e2e output must equal the device-resident output
+    assert torch.equal(host_out, dev_out.cpu()), "e2e output differs from device output"
+
+    # ---- roofline (issue-rate bound) ----
+    peaks, peaks_kind = load_peaks()
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    num_sms = torch.cuda.get_device_properties(local).multi_processor_count
+    peak_ops = num_sms * 4 * 32 * sm_mhz * 1e6
+    ops_px = colhist_ops_per_px(L + 1)
+    kernel_ms = statistics.mean(step_ms)
+    achieved_ops = ops_px * interior / (kernel_ms / 1e3)
+    traffic = None
+    tp = ROOT / "profiles" / f"{cfg.name}_dram_bytes.json"
+    if tp.exists():
+        traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
+    hbm_gbs = float(peaks.get("hbm_gbs", 6650.0))
+    alg_bytes = 6 * out_pixels / max(1, 1)
+    roofline = {
+        "bound": "issue", "achieved": round(achieved_ops / 1e12, 3),
+        "peak": round(peak_ops / 1e12, 3), "unit": "Tlane-op/s",
+        "frac": round(achieved_ops / peak_ops, 4), "traffic": traffic,
+        "model": f"colhist {ops_px} lane-ops per interior pixel (SURVEY 8d, B={L + 1}); "
+                 f"{num_sms} SMs x 4 x 32 x {sm_mhz:.0f} MHz ({peaks_kind} sm_max_mhz)",
+        "algorithmic_ops_per_launch": ops_px * interior,
+        "kernel_ms": round(kernel_ms, 4),
+        "hbm": {"achieved_gbs": round(alg_bytes / (kernel_ms / 1e3) / 1e9, 1),
+                "peak_gbs": hbm_gbs, "frac": round(alg_bytes / (kernel_ms / 1e3) / 1e9 / hbm_gbs, 4),
+                "bytes_per_launch": alg_bytes, "peak_kind": peaks_kind},
+    }
+
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "MP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic", "config": workload_config(cfg, world),
+        "roofline": roofline,
+        "e2e": {"value": round(e2e_value, 2), "unit": "MP/s",
+                "h2d_bytes_per_step": int(host_in.numel()),
+                "d2h_bytes_per_step": int(host_out.numel()),
+                "path": "opc_filter_rgb8_band / _batch (host pointers, pinned), "
+                        f"{args.e2e_steps} steps, wall clock, max over ranks"},
+        "gpu_launches": int(launches),
+        "clocks": clocks.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu and F == 1:
+        threads = host_threads()
+        kind, rows, mp, times = cpu_sample_run(cfg, full, threads, args.cpu_seconds)
+        line["cpu_baseline"] = {
+            "value": round(mp / times[0], 4), "unit": "MP/s", "cores": threads, "kind": kind,
+            "sample": f"rows [{r}, {r + rows}) x {W} cols of the {cfg.name} image "
+                      f"({mp:.2f} MP, {times[0]:.1f} s), reference apply_parallel row-band "
+                      f"engine on {threads} threads, {cpu_model()}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,127 @@
+/*
+ * oilpaint_b200.h -- C-ABI of the B200-native histogram oil-paint filter.
+ *
+ * Drop-in boundary for the reference engines of arxiv/paper_1405_1020
+ * ("oilbench", /root/reference/proj):
+ *
+ *   Image apply_sequential(const Image&, const FilterParams&)
+ *       -- proj/include/oilpaint/filter.hpp:109, proj/src/filter.cpp:51-68
+ *   Image apply_parallel(const Image&, const FilterParams&, const ParallelConfig&)
+ *       -- proj/include/oilpaint/parallel.hpp:33, proj/src/parallel.cpp:110-132
+ *   void validate(const Image&, const FilterParams&)
+ *       -- proj/include/oilpaint/filter.hpp:25, proj/src/filter.cpp:8-26
+ *
+ * Buffer layout is the reference Image layout (proj/include/oilpaint/image.hpp:
+ * 17-19, 27): interleaved 8-bit R,G,B, row-major, stride 3*W bytes, no padding,
+ * exactly 3*W*H bytes per image.  Semantics are the reference's bit for bit:
+ * bin = (R+G+B)*L/765 in unsigned integer arithmetic (filter.hpp:31-35), L+1
+ * bins, lowest-index strict-> maximum (filter.hpp:71-82), truncating channel
+ * quotient (filter.cpp:41-43), interior x in [r, W-r), y in [r, H-r), border
+ * copied (CopyInput, default) or zeroed (ZeroFill) (filter.hpp:13-22).
+ *
+ * Status codes (errors are codes here; include/oilpaint_b200.hpp maps them to
+ * the reference's exception types):
+ *   OPC_OK      0
+ *   OPC_EINVAL  1  parameter/shape error   -> std::invalid_argument
+ *   OPC_ECUDA   2  CUDA/runtime failure     -> std::runtime_error
+ *   OPC_ENOMEM  3  device/host allocation   -> std::system_error / bad_alloc
+ * opc_last_error() returns a thread-local message for the last failing call.
+ *
+ * Threading: every entry point is blocking (host-pointer calls) and
+ * thread-safe; calls on one device are serialised by the library (the
+ * reference allows "serialized or interleaved at the engine's discretion",
+ * SPEC.md concurrency model).  Device-pointer calls (OPC_FLAG_DEVICE_POINTERS)
+ * are asynchronous on cfg->stream.
+ */
+#ifndef OILPAINT_B200_H
+#define OILPAINT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OPC_OK 0
+#define OPC_EINVAL 1
+#define OPC_ECUDA 2
+#define OPC_ENOMEM 3
+
+/* BorderPolicy, proj/include/oilpaint/filter.hpp:13-16 */
+#define OPC_BORDER_COPY_INPUT 0
+#define OPC_BORDER_ZERO_FILL 1
+
+/* cfg->flags */
+#define OPC_FLAG_DEVICE_POINTERS 0x1u /* in/out are device pointers on cfg->device  */
+#define OPC_FLAG_ALLOW_LEVELS_256 0x2u /* documented extension: accept L = 256 (257 bins, config 3) */
+
+/* cfg->kernel: 0 = automatic choice; the others force one kernel family
+ * (test hooks, every family is bit-exact on every input it accepts). */
+#define OPC_KERNEL_AUTO 0
+#define OPC_KERNEL_DIRECT 1 /* one thread per output pixel, O(r^2), any r and L  */
+#define OPC_KERNEL_SKEW 2   /* warp-skewed column-difference sliding, L+1 <= 32, r <= 15 */
+
+typedef struct opc_config {
+    int32_t device;  /* CUDA device ordinal; -1 = current device              */
+    uint32_t flags;  /* OPC_FLAG_*                                            */
+    void* stream;    /* cudaStream_t for device-pointer calls; NULL = default */
+    int32_t kernel;  /* OPC_KERNEL_*                                          */
+    int32_t reserved;
+} opc_config;
+
+/* Reference validate (proj/src/filter.cpp:8-26): 0 or OPC_EINVAL with a
+ * message in opc_last_error().  Pure host logic, needs no GPU.  `flags` may
+ * carry OPC_FLAG_ALLOW_LEVELS_256. */
+int opc_validate(int32_t width, int32_t height, uint64_t nbytes, int32_t radius, int32_t levels,
+                 uint32_t flags);
+
+/* Whole-image filter: the apply_sequential / apply_parallel replacement.
+ * in, out: 3*width*height bytes each, must not alias.  cfg may be NULL. */
+int opc_filter_rgb8(const uint8_t* in, uint8_t* out, int32_t width, int32_t height,
+                    int32_t radius, int32_t levels, int32_t border, const opc_config* cfg);
+
+/* Frame batch (config 5): `frames` images of width x height stored back to
+ * back (frame f at byte offset f*3*width*height) in in and out. */
+int opc_filter_rgb8_batch(const uint8_t* in, uint8_t* out, int32_t frames, int32_t width,
+                          int32_t height, int32_t radius, int32_t levels, int32_t border,
+                          const opc_config* cfg);
+
+/* Row band of a height-row image (multi-GPU row partition):
+ * in_rows holds image rows [max(0, y_begin - radius), min(height, y_end + radius))
+ * and out_rows receives output rows [y_begin, y_end); the border policy applies
+ * to the global border only.  Bands [0,a),[a,b),...,[z,height) reassemble the
+ * whole-image result byte for byte. */
+int opc_filter_rgb8_band(const uint8_t* in_rows, uint8_t* out_rows, int32_t width,
+                         int32_t height, int32_t y_begin, int32_t y_end, int32_t radius,
+                         int32_t levels, int32_t border, const opc_config* cfg);
+
+/* Helpers for the band protocol: first input row and input row count. */
+int32_t opc_band_in_row0(int32_t height, int32_t y_begin, int32_t radius);
+int32_t opc_band_in_rows(int32_t height, int32_t y_begin, int32_t y_end, int32_t radius);
+
+const char* opc_last_error(void);
+const char* opc_version(void);
+
+/* Number of CUDA kernels this library has launched in this process (the
+ * bench's gpu_launches evidence). */
+uint64_t opc_kernel_launches(void);
+
+/* Number of visible CUDA devices (0 without a GPU; never fails). */
+int32_t opc_device_count(void);
+
+/* Blocks until all work the library queued on cfg's device/stream is done. */
+int opc_synchronize(const opc_config* cfg);
+
+/* Which kernel family OPC_KERNEL_AUTO would use for these parameters
+ * (OPC_KERNEL_*), or -1 if invalid.  Host logic only. */
+int32_t opc_plan_kernel(int32_t width, int32_t height, int32_t radius, int32_t levels);
+
+/* Releases cached device buffers and streams. */
+void opc_release(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* OILPAINT_B200_H */

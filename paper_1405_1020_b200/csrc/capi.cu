@@ -1,0 +1,410 @@
+// capi.cu -- the C-ABI (include/oilpaint_b200.h): validation with the
+// reference's rules and messages, per-device contexts (stream + cached device
+// buffers behind a mutex), host<->device staging, kernel-family dispatch and
+// status/error mapping.
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/oilpaint_b200.h"
+#include "kernels.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<unsigned long long> g_launches{0};
+
+int set_error(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+int cuda_error(cudaError_t e, const char* what) {
+    const int code = (e == cudaErrorMemoryAllocation) ? OPC_ENOMEM : OPC_ECUDA;
+    return set_error(code, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// proj/src/filter.cpp:8-26 (messages restated) and proj/src/image.cpp:10-16.
+int validate_params(int w, int h, unsigned long long nbytes, int radius, int levels,
+                    unsigned flags) {
+    if (w < 1 || h < 1) {
+        return set_error(OPC_EINVAL, "image dimensions must be positive, got " +
+                                         std::to_string(w) + "x" + std::to_string(h));
+    }
+    if (radius < 0) {
+        return set_error(OPC_EINVAL, "radius must be >= 0, got " + std::to_string(radius));
+    }
+    const int max_levels = (flags & OPC_FLAG_ALLOW_LEVELS_256) ? 256 : 255;
+    if (levels < 1 || levels > max_levels) {
+        return set_error(OPC_EINVAL, "intensity_levels must be in [1, " +
+                                         std::to_string(max_levels) + "], got " +
+                                         std::to_string(levels));
+    }
+    const int min_dim = w < h ? w : h;
+    if (2LL * radius >= min_dim) {
+        return set_error(OPC_EINVAL, "radius " + std::to_string(radius) +
+                                         " leaves no interior for a " + std::to_string(w) + "x" +
+                                         std::to_string(h) +
+                                         " image (need 2*radius < min dimension)");
+    }
+    if (nbytes != 3ull * static_cast<unsigned long long>(w) * static_cast<unsigned long long>(h)) {
+        return set_error(OPC_EINVAL, "image data length does not match its dimensions");
+    }
+    return OPC_OK;
+}
+
+struct DevCtx {
+    std::mutex mu;
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    void* d_in = nullptr;
+    std::size_t in_cap = 0;
+    void* d_out = nullptr;
+    std::size_t out_cap = 0;
+    int* d_counter = nullptr;
+    unsigned counter_idx = 0;
+    cudaStream_t s_in = nullptr;   // H2D copies
+    cudaStream_t s_out = nullptr;  // D2H copies
+    std::vector<cudaEvent_t> ev_in, ev_out;
+};
+
+int ensure_streams(DevCtx* c, std::size_t units) {
+    cudaError_t e = cudaSuccess;
+    if (!c->s_in) {
+        e = cudaStreamCreateWithFlags(&c->s_in, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking);
+        if (e != cudaSuccess) {
+            g_last_error = std::string("cudaStreamCreate: ") + cudaGetErrorString(e);
+            return OPC_ECUDA;
+        }
+    }
+    while (c->ev_in.size() < units) {
+        cudaEvent_t a = nullptr, b = nullptr;
+        e = cudaEventCreateWithFlags(&a, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b, cudaEventDisableTiming);
+        if (e != cudaSuccess) {
+            g_last_error = std::string("cudaEventCreate: ") + cudaGetErrorString(e);
+            return OPC_ECUDA;
+        }
+        c->ev_in.push_back(a);
+        c->ev_out.push_back(b);
+    }
+    return OPC_OK;
+}
+
+std::mutex g_ctx_mu;
+std::vector<std::unique_ptr<DevCtx>> g_ctx;
+
+int get_ctx(int device, DevCtx** out) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        return set_error(OPC_ECUDA, std::string("no CUDA device available: ") +
+                                        (e == cudaSuccess ? "0 devices" : cudaGetErrorString(e)));
+    }
+    if (device < 0) {
+        e = cudaGetDevice(&device);
+        if (e != cudaSuccess) return cuda_error(e, "cudaGetDevice");
+    }
+    if (device >= count) {
+        return set_error(OPC_EINVAL, "device " + std::to_string(device) + " out of range (" +
+                                         std::to_string(count) + " devices)");
+    }
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    if (g_ctx.size() < static_cast<std::size_t>(count)) g_ctx.resize(count);
+    if (!g_ctx[device]) {
+        auto c = std::make_unique<DevCtx>();
+        c->device = device;
+        e = cudaSetDevice(device);
+        if (e != cudaSuccess) return cuda_error(e, "cudaSetDevice");
+        cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+        e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return cuda_error(e, "cudaStreamCreate");
+        e = cudaMalloc(&c->d_counter, 64 * sizeof(int));
+        if (e != cudaSuccess) return cuda_error(e, "cudaMalloc(counter)");
+        g_ctx[device] = std::move(c);
+    }
+    *out = g_ctx[device].get();
+    return OPC_OK;
+}
+
+int ensure(void** p, std::size_t* cap, std::size_t need) {
+    if (*cap >= need) return OPC_OK;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *cap = 0;
+    cudaError_t e = cudaMalloc(p, need);
+    if (e != cudaSuccess) return cuda_error(e, "cudaMalloc");
+    *cap = need;
+    return OPC_OK;
+}
+
+int plan(int levels, int radius, int forced) {
+    if (forced == OPC_KERNEL_DIRECT) return OPC_KERNEL_DIRECT;
+    if (forced == OPC_KERNEL_SKEW) return opc::skew_supported(levels, radius) ? OPC_KERNEL_SKEW : -1;
+    return opc::skew_supported(levels, radius) ? OPC_KERNEL_SKEW : OPC_KERNEL_DIRECT;
+}
+
+// Runs the filter on device buffers already holding the band input.
+int run_device(const opc::BandArgs& a, int border, int kernel, DevCtx* ctx, cudaStream_t s) {
+    cudaError_t e = cudaSuccess;
+    if (kernel == OPC_KERNEL_SKEW) {
+        // Rotate over 64 task counters so kernels in flight on different
+        // streams never share one.
+        int* counter = ctx->d_counter + (ctx->counter_idx++ & 63u);
+        e = opc::launch_skew(a, counter, ctx->num_sms, s);
+        if (e != cudaSuccess) return cuda_error(e, "skew kernel launch");
+    } else {
+        e = opc::launch_direct(a, s);
+        if (e != cudaSuccess) return cuda_error(e, "direct kernel launch");
+    }
+    if (a.y_hi > a.y_lo && a.x_hi > a.x_lo) g_launches.fetch_add(1);
+    e = opc::launch_border(a, border, s);
+    if (e != cudaSuccess) return cuda_error(e, "border kernel launch");
+    if (a.radius > 0) g_launches.fetch_add(1);
+    return OPC_OK;
+}
+
+int filter_core(const std::uint8_t* in, std::uint8_t* out, int frames, int w, int h, int y_begin,
+                int y_end, int radius, int levels, int border, const opc_config* cfg) {
+    const unsigned flags = cfg ? cfg->flags : 0u;
+    int rc = validate_params(w, h, 3ull * w * h, radius, levels, flags);
+    if (rc != OPC_OK) return rc;
+    if (frames < 1) return set_error(OPC_EINVAL, "frames must be >= 1, got " + std::to_string(frames));
+    if (y_begin < 0 || y_end > h || y_begin >= y_end) {
+        return set_error(OPC_EINVAL, "row band [" + std::to_string(y_begin) + ", " +
+                                         std::to_string(y_end) + ") is not inside [0, " +
+                                         std::to_string(h) + ")");
+    }
+    if (border != OPC_BORDER_COPY_INPUT && border != OPC_BORDER_ZERO_FILL) {
+        return set_error(OPC_EINVAL, "border must be 0 (CopyInput) or 1 (ZeroFill), got " +
+                                         std::to_string(border));
+    }
+    if (!in || !out) return set_error(OPC_EINVAL, "null image buffer");
+    const int kernel = plan(levels, radius, cfg ? cfg->kernel : 0);
+    if (kernel < 0) {
+        return set_error(OPC_EINVAL, "requested kernel family does not support L=" +
+                                         std::to_string(levels) + " r=" + std::to_string(radius));
+    }
+
+    DevCtx* ctx = nullptr;
+    rc = get_ctx(cfg ? cfg->device : -1, &ctx);
+    if (rc != OPC_OK) return rc;
+
+    // Buffer geometry: per frame, `in` holds image rows [in_row0, in_row0 +
+    // in_rows) and `out` holds output rows [y_begin, y_end).
+    opc::BandArgs a{};
+    a.width = w;
+    a.height = h;
+    a.in_row0 = opc_band_in_row0(h, y_begin, radius);
+    a.in_rows = opc_band_in_rows(h, y_begin, y_end, radius);
+    a.out_row0 = y_begin;
+    a.x_lo = radius;
+    a.x_hi = w - radius;
+    a.radius = radius;
+    a.levels = levels;
+    a.bin_mul = opc::bin_multiplier(levels);
+    const std::size_t row_bytes = static_cast<std::size_t>(w) * 3;
+    const std::size_t in_bytes = row_bytes * a.in_rows;
+    const std::size_t out_bytes = row_bytes * (y_end - y_begin);
+    a.in_frame_stride = in_bytes;
+    a.out_frame_stride = out_bytes;
+    auto set_rows = [&](int y0, int y1) {
+        a.y_begin = y0;
+        a.y_end = y1;
+        a.y_lo = y0 > radius ? y0 : radius;
+        a.y_hi = y1 < h - radius ? y1 : h - radius;
+        if (a.y_hi < a.y_lo) a.y_hi = a.y_lo;
+    };
+
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    cudaError_t e = cudaSetDevice(ctx->device);
+    if (e != cudaSuccess) return cuda_error(e, "cudaSetDevice");
+
+    if (flags & OPC_FLAG_DEVICE_POINTERS) {
+        cudaStream_t s = cfg && cfg->stream ? static_cast<cudaStream_t>(cfg->stream) : ctx->stream;
+        a.in = in;
+        a.out = out;
+        a.frames = frames;
+        set_rows(y_begin, y_end);
+        return run_device(a, border, kernel, ctx, s);
+    }
+
+    // Host pointers: H2D / kernels / D2H pipelined over units (row chunks of
+    // a large image, or frames of a batch) on three streams, so PCIe traffic
+    // in both directions overlaps the filter.
+    const std::size_t tot_in = in_bytes * frames, tot_out = out_bytes * frames;
+    rc = ensure(&ctx->d_in, &ctx->in_cap, tot_in);
+    if (rc != OPC_OK) return rc;
+    rc = ensure(&ctx->d_out, &ctx->out_cap, tot_out);
+    if (rc != OPC_OK) return rc;
+    struct Unit {
+        int frame, y0, y1;
+    };
+    std::vector<Unit> units;
+    const int rows = y_end - y_begin;
+    if (frames == 1) {
+        const std::size_t chunk_target = 48ull << 20;
+        int n = static_cast<int>((in_bytes + chunk_target - 1) / chunk_target);
+        n = n < 1 ? 1 : (n > 16 ? 16 : n);
+        if (n > rows) n = rows;
+        for (int k = 0; k < n; ++k) {
+            units.push_back({0, y_begin + static_cast<int>(static_cast<long long>(rows) * k / n),
+                             y_begin + static_cast<int>(static_cast<long long>(rows) * (k + 1) / n)});
+        }
+    } else if (in_bytes >= (4ull << 20)) {
+        for (int f = 0; f < frames; ++f) units.push_back({f, y_begin, y_end});
+    } else {
+        units.push_back({-1, y_begin, y_end});  // whole batch in one launch
+    }
+    rc = ensure_streams(ctx, units.size());
+    if (rc != OPC_OK) return rc;
+    std::vector<int> loaded_hi(frames > 0 ? frames : 1, a.in_row0);
+    for (std::size_t u = 0; u < units.size(); ++u) {
+        const Unit& un = units[u];
+        const int f0 = un.frame < 0 ? 0 : un.frame;
+        const int nf = un.frame < 0 ? frames : 1;
+        // New input rows this unit needs beyond what earlier units loaded.
+        const int need_hi = opc_band_in_row0(h, un.y0, radius) +
+                            opc_band_in_rows(h, un.y0, un.y1, radius);
+        if (need_hi > loaded_hi[f0] || un.frame < 0) {
+            const int lo = un.frame < 0 ? a.in_row0 : loaded_hi[f0];
+            const std::size_t off = static_cast<std::size_t>(lo - a.in_row0) * row_bytes;
+            const std::size_t n = static_cast<std::size_t>(need_hi - lo) * row_bytes;
+            const std::size_t base = in_bytes * f0;
+            if (un.frame < 0) {
+                e = cudaMemcpyAsync(ctx->d_in, in, tot_in, cudaMemcpyHostToDevice, ctx->s_in);
+            } else {
+                e = cudaMemcpyAsync(static_cast<std::uint8_t*>(ctx->d_in) + base + off,
+                                    in + base + off, n, cudaMemcpyHostToDevice, ctx->s_in);
+            }
+            if (e != cudaSuccess) return cuda_error(e, "cudaMemcpyAsync(H2D)");
+            loaded_hi[f0] = need_hi;
+        }
+        e = cudaEventRecord(ctx->ev_in[u], ctx->s_in);
+        if (e != cudaSuccess) return cuda_error(e, "cudaEventRecord");
+        e = cudaStreamWaitEvent(ctx->stream, ctx->ev_in[u], 0);
+        if (e != cudaSuccess) return cuda_error(e, "cudaStreamWaitEvent");
+        a.in = static_cast<const std::uint8_t*>(ctx->d_in) + in_bytes * f0;
+        a.out = static_cast<std::uint8_t*>(ctx->d_out) + out_bytes * f0;
+        a.frames = nf;
+        set_rows(un.y0, un.y1);
+        rc = run_device(a, border, kernel, ctx, ctx->stream);
+        if (rc != OPC_OK) return rc;
+        e = cudaEventRecord(ctx->ev_out[u], ctx->stream);
+        if (e != cudaSuccess) return cuda_error(e, "cudaEventRecord");
+        e = cudaStreamWaitEvent(ctx->s_out, ctx->ev_out[u], 0);
+        if (e != cudaSuccess) return cuda_error(e, "cudaStreamWaitEvent");
+        const std::size_t ooff = out_bytes * f0 + static_cast<std::size_t>(un.y0 - y_begin) * row_bytes;
+        const std::size_t on = un.frame < 0 ? tot_out
+                                            : static_cast<std::size_t>(un.y1 - un.y0) * row_bytes;
+        e = cudaMemcpyAsync(out + ooff, static_cast<std::uint8_t*>(ctx->d_out) + ooff, on,
+                            cudaMemcpyDeviceToHost, ctx->s_out);
+        if (e != cudaSuccess) return cuda_error(e, "cudaMemcpyAsync(D2H)");
+    }
+    e = cudaStreamSynchronize(ctx->s_out);
+    if (e != cudaSuccess) return cuda_error(e, "cudaStreamSynchronize");
+    e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return cuda_error(e, "cudaStreamSynchronize");
+    return OPC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int opc_validate(int32_t width, int32_t height, uint64_t nbytes, int32_t radius, int32_t levels,
+                 uint32_t flags) {
+    return validate_params(width, height, nbytes, radius, levels, flags);
+}
+
+int opc_filter_rgb8(const uint8_t* in, uint8_t* out, int32_t width, int32_t height,
+                    int32_t radius, int32_t levels, int32_t border, const opc_config* cfg) {
+    return filter_core(in, out, 1, width, height, 0, height, radius, levels, border, cfg);
+}
+
+int opc_filter_rgb8_batch(const uint8_t* in, uint8_t* out, int32_t frames, int32_t width,
+                          int32_t height, int32_t radius, int32_t levels, int32_t border,
+                          const opc_config* cfg) {
+    return filter_core(in, out, frames, width, height, 0, height, radius, levels, border, cfg);
+}
+
+int opc_filter_rgb8_band(const uint8_t* in_rows, uint8_t* out_rows, int32_t width,
+                         int32_t height, int32_t y_begin, int32_t y_end, int32_t radius,
+                         int32_t levels, int32_t border, const opc_config* cfg) {
+    return filter_core(in_rows, out_rows, 1, width, height, y_begin, y_end, radius, levels, border,
+                       cfg);
+}
+
+int32_t opc_band_in_row0(int32_t height, int32_t y_begin, int32_t radius) {
+    (void)height;
+    const int32_t v = y_begin - radius;
+    return v > 0 ? v : 0;
+}
+
+int32_t opc_band_in_rows(int32_t height, int32_t y_begin, int32_t y_end, int32_t radius) {
+    const int32_t lo = opc_band_in_row0(height, y_begin, radius);
+    const int32_t hi = y_end + radius < height ? y_end + radius : height;
+    return hi - lo;
+}
+
+const char* opc_last_error(void) { return g_last_error.c_str(); }
+
+const char* opc_version(void) { return "oilpaint-b200 0.1.0 (sm_100a)"; }
+
+uint64_t opc_kernel_launches(void) { return g_launches.load(); }
+
+int32_t opc_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int opc_synchronize(const opc_config* cfg) {
+    DevCtx* ctx = nullptr;
+    int rc = get_ctx(cfg ? cfg->device : -1, &ctx);
+    if (rc != OPC_OK) return rc;
+    cudaError_t e = cudaSetDevice(ctx->device);
+    if (e != cudaSuccess) return cuda_error(e, "cudaSetDevice");
+    cudaStream_t s = cfg && cfg->stream ? static_cast<cudaStream_t>(cfg->stream) : ctx->stream;
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_error(e, "cudaStreamSynchronize");
+    return OPC_OK;
+}
+
+int32_t opc_plan_kernel(int32_t width, int32_t height, int32_t radius, int32_t levels) {
+    if (validate_params(width, height, 3ull * width * height, radius, levels,
+                        OPC_FLAG_ALLOW_LEVELS_256) != OPC_OK) {
+        return -1;
+    }
+    return plan(levels, radius, 0);
+}
+
+void opc_release(void) {
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    for (auto& c : g_ctx) {
+        if (!c) continue;
+        std::lock_guard<std::mutex> lk2(c->mu);
+        cudaSetDevice(c->device);
+        if (c->d_in) cudaFree(c->d_in);
+        if (c->d_out) cudaFree(c->d_out);
+        if (c->d_counter) cudaFree(c->d_counter);
+        if (c->stream) cudaStreamDestroy(c->stream);
+        if (c->s_in) cudaStreamDestroy(c->s_in);
+        if (c->s_out) cudaStreamDestroy(c->s_out);
+        for (cudaEvent_t ev : c->ev_in) cudaEventDestroy(ev);
+        for (cudaEvent_t ev : c->ev_out) cudaEventDestroy(ev);
+        c.reset();
+    }
+    g_ctx.clear();
+}
+
+}  // extern "C"

@@ -1,0 +1,170 @@
+// direct.cu -- the generic kernel family (any radius, any L <= 256) and the
+// border kernel.
+//
+// DIRECT: one thread per interior output pixel, the reference's O((2r+1)^2)
+// scan restated for the GPU (proj/src/filter.cpp:28-44):
+//   pass 1  per-bin counts in shared memory ([bin][thread] layout, so the
+//           dynamic-bin increments of a warp hit 32 distinct banks);
+//   argmax  lowest index with the strictly largest count (filter.hpp:71-82);
+//   pass 2  channel sums of the winning bin only, in registers (u64), then the
+//           truncating quotient (filter.cpp:41-43).
+// It is the correctness backstop for shapes the fast families do not cover
+// (r > 15, or L+1 > 32 at r > 15) and the kernel the tests force to cross-check
+// the fast families.
+#include "kernels.cuh"
+
+namespace opc {
+
+namespace {
+
+constexpr int kDirectThreads = 64;
+
+__device__ __forceinline__ unsigned bin_of(unsigned s, int levels, std::uint32_t bin_mul) {
+    // filter.hpp:31-35: (r+g+b) * L / 765 in unsigned arithmetic.
+    return bin_mul ? __umulhi(s, bin_mul) : (s * static_cast<unsigned>(levels)) / 765u;
+}
+
+__global__ void __launch_bounds__(kDirectThreads)
+    direct_kernel(BandArgs a, long long pixels_per_frame) {
+    extern __shared__ std::uint32_t counts[];  // [bins][kDirectThreads]
+    const int tid = threadIdx.x;
+    const long long idx = static_cast<long long>(blockIdx.x) * kDirectThreads + tid;
+    const int frame = blockIdx.y;
+    if (idx >= pixels_per_frame) return;
+    const int iw = a.x_hi - a.x_lo;
+    const int y = a.y_lo + static_cast<int>(idx / iw);
+    const int x = a.x_lo + static_cast<int>(idx % iw);
+    const int r = a.radius;
+    const int bins = a.levels + 1;
+    const std::size_t stride = static_cast<std::size_t>(a.width) * 3;
+    const std::uint8_t* in = a.in + a.in_frame_stride * frame;
+    std::uint8_t* out = a.out + a.out_frame_stride * frame;
+
+    for (int b = 0; b < bins; ++b) counts[b * kDirectThreads + tid] = 0;
+    for (int ny = y - r; ny <= y + r; ++ny) {
+        const std::uint8_t* p = in + static_cast<std::size_t>(ny - a.in_row0) * stride +
+                                static_cast<std::size_t>(x - r) * 3;
+        for (int i = 0; i <= 2 * r; ++i, p += 3) {
+            const unsigned b = bin_of(unsigned(p[0]) + p[1] + p[2], a.levels, a.bin_mul);
+            counts[b * kDirectThreads + tid] += 1;
+        }
+    }
+    int best = 0;
+    std::uint32_t best_count = counts[tid];
+    for (int b = 1; b < bins; ++b) {
+        const std::uint32_t c = counts[b * kDirectThreads + tid];
+        if (c > best_count) {  // strict '>' keeps the lowest index on ties
+            best_count = c;
+            best = b;
+        }
+    }
+    unsigned long long sr = 0, sg = 0, sb = 0;
+    for (int ny = y - r; ny <= y + r; ++ny) {
+        const std::uint8_t* p = in + static_cast<std::size_t>(ny - a.in_row0) * stride +
+                                static_cast<std::size_t>(x - r) * 3;
+        for (int i = 0; i <= 2 * r; ++i, p += 3) {
+            const unsigned b = bin_of(unsigned(p[0]) + p[1] + p[2], a.levels, a.bin_mul);
+            if (b == static_cast<unsigned>(best)) {
+                sr += p[0];
+                sg += p[1];
+                sb += p[2];
+            }
+        }
+    }
+    std::uint8_t* o = out + static_cast<std::size_t>(y - a.out_row0) * stride +
+                      static_cast<std::size_t>(x) * 3;
+    o[0] = static_cast<std::uint8_t>(sr / best_count);
+    o[1] = static_cast<std::uint8_t>(sg / best_count);
+    o[2] = static_cast<std::uint8_t>(sb / best_count);
+}
+
+// Border pixels of the output band (filter.cpp:54 / parallel.cpp:113):
+// CopyInput copies the input bytes, ZeroFill writes zeros.  The flat byte
+// index space is [full border rows][left+right strips of interior rows].
+__global__ void border_kernel(BandArgs a, int policy, long long full_bytes, long long strip_bytes,
+                              int top_rows, int first_full_top, int first_full_bottom) {
+    const long long per_frame = full_bytes + strip_bytes;
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int frame = blockIdx.y;
+    if (i >= per_frame) return;
+    const long long row_bytes = static_cast<long long>(a.width) * 3;
+    int y;
+    long long col_byte;
+    if (i < full_bytes) {
+        const long long row = i / row_bytes;
+        col_byte = i % row_bytes;
+        y = row < top_rows ? first_full_top + static_cast<int>(row)
+                           : first_full_bottom + static_cast<int>(row - top_rows);
+    } else {
+        const long long j = i - full_bytes;
+        const long long side = static_cast<long long>(a.radius) * 3;
+        const long long per_row = 2 * side;
+        y = a.y_lo + static_cast<int>(j / per_row);
+        const long long k = j % per_row;
+        col_byte = k < side ? k : row_bytes - per_row + k;
+    }
+    std::uint8_t v = 0;
+    if (policy == 0) {
+        v = a.in[a.in_frame_stride * frame + static_cast<std::size_t>(y - a.in_row0) * row_bytes +
+                 col_byte];
+    }
+    a.out[a.out_frame_stride * frame + static_cast<std::size_t>(y - a.out_row0) * row_bytes +
+          col_byte] = v;
+}
+
+}  // namespace
+
+std::uint32_t bin_multiplier(int levels) {
+    // Smallest-error magic for floor(s*L/765) over s in [0, 765]; verified
+    // exhaustively, else 0 (kernels then divide).
+    if (levels < 1 || levels > 256) return 0;
+    const unsigned long long base =
+        ((static_cast<unsigned long long>(levels) << 32) + 764ull) / 765ull;
+    for (unsigned long long c = base; c < base + 4 && c <= 0xFFFFFFFFull; ++c) {
+        bool ok = true;
+        for (unsigned s = 0; s <= 765 && ok; ++s) {
+            const unsigned want = s * static_cast<unsigned>(levels) / 765u;
+            const unsigned got = static_cast<unsigned>((s * c) >> 32);
+            ok = want == got;
+        }
+        if (ok) return static_cast<std::uint32_t>(c);
+    }
+    return 0;
+}
+
+cudaError_t launch_direct(const BandArgs& a, cudaStream_t s) {
+    if (a.y_hi <= a.y_lo || a.x_hi <= a.x_lo || a.frames <= 0) return cudaSuccess;
+    const long long pixels = static_cast<long long>(a.y_hi - a.y_lo) * (a.x_hi - a.x_lo);
+    const std::size_t smem =
+        static_cast<std::size_t>(a.levels + 1) * kDirectThreads * sizeof(std::uint32_t);
+    cudaError_t e = cudaFuncSetAttribute(direct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    const dim3 grid(static_cast<unsigned>((pixels + kDirectThreads - 1) / kDirectThreads),
+                    static_cast<unsigned>(a.frames));
+    direct_kernel<<<grid, kDirectThreads, smem, s>>>(a, pixels);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_border(const BandArgs& a, int policy, cudaStream_t s) {
+    // Full border rows inside this band's output rows.
+    const int out_lo = a.y_begin, out_hi = a.y_end;
+    const int top_lo = out_lo, top_hi = out_hi < a.radius ? out_hi : a.radius;
+    const int top_rows = top_hi > top_lo ? top_hi - top_lo : 0;
+    const int bot_lo = out_lo > a.height - a.radius ? out_lo : a.height - a.radius;
+    const int bot_rows = out_hi > bot_lo ? out_hi - bot_lo : 0;
+    const long long row_bytes = static_cast<long long>(a.width) * 3;
+    const long long full_bytes = static_cast<long long>(top_rows + bot_rows) * row_bytes;
+    const int mid_rows = a.y_hi > a.y_lo ? a.y_hi - a.y_lo : 0;
+    const long long strip_bytes = static_cast<long long>(mid_rows) * 2 * a.radius * 3;
+    const long long per_frame = full_bytes + strip_bytes;
+    if (per_frame <= 0 || a.frames <= 0) return cudaSuccess;
+    const int threads = 256;
+    const dim3 grid(static_cast<unsigned>((per_frame + threads - 1) / threads),
+                    static_cast<unsigned>(a.frames));
+    border_kernel<<<grid, threads, 0, s>>>(a, policy, full_bytes, strip_bytes, top_rows, top_lo,
+                                           bot_lo);
+    return cudaGetLastError();
+}
+
+}  // namespace opc

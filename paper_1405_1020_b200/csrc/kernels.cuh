@@ -1,0 +1,52 @@
+// kernels.cuh -- device-side declarations shared by the kernel families and
+// the C-ABI host code.  All kernels follow the reference semantics of
+// proj/include/oilpaint/filter.hpp:31-105 and proj/src/filter.cpp:28-68.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace opc {
+
+// One launch produces output rows [y_begin, y_end) of `frames` frames of a
+// width x height image.  Input buffer row 0 is image row in_row0 and holds
+// in_rows rows; output buffer row 0 is image row out_row0.  Interior rows
+// [y_lo, y_hi) (= [y_begin, y_end) clipped to [r, H-r)) and columns
+// [x_lo, x_hi) are computed by the filter kernels; the border pixels of rows
+// [y_begin, y_end) are written by the border kernel.
+struct BandArgs {
+    const std::uint8_t* in;
+    std::uint8_t* out;
+    std::size_t in_frame_stride;   // bytes between frames in `in`
+    std::size_t out_frame_stride;  // bytes between frames in `out`
+    int frames;
+    int width;
+    int height;  // full image height (global border rows)
+    int in_row0;
+    int in_rows;
+    int out_row0;
+    int y_begin, y_end;  // output rows this launch produces
+    int y_lo, y_hi;  // interior rows of this band (may be empty)
+    int x_lo, x_hi;  // interior columns [r, W - r)
+    int radius;
+    int levels;
+    std::uint32_t bin_mul;  // bin = umulhi(r+g+b, bin_mul) == (r+g+b)*L/765
+};
+
+// Exact magic multiplier for floor(s * L / 765), s in [0, 765], L in [1, 256];
+// 0 if none exists (host falls back to the generic division path).
+std::uint32_t bin_multiplier(int levels);
+
+// ---- kernel families (each returns cudaError_t of the launch) ----
+cudaError_t launch_direct(const BandArgs& a, cudaStream_t s);
+cudaError_t launch_border(const BandArgs& a, int border_policy, cudaStream_t s);
+
+// Skew family: L + 1 <= 32, radius <= 15.  `task_counter` is a device int
+// (zeroed by the launcher on the stream).
+bool skew_supported(int levels, int radius);
+std::size_t skew_smem_bytes(int levels, int radius);
+cudaError_t launch_skew(const BandArgs& a, int* task_counter, int num_sms, cudaStream_t s);
+
+}  // namespace opc

@@ -1,0 +1,229 @@
+"""GPU parity suite: the CUDA product path through the C-ABI vs the oracle.
+
+Mirrors the reference's own tests:
+  * acceptance criterion 1 (proj/tests/acceptance.cpp:44-67) -- 1000 random
+    small cases vs the brute-force oracle, bit exact;
+  * criterion 2 (acceptance.cpp:71-101) -- 200 cases up to 128x128, r <= 5;
+  * criterion 6 / test_filter.cpp:205-211 -- the golden 8x8 gradient PPM;
+  * test_filter.cpp known answers, invariants, border policy, validation;
+  * test_parallel.cpp's partition checks, with GPU row bands in place of worker
+    chunks (every output row produced exactly once, bands == whole image).
+Every kernel family is also forced on every case it accepts.
+"""
+from __future__ import annotations
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle_lib
+from test_oracle import load_cases, ppm_payload
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+AUTO, DIRECT, SKEW = 0, 1, 2
+
+
+def run(opc, img, r, L, border=0, kernel=AUTO, allow256=False):
+    cfg = opc.CudaConfig(kernel=kernel, allow_levels_256=allow256)
+    return opc.apply_cuda(img, opc.FilterParams(r, L, opc.BorderPolicy(border)), cfg)
+
+
+def skew_ok(r, L):
+    return L + 1 <= 32 and r <= 15
+
+
+def test_reference_fixture_cases_all_kernels(gpu):
+    n = 0
+    for w, h, r, L, border, src, img, want in load_cases():
+        allow = L == 256
+        assert np.array_equal(run(gpu, img, r, L, border, AUTO, allow), want), (w, h, r, L, border)
+        assert np.array_equal(run(gpu, img, r, L, border, DIRECT, allow), want), (w, h, r, L)
+        if skew_ok(r, L):
+            assert np.array_equal(run(gpu, img, r, L, border, SKEW), want), (w, h, r, L, border)
+        n += 1
+    assert n == 296
+
+
+def test_golden_ppm(gpu):
+    _, _, golden = ppm_payload(GOLDEN / "gradient8_r2_l20_zero.ppm")
+    img = gpu.generate(gpu.Pattern.GRADIENT, 8, 8)
+    for k in (AUTO, DIRECT, SKEW):
+        assert np.array_equal(run(gpu, img, 2, 20, 1, k), golden)
+
+
+def test_criterion1_random_small_vs_oracle(gpu):
+    rng = np.random.default_rng(101)
+    for i in range(1000):
+        w, h = int(rng.integers(1, 17)), int(rng.integers(1, 17))
+        r = int(rng.integers(0, min(3, (min(w, h) - 1) // 2) + 1))
+        L = int(rng.choice([1, 10, 20, 255]))
+        b = int(rng.integers(0, 2))
+        img = rng.integers(0, 256, (h, w, 3), dtype=np.uint8)
+        want = oracle_lib.oracle_filter(img, r, L, b)
+        assert np.array_equal(run(gpu, img, r, L, b), want), (i, w, h, r, L, b)
+
+
+def test_criterion2_random_medium_vs_oracle(gpu):
+    rng = np.random.default_rng(202)
+    for i in range(200):
+        w, h = int(rng.integers(1, 129)), int(rng.integers(1, 129))
+        r = int(rng.integers(0, min(5, (min(w, h) - 1) // 2) + 1))
+        L = int(rng.choice([1, 20, 30, 255]))
+        b = int(rng.integers(0, 2))
+        img = rng.integers(0, 256, (h, w, 3), dtype=np.uint8)
+        want = oracle_lib.oracle_filter(img, r, L, b, threads=4)
+        assert np.array_equal(run(gpu, img, r, L, b), want), (i, w, h, r, L, b)
+        if skew_ok(r, L):
+            assert np.array_equal(run(gpu, img, r, L, b, SKEW), want), (i, w, h, r, L, b)
+
+
+@pytest.mark.parametrize("r", [0, 1, 2, 5, 7, 10, 14, 15])
+@pytest.mark.parametrize("L", [1, 2, 7, 11, 20, 23, 30, 31])
+def test_skew_radius_levels_grid(gpu, r, L):
+    rng = np.random.default_rng(r * 100 + L)
+    h = 2 * r + 1 + int(rng.integers(0, 70))
+    w = 2 * r + 1 + int(rng.integers(0, 300))
+    img = rng.integers(0, 256, (h, w, 3), dtype=np.uint8)
+    want = oracle_lib.oracle_filter(img, r, L, 0, threads=4)
+    assert np.array_equal(run(gpu, img, r, L, 0, SKEW), want)
+
+
+@pytest.mark.parametrize("content", ["flat", "smooth", "two_tone", "white"])
+def test_skew_tie_heavy_content(gpu, content):
+    """Smooth / flat content: single-bin windows, many exact ties, bin L (white)."""
+    rng = np.random.default_rng(7)
+    h, w = 97, 211
+    if content == "flat":
+        img = np.full((h, w, 3), 77, np.uint8)
+    elif content == "smooth":
+        base = rng.integers(0, 256, 3)
+        img = np.clip(base + rng.integers(-10, 11, (h, w, 3)), 0, 255).astype(np.uint8)
+    elif content == "two_tone":
+        img = np.where(rng.random((h, w, 1)) < 0.5, 40, 200).astype(np.uint8).repeat(3, 2)
+    else:
+        img = np.where(rng.random((h, w, 1)) < 0.5, 255, 254).astype(np.uint8).repeat(3, 2)
+    for r, L in ((3, 20), (7, 30), (15, 20), (2, 1)):
+        want = oracle_lib.oracle_filter(img, r, L, 0, threads=4)
+        assert np.array_equal(run(gpu, img, r, L, 0, SKEW), want), (content, r, L)
+        assert np.array_equal(run(gpu, img, r, L, 0, DIRECT), want), (content, r, L)
+
+
+def test_large_radius_and_l256(gpu):
+    rng = np.random.default_rng(9)
+    for r, L in ((16, 20), (20, 5), (31, 255), (12, 256), (3, 256)):
+        h, w = 2 * r + 1 + 17, 2 * r + 1 + 29
+        img = rng.integers(0, 256, (h, w, 3), dtype=np.uint8)
+        want = oracle_lib.oracle_filter(img, r, L, 1)
+        assert np.array_equal(run(gpu, img, r, L, 1, AUTO, L == 256), want), (r, L)
+
+
+def test_edge_shapes(gpu):
+    rng = np.random.default_rng(11)
+    img = np.array([[[42, 43, 44]]], np.uint8)  # test_parallel.cpp:142-145
+    for b in (0, 1):
+        assert np.array_equal(run(gpu, img, 0, 20, b), img)
+    for (h, w, r) in ((5, 9, 0), (3, 1000, 1), (1000, 3, 1), (31, 31, 15), (33, 257, 15),
+                      (64, 129, 15), (40, 1, 0), (2, 2, 0)):
+        img = rng.integers(0, 256, (h, w, 3), dtype=np.uint8)
+        for L in (1, 20, 255):
+            for b in (0, 1):
+                want = oracle_lib.oracle_filter(img, r, L, b)
+                assert np.array_equal(run(gpu, img, r, L, b), want), (h, w, r, L, b)
+
+
+def test_identity_uniform_and_border_policy(gpu):
+    rng = np.random.default_rng(3)
+    img = rng.integers(0, 256, (5, 9, 3), dtype=np.uint8)
+    for b in (0, 1):  # test_filter.cpp:192-198: r=0 is the identity
+        assert np.array_equal(run(gpu, img, 0, 20, b), img)
+    uni = np.empty((9, 12, 3), np.uint8)
+    uni[:] = (17, 170, 71)  # test_filter.cpp:200-203
+    assert np.array_equal(run(gpu, uni, 2, 20, 0), uni)
+    img = rng.integers(0, 256, (8, 10, 3), dtype=np.uint8)  # test_filter.cpp:213-233
+    z, c = run(gpu, img, 2, 20, 1), run(gpu, img, 2, 20, 0)
+    inner = np.zeros((8, 10), bool)
+    inner[2:6, 2:8] = True
+    assert np.array_equal(z[inner], c[inner])
+    assert (z[~inner] == 0).all() and np.array_equal(c[~inner], img[~inner])
+
+
+def test_output_within_neighbourhood_extremes(gpu):
+    rng = np.random.default_rng(5)  # test_filter.cpp:235-266
+    for _ in range(20):
+        h, w = int(rng.integers(3, 40)), int(rng.integers(3, 40))
+        r = int(rng.integers(1, max(1, min(3, (min(h, w) - 1) // 2)) + 1))
+        L = int(rng.integers(1, 256))
+        img = rng.integers(0, 256, (h, w, 3), dtype=np.uint8)
+        out = run(gpu, img, r, L)
+        for y in range(r, h - r):
+            for x in range(r, w - r):
+                win = img[y - r:y + r + 1, x - r:x + r + 1].reshape(-1, 3)
+                assert (out[y, x] >= win.min(0)).all() and (out[y, x] <= win.max(0)).all()
+
+
+def test_validation_errors(gpu):
+    img = np.zeros((8, 8, 3), np.uint8)  # test_filter.cpp:293-304
+    P = gpu.FilterParams
+    for p in (P(4, 20), P(-1, 20), P(1, 0), P(1, 256)):
+        with pytest.raises(gpu.InvalidArgument):
+            gpu.apply_cuda(img, p)
+    gpu.apply_cuda(np.zeros((1, 1, 3), np.uint8), P(0, 20))
+    gpu.apply_cuda(img, P(3, 20))
+    with pytest.raises(gpu.InvalidArgument, match="intensity_levels must be in"):
+        gpu.apply_cuda(img, P(1, 257), gpu.CudaConfig(allow_levels_256=True))
+    with pytest.raises(gpu.InvalidArgument):  # forcing SKEW beyond its r <= 15 range
+        gpu.apply_cuda(np.zeros((40, 40, 3), np.uint8), P(16, 20), gpu.CudaConfig(kernel=SKEW))
+
+
+def test_bands_reassemble_whole_image(gpu):
+    """Row bands with r-row halos (multi-GPU partition) == whole-image result,
+    every output row covered exactly once (test_parallel.cpp:65-103 analogue)."""
+    rng = np.random.default_rng(12)
+    h, w = 301, 173
+    img = rng.integers(0, 256, (h, w, 3), dtype=np.uint8)
+    for r, L, b in ((15, 20, 0), (7, 30, 1), (2, 255, 0), (0, 20, 1)):
+        whole = run(gpu, img, r, L, b)
+        assert np.array_equal(whole, oracle_lib.oracle_filter(img, r, L, b, threads=4))
+        for n in (1, 2, 3, 8, 13):
+            cuts = [h * k // n for k in range(n + 1)]
+            parts = []
+            for y0, y1 in zip(cuts[:-1], cuts[1:]):
+                lo, hi = gpu.band_input_rows(h, y0, y1, r)
+                parts.append(gpu.apply_cuda_band(img[lo:hi], h, y0, y1,
+                                                 gpu.FilterParams(r, L, gpu.BorderPolicy(b))))
+            assert sum(p.shape[0] for p in parts) == h
+            assert np.array_equal(np.concatenate(parts), whole), (r, L, b, n)
+
+
+def test_batch_equals_per_frame(gpu):
+    rng = np.random.default_rng(13)
+    frames = rng.integers(0, 256, (5, 67, 91, 3), dtype=np.uint8)
+    p = gpu.FilterParams(7, 30)
+    out = gpu.apply_cuda_batch(frames, p)
+    for f in range(5):
+        assert np.array_equal(out[f], oracle_lib.oracle_filter(frames[f], 7, 30))
+
+
+def test_device_pointer_path_with_torch_stream(gpu):
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(14)
+    img = rng.integers(0, 256, (130, 250, 3), dtype=np.uint8)
+    want = oracle_lib.oracle_filter(img, 15, 20)
+    dev_in = torch.from_numpy(img).cuda()
+    dev_out = torch.empty_like(dev_in)
+    stream = torch.cuda.Stream()
+    cfg = gpu.CudaConfig(device=dev_in.device.index, stream=stream.cuda_stream)
+    with torch.cuda.stream(stream):
+        gpu.apply_cuda_device(dev_in.data_ptr(), dev_out.data_ptr(), 250, 130,
+                              gpu.FilterParams(15, 20), cfg)
+    stream.synchronize()
+    assert np.array_equal(dev_out.cpu().numpy(), want)
+
+
+def test_launch_counter_advances(gpu):
+    before = gpu.kernel_launches()
+    run(gpu, np.zeros((40, 40, 3), np.uint8), 3, 20)
+    assert gpu.kernel_launches() >= before + 2  # filter kernel + border kernel
