@@ -66,6 +66,8 @@ struct DevCtx {
     std::size_t in_cap = 0;
     void* d_out = nullptr;
     std::size_t out_cap = 0;
+    void* d_scratch = nullptr;  // skew family: sheared entry plane
+    std::size_t scratch_cap = 0;
     int* d_counter = nullptr;
     unsigned counter_idx = 0;
     cudaStream_t s_in = nullptr;   // H2D copies
@@ -157,13 +159,15 @@ int run_device(const opc::BandArgs& a, int border, int kernel, DevCtx* ctx, cuda
         // Rotate over 64 task counters so kernels in flight on different
         // streams never share one.
         int* counter = ctx->d_counter + (ctx->counter_idx++ & 63u);
-        e = opc::launch_skew(a, counter, ctx->num_sms, s);
+        const int rc = ensure(&ctx->d_scratch, &ctx->scratch_cap, opc::skew_scratch_bytes(a));
+        if (rc != OPC_OK) return rc;
+        e = opc::launch_skew(a, counter, ctx->d_scratch, ctx->num_sms, s);
         if (e != cudaSuccess) return cuda_error(e, "skew kernel launch");
     } else {
         e = opc::launch_direct(a, s);
         if (e != cudaSuccess) return cuda_error(e, "direct kernel launch");
     }
-    if (a.y_hi > a.y_lo && a.x_hi > a.x_lo) g_launches.fetch_add(1);
+    if (a.y_hi > a.y_lo && a.x_hi > a.x_lo) g_launches.fetch_add(kernel == OPC_KERNEL_SKEW ? 2 : 1);
     e = opc::launch_border(a, border, s);
     if (e != cudaSuccess) return cuda_error(e, "border kernel launch");
     if (a.radius > 0) g_launches.fetch_add(1);
@@ -396,6 +400,7 @@ void opc_release(void) {
         cudaSetDevice(c->device);
         if (c->d_in) cudaFree(c->d_in);
         if (c->d_out) cudaFree(c->d_out);
+        if (c->d_scratch) cudaFree(c->d_scratch);
         if (c->d_counter) cudaFree(c->d_counter);
         if (c->stream) cudaStreamDestroy(c->stream);
         if (c->s_in) cudaStreamDestroy(c->s_in);

@@ -45,8 +45,11 @@ cudaError_t launch_border(const BandArgs& a, int border_policy, cudaStream_t s);
 
 // Skew family: L + 1 <= 32, radius <= 15.  `task_counter` is a device int
 // (zeroed by the launcher on the stream).
+// Skew family also needs device scratch (the sheared entry plane) of
+// skew_scratch_bytes(a) bytes.
 bool skew_supported(int levels, int radius);
-std::size_t skew_smem_bytes(int levels, int radius);
-cudaError_t launch_skew(const BandArgs& a, int* task_counter, int num_sms, cudaStream_t s);
+std::size_t skew_scratch_bytes(const BandArgs& a);
+cudaError_t launch_skew(const BandArgs& a, int* task_counter, void* scratch, int num_sms,
+                        cudaStream_t s);
 
 }  // namespace opc

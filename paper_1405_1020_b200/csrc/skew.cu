@@ -2,7 +2,7 @@
 //
 // Algorithm: column-difference sliding window, one output ROW per lane, the 32
 // lanes of a warp skewed by one column each (lane t works on virtual column
-// v = s - t at step s).  See DESIGN.md section 3 for the derivation; in short:
+// v = s - t at step s).  DESIGN.md section 3 has the derivation; in short:
 //
 //  * The window histogram of lane t (row y) lives in registers as NB packed
 //    64-bit words  [count:10 | sumR:18 | sumG:18 | sumB:18]  (exact for
@@ -10,43 +10,65 @@
 //    every window total fits its field).
 //  * Sliding right:  W(x+1,y) = W(x,y) + E(x,y),
 //        E(x,y) = Col(x+r+1,y) - Col(x-r,y)   (Col = 2r+1-row column histogram).
-//    E slots live in shared memory, [bin][slot] layout.
+//    E slots live in shared memory, [bin][slot] layout (conflict-free: lanes
+//    always touch distinct slots, the dynamic bin only selects the row).
 //  * E(x,y+1) = E(x,y) + f(x+r+1,y+r+1) - f(x+r+1,y-r) - f(x-r,y+r+1) + f(x-r,y-r)
 //    -- four dynamic-bin updates.  Lane t reads E(x,y) at step s and advances it
-//    to row y+1; lane t+1 consumes it at step s+1 (same column, next row).  The
-//    skew is what turns the vertical recurrence into a conflict-free pipeline.
-//  * E(x, band top) is built from scratch (2(2r+1) updates per column) one
-//    phase (32 steps) ahead, one column per lane.
+//    to row y+1; lane t+1 consumes it at step s+1.  The skew turns the vertical
+//    recurrence into a pipeline across the lanes.
+//  * E(x, band top) is built from scratch (2(2r+1) updates per column), the
+//    lane of column vi working on row k = (s - t) mod 32 at step s, which
+//    finishes each column exactly one step before lane 0 first reads it.
+//  * Pixels come from a SHEARED entry plane S[d = x + y][y] written by
+//    shear_kernel (u32 = R | G<<8 | B<<16 | bin<<24): every pixel a warp needs
+//    at step s lies on one of six anti-diagonals, 32 consecutive rows each, so
+//    every access is a single coalesced 128-byte load.
 //  * Argmax: a static tournament over the NB words comparing counts only
 //    (hi word > other.hi | 0x3FFFFF <=> strictly larger count), left (lower
 //    bin) operand kept on ties -> lowest-index maximum, filter.hpp:71-82.
 //  * Quotient: q = umulhi(2*sum, floor(2^31/c)+1), exact for c <= 1023,
 //    sum <= 255c (tests/test_oracle.py checks it exhaustively); filter.cpp:41-43.
-//
-// Memory: per warp a pixel ring (33+2r rows x 128 columns, 4 B per pixel:
-// R,G,B,bin), the E ring (96 slots x NB x 8 B) and a 32x32 output staging tile
-// that is flushed one completed row-block per step as coalesced 96-byte runs.
+//  * Output: a 32x32 staging tile; each step one row completes a 32-pixel
+//    block, written as one coalesced 96-byte run.
 #include "kernels.cuh"
 
 namespace opc {
 
 namespace {
 
-constexpr int kMaxWarps = 4;
-constexpr int kRing = 128;
-constexpr int kRingStride = kRing + 2;  // == 2 (mod 32): skewed accesses hit distinct banks
+constexpr int kMaxWarps = 8;
 constexpr int kSlots = 96;
 constexpr int kStageStride = 33;
 constexpr int kRecipBytes = 1024 * 4;
+constexpr int kShearRows = 32;
+constexpr int kShearCols = 128;
+constexpr int kShearStride = kShearCols + 2;  // == 2 (mod 32): diagonal reads conflict-free
+// Zero entries are written for columns [W, W + kShearPad): the E column past
+// the last output column reads column W, and a zero entry keeps its bin in
+// range (its value is never used for an output pixel).
+constexpr int kShearPad = 32;
 
-__host__ __device__ inline int ring_rows(int r) { return 33 + 2 * r; }
-
-__host__ __device__ inline std::size_t ring_bytes(int r) {
-    return static_cast<std::size_t>(ring_rows(r)) * kRingStride * 4;
+__host__ __device__ inline std::size_t per_warp_bytes(int nb) {
+    return static_cast<std::size_t>(nb) * kSlots * 8 + 32 * kStageStride * 4;
 }
 
-__host__ __device__ inline std::size_t per_warp_bytes(int nb, int r) {
-    return ring_bytes(r) + static_cast<std::size_t>(nb) * kSlots * 8 + 32 * kStageStride * 4;
+// Geometry of the sheared plane for a launch: rows [y_base, y_base + Hs) of
+// the image, diagonal d = x + (y - y_base), element (d, y) at d * Hs + (y - y_base).
+struct ShearGeom {
+    int y_base;
+    int Hs;       // multiple of 32
+    int ndiag;    // W + kShearPad + Hs
+    std::size_t frame_elems;
+};
+
+__host__ inline ShearGeom shear_geom(const BandArgs& a) {
+    ShearGeom g{};
+    g.y_base = a.y_lo - a.radius;
+    const int nbands = (a.y_hi - a.y_lo + 31) / 32;
+    g.Hs = 32 * nbands + 64;
+    g.ndiag = a.width + kShearPad + g.Hs;
+    g.frame_elems = static_cast<std::size_t>(g.ndiag) * g.Hs;
+    return g;
 }
 
 __device__ __forceinline__ std::uint32_t make_entry(std::uint32_t r, std::uint32_t g,
@@ -55,7 +77,48 @@ __device__ __forceinline__ std::uint32_t make_entry(std::uint32_t r, std::uint32
     return r | (g << 8) | (b << 16) | (bin << 24);
 }
 
-// Packed single-pixel contribution (count 1, R, G, B) of a ring entry.
+// Sheared entry plane.  Block: 32 rows x 128 columns staged through shared
+// memory, then written diagonal by diagonal (lane = row -> contiguous).
+__global__ void __launch_bounds__(256) shear_kernel(BandArgs a, std::uint32_t* S, ShearGeom g) {
+    __shared__ std::uint32_t tile[kShearRows * kShearStride];
+    const int x0 = blockIdx.x * kShearCols;
+    const int y0 = g.y_base + blockIdx.y * kShearRows;
+    const int frame = blockIdx.z;
+    const std::uint8_t* in = a.in + a.in_frame_stride * frame;
+    std::uint32_t* Sf = S + g.frame_elems * frame;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const std::size_t stride = static_cast<std::size_t>(a.width) * 3;
+    const int in_hi = a.in_row0 + a.in_rows;
+#pragma unroll
+    for (int k = 0; k < kShearRows / 8; ++k) {
+        const int row = warp + 8 * k;
+        const int y = y0 + row;
+#pragma unroll
+        for (int j = 0; j < kShearCols / 32; ++j) {
+            const int c = lane + 32 * j;
+            const int x = x0 + c;
+            std::uint32_t e = 0;
+            if (x < a.width && y < in_hi) {
+                const std::uint8_t* p = in + static_cast<std::size_t>(y - a.in_row0) * stride +
+                                        static_cast<std::size_t>(x) * 3;
+                e = make_entry(p[0], p[1], p[2], a.bin_mul);
+            }
+            tile[row * kShearStride + c] = e;
+        }
+    }
+    __syncthreads();
+    const int ymax = g.y_base + g.Hs;
+    for (int dd = warp; dd < kShearCols + kShearRows - 1; dd += 8) {
+        const int c = dd - lane;
+        const int x = x0 + c, y = y0 + lane;
+        if (c >= 0 && c < kShearCols && x < a.width + kShearPad && y < ymax) {
+            const std::size_t d = static_cast<std::size_t>(x + (y - g.y_base));
+            Sf[d * g.Hs + (y - g.y_base)] = tile[lane * kShearStride + c];
+        }
+    }
+}
+
+// Packed single-pixel contribution (count 1, R, G, B) of an entry.
 __device__ __forceinline__ unsigned long long packed_of(std::uint32_t e) {
     const std::uint32_t lo = ((e >> 16) & 0xFFu) | ((e & 0xFF00u) << 10);  // B | G << 18
     const std::uint32_t hi = ((e & 0xFFu) << 4) | 0x400000u;                // R << 36, 1 << 54
@@ -104,21 +167,23 @@ struct TaskGeom {
     int nbands, nsegs, segw, ntasks;
 };
 
+struct Loads {
+    std::uint32_t a, b, c, d, i1, i2;
+};
+
 template <int NB>
-__global__ void __launch_bounds__(kMaxWarps * 32, 1)
-    skew_kernel(BandArgs a, int* task_counter, TaskGeom g) {
+__global__ void __launch_bounds__(kMaxWarps * 32)
+    skew_kernel(BandArgs a, const std::uint32_t* __restrict__ S, ShearGeom sg, int* task_counter,
+                TaskGeom g) {
     extern __shared__ __align__(16) unsigned char smem[];
     std::uint32_t* recip = reinterpret_cast<std::uint32_t*>(smem);
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int r = a.radius;
     const int w2 = 2 * r + 1;
-    const int rows = ring_rows(r);
-    unsigned char* wbase = smem + kRecipBytes + warp * per_warp_bytes(NB, r);
-    std::uint32_t* ring = reinterpret_cast<std::uint32_t*>(wbase);
-    unsigned long long* E = reinterpret_cast<unsigned long long*>(wbase + ring_bytes(r));
-    std::uint32_t* stage =
-        reinterpret_cast<std::uint32_t*>(wbase + ring_bytes(r) + std::size_t(NB) * kSlots * 8);
+    unsigned char* wbase = smem + kRecipBytes + warp * per_warp_bytes(NB);
+    unsigned long long* E = reinterpret_cast<unsigned long long*>(wbase);
+    std::uint32_t* stage = reinterpret_cast<std::uint32_t*>(wbase + std::size_t(NB) * kSlots * 8);
 
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
         recip[i] = i ? 0x80000000u / static_cast<std::uint32_t>(i) + 1u : 0u;
@@ -128,6 +193,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1)
     const int W = a.width;
     const std::size_t stride = static_cast<std::size_t>(W) * 3;
     const int per_frame = g.nbands * g.nsegs;
+    const int Hs = sg.Hs;
 
     for (;;) {
         int task = 0;
@@ -142,60 +208,54 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1)
         const int xs = a.x_lo + js * g.segw;
         const int xe = min(xs + g.segw, a.x_hi);
         const int NV = w2 + (xe - xs);  // virtual columns: w2 warm-up + outputs
-        const int base_col = xs - r;    // image column of ring-relative column 0
         const int X0 = xs - w2;         // image column of virtual column 0
-        const int row0 = yb - r;        // image row of ring row 0
-        const std::uint8_t* in = a.in + a.in_frame_stride * f;
         std::uint8_t* out = a.out + a.out_frame_stride * f;
         const bool row_ok = yb + lane < a.y_hi;
+        // Sheared address of (ring column c, ring row rho) = S[(D0 + c) * Hs + R0 + rho],
+        // ring column c = image column xs - r + c, ring row rho = image row yb - r + rho.
+        const std::uint32_t* Sf = S + sg.frame_elems * f;
+        const int R0 = yb - r - sg.y_base;
+        const long long D0 = static_cast<long long>(xs - r) + R0;
+        const std::uint32_t* row_t = Sf + R0 + lane;        // ring row t
+        const std::uint32_t* row_tw = Sf + R0 + lane + w2;  // ring row t + w2
 
-        // Pixel ring loader: ring-relative columns [32c, 32c+32), all ring rows.
-        auto load_chunk = [&](int c) {
-            const int col = base_col + 32 * c + lane;
-            const int ridx = (32 * c + lane) & (kRing - 1);
-            const bool col_ok = col < W;
-#pragma unroll 4
-            for (int rho = 0; rho < rows; ++rho) {
-                const int y = row0 + rho;
-                std::uint32_t e = 0;
-                if (col_ok && y < a.in_row0 + a.in_rows) {
-                    const std::uint8_t* p = in + static_cast<std::size_t>(y - a.in_row0) * stride +
-                                            static_cast<std::size_t>(col) * 3;
-                    e = make_entry(p[0], p[1], p[2], a.bin_mul);
+        auto fetch = [&](int s) {
+            Loads L{0, 0, 0, 0, 0, 0};
+            const int v = s - lane;
+            const int k = (s - lane) & 31;
+            const int vi = s - k + 32;
+            if (v >= 0 && v < NV) {
+                L.a = row_tw[(D0 + s + w2) * Hs];
+                L.b = row_t[(D0 + s) * Hs];
+                if (v >= w2) {
+                    L.c = row_tw[(D0 + s) * Hs];
+                    L.d = row_t[(D0 + s - w2) * Hs];
                 }
-                ring[rho * kRingStride + ridx] = e;
             }
-        };
-        auto zero_slot = [&](int slot) {
-#pragma unroll
-            for (int b = 0; b < NB; ++b) E[b * kSlots + slot] = 0ull;
-        };
-        // One row (k) of the from-scratch build of E(vi, yb).
-        auto init_step = [&](int vi, int k) {
-            const int slot = vi % kSlots;
-            rmw_add(E, slot, ring[k * kRingStride + (vi & (kRing - 1))]);
-            if (vi >= w2) rmw_sub(E, slot, ring[k * kRingStride + ((vi - w2) & (kRing - 1))]);
+            if (k < w2 && vi >= 0 && vi < NV) {
+                const std::uint32_t* rk = Sf + R0 + k;
+                L.i1 = rk[(D0 + s + 32) * Hs];
+                if (vi >= w2) L.i2 = rk[(D0 + s + 32 - w2) * Hs];
+            }
+            return L;
         };
 
         unsigned long long win[NB];
 #pragma unroll
         for (int b = 0; b < NB; ++b) win[b] = 0ull;
 
-        // Prologue: chunk 0 and E(v, yb) for v in [0, 32).
-        load_chunk(0);
-        zero_slot(lane);
-        __syncwarp();
-        for (int k = 0; k < w2; ++k) init_step(lane, k);
-        __syncwarp();
-
         const int nphases = ((NV - 1) >> 5) + 2;
-        for (int p = 0; p < nphases; ++p) {
-            load_chunk(p + 1);
-            const int vi = 32 * (p + 1) + lane;
-            zero_slot(vi % kSlots);
+        Loads cur = fetch(-32);
+        for (int p = -1; p < nphases; ++p) {
+            {  // zero the E slots of the columns initialised during this phase
+                const int slot = (32 * (p + 1) + lane) % kSlots;
+#pragma unroll
+                for (int b = 0; b < NB; ++b) E[b * kSlots + slot] = 0ull;
+            }
             __syncwarp();
             for (int ss = 0; ss < 32; ++ss) {
                 const int s = 32 * p + ss;
+                const Loads nxt = fetch(s + 1);
                 const int v = s - lane;
                 if (v >= 0 && v < NV) {
                     const int slot = v % kSlots;
@@ -208,75 +268,90 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1)
 #pragma unroll
                     for (int b = 0; b < NB; ++b) win[b] += e[b];
                     // Advance E(v) from row yb+lane to yb+lane+1 for lane+1.
-                    const int ce = v & (kRing - 1);
-                    const std::uint32_t* rn = ring + (lane + w2) * kRingStride;  // row y+r+1
-                    const std::uint32_t* ro = ring + lane * kRingStride;         // row y-r
-                    rmw_add(E, slot, rn[ce]);
-                    rmw_sub(E, slot, ro[ce]);
+                    rmw_add(E, slot, cur.a);
+                    rmw_sub(E, slot, cur.b);
                     if (v >= w2) {
-                        const int cl = (v - w2) & (kRing - 1);
-                        rmw_sub(E, slot, rn[cl]);
-                        rmw_add(E, slot, ro[cl]);
+                        rmw_sub(E, slot, cur.c);
+                        rmw_add(E, slot, cur.d);
                     }
                 }
-                if (ss < w2) init_step(vi, ss);
+                {  // one row of the from-scratch build of E(vi, yb)
+                    const int k = (s - lane) & 31;
+                    const int vi = s - k + 32;
+                    if (k < w2 && vi >= 0 && vi < NV) {
+                        const int slot = vi % kSlots;
+                        rmw_add(E, slot, cur.i1);
+                        if (vi >= w2) rmw_sub(E, slot, cur.i2);
+                    }
+                }
                 __syncwarp();
                 // Row fr just completed the 32-column block ending at v = s - fr.
                 const int fr = (s + 1) & 31;
-                const int vend = s - fr;
-                if (vend >= 0) {
-                    const int vv = vend - 31 + lane;
-                    if (vv >= w2 && vv < NV && yb + fr < a.y_hi) {
-                        const std::uint32_t rgb = stage[fr * kStageStride + lane];
-                        std::uint8_t* o = out +
-                                          static_cast<std::size_t>(yb + fr - a.out_row0) * stride +
-                                          static_cast<std::size_t>(X0 + vv) * 3;
-                        o[0] = static_cast<std::uint8_t>(rgb);
-                        o[1] = static_cast<std::uint8_t>(rgb >> 8);
-                        o[2] = static_cast<std::uint8_t>(rgb >> 16);
-                    }
+                const int vv = s - fr - 31 + lane;
+                if (vv >= w2 && vv < NV && yb + fr < a.y_hi) {
+                    const std::uint32_t rgb = stage[fr * kStageStride + lane];
+                    std::uint8_t* o = out + static_cast<std::size_t>(yb + fr - a.out_row0) * stride +
+                                      static_cast<std::size_t>(X0 + vv) * 3;
+                    o[0] = static_cast<std::uint8_t>(rgb);
+                    o[1] = static_cast<std::uint8_t>(rgb >> 8);
+                    o[2] = static_cast<std::uint8_t>(rgb >> 16);
                 }
                 __syncwarp();
+                cur = nxt;
             }
         }
     }
 }
 
 template <int NB>
-cudaError_t launch_nb(const BandArgs& a, int* counter, int num_sms, cudaStream_t s) {
-    const std::size_t pw = per_warp_bytes(NB, a.radius);
-    int warps = kMaxWarps;
+cudaError_t launch_nb(const BandArgs& a, int* counter, void* scratch, int num_sms,
+                      cudaStream_t s) {
+    const std::size_t pw = per_warp_bytes(NB);
     const std::size_t limit = 227 * 1024;
+    int warps = kMaxWarps;
     while (warps > 1 && kRecipBytes + warps * pw > limit) --warps;
     const std::size_t smem = kRecipBytes + warps * pw;
-    if (smem > limit) return cudaErrorInvalidConfiguration;
     cudaError_t e = cudaFuncSetAttribute(skew_kernel<NB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, skew_kernel<NB>, warps * 32, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+
+    const ShearGeom sg = shear_geom(a);
+    std::uint32_t* S = static_cast<std::uint32_t*>(scratch);
+    {
+        const dim3 grid(static_cast<unsigned>((a.width + kShearPad + kShearCols - 1) / kShearCols),
+                        static_cast<unsigned>(sg.Hs / kShearRows), static_cast<unsigned>(a.frames));
+        shear_kernel<<<grid, 256, 0, s>>>(a, S, sg);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
 
     TaskGeom g{};
     const int rows = a.y_hi - a.y_lo;
     const int iw = a.x_hi - a.x_lo;
     g.nbands = (rows + 31) / 32;
-    const long long total_warps = static_cast<long long>(num_sms) * warps;
-    // Aim for >= 4 tasks per resident warp, segments no narrower than 128.
-    long long want = 4 * total_warps;
-    long long per_seg = static_cast<long long>(g.nbands) * a.frames;
+    const long long total_warps = static_cast<long long>(num_sms) * per_sm * warps;
+    // Aim for >= 4 tasks per resident warp, segments no narrower than 256.
+    const long long want = 4 * total_warps;
+    const long long per_seg = static_cast<long long>(g.nbands) * a.frames;
     int nsegs = static_cast<int>((want + per_seg - 1) / per_seg);
-    const int max_segs = (iw + 127) / 128;
+    const int max_segs = (iw + 255) / 256;
     if (nsegs > max_segs) nsegs = max_segs;
     if (nsegs < 1) nsegs = 1;
     g.segw = (iw + nsegs - 1) / nsegs;
     g.nsegs = (iw + g.segw - 1) / g.segw;
     g.ntasks = a.frames * g.nbands * g.nsegs;
-    int blocks = static_cast<int>((g.ntasks + warps - 1) / warps);
-    if (blocks > num_sms) blocks = num_sms;
+    long long blocks = (g.ntasks + warps - 1) / warps;
+    if (blocks > static_cast<long long>(num_sms) * per_sm) blocks = num_sms * per_sm;
     if (blocks < 1) blocks = 1;
 
     e = cudaMemsetAsync(counter, 0, sizeof(int), s);
     if (e != cudaSuccess) return e;
-    skew_kernel<NB><<<blocks, warps * 32, smem, s>>>(a, counter, g);
+    skew_kernel<NB><<<static_cast<unsigned>(blocks), warps * 32, smem, s>>>(a, S, sg, counter, g);
     return cudaGetLastError();
 }
 
@@ -287,22 +362,24 @@ bool skew_supported(int levels, int radius) {
            bin_multiplier(levels) != 0;
 }
 
-std::size_t skew_smem_bytes(int levels, int radius) {
-    return kRecipBytes + per_warp_bytes(levels + 1, radius);
+std::size_t skew_scratch_bytes(const BandArgs& a) {
+    if (a.y_hi <= a.y_lo || a.x_hi <= a.x_lo) return 0;
+    return shear_geom(a).frame_elems * a.frames * sizeof(std::uint32_t);
 }
 
-cudaError_t launch_skew(const BandArgs& a, int* task_counter, int num_sms, cudaStream_t s) {
+cudaError_t launch_skew(const BandArgs& a, int* task_counter, void* scratch, int num_sms,
+                        cudaStream_t s) {
     if (a.y_hi <= a.y_lo || a.x_hi <= a.x_lo || a.frames <= 0) return cudaSuccess;
     const int bins = a.levels + 1;
-    if (bins <= 4) return launch_nb<4>(a, task_counter, num_sms, s);
-    if (bins <= 8) return launch_nb<8>(a, task_counter, num_sms, s);
-    if (bins <= 12) return launch_nb<12>(a, task_counter, num_sms, s);
-    if (bins <= 16) return launch_nb<16>(a, task_counter, num_sms, s);
-    if (bins <= 21) return launch_nb<21>(a, task_counter, num_sms, s);
-    if (bins <= 24) return launch_nb<24>(a, task_counter, num_sms, s);
-    if (bins <= 28) return launch_nb<28>(a, task_counter, num_sms, s);
-    if (bins <= 31) return launch_nb<31>(a, task_counter, num_sms, s);
-    return launch_nb<32>(a, task_counter, num_sms, s);
+    if (bins <= 4) return launch_nb<4>(a, task_counter, scratch, num_sms, s);
+    if (bins <= 8) return launch_nb<8>(a, task_counter, scratch, num_sms, s);
+    if (bins <= 12) return launch_nb<12>(a, task_counter, scratch, num_sms, s);
+    if (bins <= 16) return launch_nb<16>(a, task_counter, scratch, num_sms, s);
+    if (bins <= 21) return launch_nb<21>(a, task_counter, scratch, num_sms, s);
+    if (bins <= 24) return launch_nb<24>(a, task_counter, scratch, num_sms, s);
+    if (bins <= 28) return launch_nb<28>(a, task_counter, scratch, num_sms, s);
+    if (bins <= 31) return launch_nb<31>(a, task_counter, scratch, num_sms, s);
+    return launch_nb<32>(a, task_counter, scratch, num_sms, s);
 }
 
 }  // namespace opc
