@@ -37,16 +37,16 @@ namespace opc {
 namespace {
 
 constexpr int kMaxWarps = 8;
-constexpr int kSlots = 96;
+constexpr int kSlots = 128;  // E ring slots (power of two)
 constexpr int kStageStride = 33;
 constexpr int kRecipBytes = 1024 * 4;
 constexpr int kShearRows = 32;
 constexpr int kShearCols = 128;
 constexpr int kShearStride = kShearCols + 2;  // == 2 (mod 32): diagonal reads conflict-free
-// Zero entries are written for columns [W, W + kShearPad): the E column past
-// the last output column reads column W, and a zero entry keeps its bin in
-// range (its value is never used for an output pixel).
-constexpr int kShearPad = 32;
+// Zero entries are written for columns [W, W + kShearPad): E columns past the
+// last output column (unused values) read up to column W + 32, and a zero
+// entry keeps their bin index in range.
+constexpr int kShearPad = 64;
 
 __host__ __device__ inline std::size_t per_warp_bytes(int nb) {
     return static_cast<std::size_t>(nb) * kSlots * 8 + 32 * kStageStride * 4;
@@ -167,9 +167,113 @@ struct TaskGeom {
     int nbands, nsegs, segw, ntasks;
 };
 
+// Everything one step needs, per lane.
 struct Loads {
     std::uint32_t a, b, c, d, i1, i2;
 };
+
+struct Task {
+    const std::uint32_t* P0;  // sheared plane at diagonal D0 (ring column 0), ring row 0
+    std::uint8_t* out_row0;   // output row yb (band row 0), column 0
+    long long Hs;             // elements per diagonal
+    int NV, X0, w2, lane;
+    bool rows_ok;             // all 32 rows of the band are interior rows
+    int y_rows;               // valid rows in the band (<= 32)
+    std::size_t stride;
+};
+
+// Loads of step s.  Ring column c, ring row rho live at P0[(c + rho) * Hs + rho],
+// so every access of a step is on diagonal D0 + s (+ a step-independent shift).
+template <bool EDGE>
+__device__ __forceinline__ Loads fetch(const Task& T, int s) {
+    Loads L{0, 0, 0, 0, 0, 0};
+    const int t = T.lane;
+    const int v = s - t;
+    const int k = (s - t) & 31;
+    const int w2 = T.w2;
+    const std::uint32_t* P = T.P0 + static_cast<long long>(s) * T.Hs;  // diagonal D0 + s
+    const long long h = T.Hs;
+    if (!EDGE || (v >= 0 && v < T.NV)) {
+        L.a = P[w2 * h + t + w2];  // new row t+w2, entering column v
+        L.b = P[t];                // old row t,    entering column v
+        if (!EDGE || v >= w2) {
+            L.c = P[t + w2];          // new row, leaving column v - w2
+            L.d = P[-w2 * h + t];     // old row, leaving column v - w2
+        }
+    }
+    const int vi = s - k + 32;
+    if (!EDGE || (k < w2 && vi >= 0 && vi < T.NV)) {
+        L.i1 = P[32 * h + k];  // init: column vi, row k
+        if (!EDGE || vi >= w2) L.i2 = P[(32 - w2) * h + k];
+    }
+    return L;
+}
+
+// L2 prefetch of the 64 band rows of the diagonal the init reads at step s.
+__device__ __forceinline__ void prefetch_l2(const Task& T, int s) {
+    const std::uint32_t* p = T.P0 + (static_cast<long long>(s) + 32) * T.Hs + T.lane;
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 32));
+}
+
+template <int NB, bool EDGE>
+__device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
+                                     unsigned long long (&win)[NB], unsigned long long* E,
+                                     std::uint32_t* stage, const std::uint32_t* recip) {
+    const int t = T.lane;
+    const int v = s - t;
+    const int w2 = T.w2;
+    if (!EDGE || (v >= 0 && v < T.NV)) {
+        const int slot = v & (kSlots - 1);
+        unsigned long long e[NB];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) e[b] = E[b * kSlots + slot];
+        if (!EDGE || (v >= w2 && t < T.y_rows)) {
+            stage[t * kStageStride + (v & 31)] = winner_rgb<NB>(win, recip);
+        }
+#pragma unroll
+        for (int b = 0; b < NB; ++b) win[b] += e[b];
+        // Advance E(v) from row yb+t to yb+t+1 for lane t+1.
+        rmw_add(E, slot, cur.a);
+        rmw_sub(E, slot, cur.b);
+        if (!EDGE || v >= w2) {
+            rmw_sub(E, slot, cur.c);
+            rmw_add(E, slot, cur.d);
+        }
+    }
+    {  // one row of the from-scratch build of E(vi, yb)
+        const int k = (s - t) & 31;
+        const int vi = s - k + 32;
+        const int islot = vi & (kSlots - 1);
+        if (EDGE) {
+            if (k < w2 && vi >= 0 && vi < T.NV) {
+                rmw_add(E, islot, cur.i1);
+                if (vi >= w2) rmw_sub(E, islot, cur.i2);
+            }
+        } else {
+            // Branch-free: rows k >= w2 contribute zero (their entries are valid
+            // memory, so the bin index stays in range).
+            const unsigned long long m = k < w2 ? ~0ull : 0ull;
+            unsigned long long* p1 = E + (cur.i1 >> 24) * kSlots + islot;
+            *p1 += packed_of(cur.i1) & m;
+            unsigned long long* p2 = E + (cur.i2 >> 24) * kSlots + islot;
+            *p2 -= packed_of(cur.i2) & m;
+        }
+    }
+    __syncwarp();
+    // Row fr just completed the 32-column block ending at v = s - fr.
+    const int fr = (s + 1) & 31;
+    const int vv = s - fr - 31 + t;
+    if (!EDGE || (vv >= w2 && vv < T.NV && fr < T.y_rows)) {
+        const std::uint32_t rgb = stage[fr * kStageStride + t];
+        std::uint8_t* o = T.out_row0 + static_cast<std::size_t>(fr) * T.stride +
+                          static_cast<std::size_t>(T.X0 + vv) * 3;
+        o[0] = static_cast<std::uint8_t>(rgb);
+        o[1] = static_cast<std::uint8_t>(rgb >> 8);
+        o[2] = static_cast<std::uint8_t>(rgb >> 16);
+    }
+    __syncwarp();
+}
 
 template <int NB>
 __global__ void __launch_bounds__(kMaxWarps * 32)
@@ -180,7 +284,6 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int r = a.radius;
-    const int w2 = 2 * r + 1;
     unsigned char* wbase = smem + kRecipBytes + warp * per_warp_bytes(NB);
     unsigned long long* E = reinterpret_cast<unsigned long long*>(wbase);
     std::uint32_t* stage = reinterpret_cast<std::uint32_t*>(wbase + std::size_t(NB) * kSlots * 8);
@@ -190,10 +293,12 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
     }
     __syncthreads();
 
-    const int W = a.width;
-    const std::size_t stride = static_cast<std::size_t>(W) * 3;
     const int per_frame = g.nbands * g.nsegs;
-    const int Hs = sg.Hs;
+    Task T;
+    T.Hs = sg.Hs;
+    T.w2 = 2 * r + 1;
+    T.lane = lane;
+    T.stride = static_cast<std::size_t>(a.width) * 3;
 
     for (;;) {
         int task = 0;
@@ -207,97 +312,57 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
         const int yb = a.y_lo + 32 * kb;
         const int xs = a.x_lo + js * g.segw;
         const int xe = min(xs + g.segw, a.x_hi);
-        const int NV = w2 + (xe - xs);  // virtual columns: w2 warm-up + outputs
-        const int X0 = xs - w2;         // image column of virtual column 0
-        std::uint8_t* out = a.out + a.out_frame_stride * f;
-        const bool row_ok = yb + lane < a.y_hi;
-        // Sheared address of (ring column c, ring row rho) = S[(D0 + c) * Hs + R0 + rho],
-        // ring column c = image column xs - r + c, ring row rho = image row yb - r + rho.
-        const std::uint32_t* Sf = S + sg.frame_elems * f;
+        T.NV = T.w2 + (xe - xs);  // virtual columns: w2 warm-up + outputs
+        T.X0 = xs - T.w2;         // image column of virtual column 0
+        T.y_rows = min(32, a.y_hi - yb);
+        T.rows_ok = T.y_rows == 32;
+        T.out_row0 = a.out + a.out_frame_stride * f +
+                     static_cast<std::size_t>(yb - a.out_row0) * T.stride;
+        // ring column c = image column xs - r + c, ring row rho = image row yb - r + rho;
+        // element (d, y) of the plane at d * Hs + (y - y_base), d = x + (y - y_base).
         const int R0 = yb - r - sg.y_base;
         const long long D0 = static_cast<long long>(xs - r) + R0;
-        const std::uint32_t* row_t = Sf + R0 + lane;        // ring row t
-        const std::uint32_t* row_tw = Sf + R0 + lane + w2;  // ring row t + w2
-
-        auto fetch = [&](int s) {
-            Loads L{0, 0, 0, 0, 0, 0};
-            const int v = s - lane;
-            const int k = (s - lane) & 31;
-            const int vi = s - k + 32;
-            if (v >= 0 && v < NV) {
-                L.a = row_tw[(D0 + s + w2) * Hs];
-                L.b = row_t[(D0 + s) * Hs];
-                if (v >= w2) {
-                    L.c = row_tw[(D0 + s) * Hs];
-                    L.d = row_t[(D0 + s - w2) * Hs];
-                }
-            }
-            if (k < w2 && vi >= 0 && vi < NV) {
-                const std::uint32_t* rk = Sf + R0 + k;
-                L.i1 = rk[(D0 + s + 32) * Hs];
-                if (vi >= w2) L.i2 = rk[(D0 + s + 32 - w2) * Hs];
-            }
-            return L;
-        };
+        T.P0 = S + sg.frame_elems * f + D0 * T.Hs + R0;
 
         unsigned long long win[NB];
 #pragma unroll
         for (int b = 0; b < NB; ++b) win[b] = 0ull;
 
-        const int nphases = ((NV - 1) >> 5) + 2;
-        Loads cur = fetch(-32);
+        const int nphases = ((T.NV - 1) >> 5) + 2;
+        const int p_steady_lo = (T.w2 + 62 + 31) >> 5;  // all lanes past warm-up and flush start
+        Loads cur = fetch<true>(T, -32);
         for (int p = -1; p < nphases; ++p) {
             {  // zero the E slots of the columns initialised during this phase
-                const int slot = (32 * (p + 1) + lane) % kSlots;
+                const int slot = (32 * (p + 1) + lane) & (kSlots - 1);
 #pragma unroll
                 for (int b = 0; b < NB; ++b) E[b * kSlots + slot] = 0ull;
             }
             __syncwarp();
-            for (int ss = 0; ss < 32; ++ss) {
-                const int s = 32 * p + ss;
-                const Loads nxt = fetch(s + 1);
-                const int v = s - lane;
-                if (v >= 0 && v < NV) {
-                    const int slot = v % kSlots;
-                    unsigned long long e[NB];
-#pragma unroll
-                    for (int b = 0; b < NB; ++b) e[b] = E[b * kSlots + slot];
-                    if (v >= w2 && row_ok) {
-                        stage[lane * kStageStride + (v & 31)] = winner_rgb<NB>(win, recip);
-                    }
-#pragma unroll
-                    for (int b = 0; b < NB; ++b) win[b] += e[b];
-                    // Advance E(v) from row yb+lane to yb+lane+1 for lane+1.
-                    rmw_add(E, slot, cur.a);
-                    rmw_sub(E, slot, cur.b);
-                    if (v >= w2) {
-                        rmw_sub(E, slot, cur.c);
-                        rmw_add(E, slot, cur.d);
-                    }
+            const bool steady = T.rows_ok && p >= p_steady_lo && 32 * p + 31 < T.NV;
+            if (steady) {
+                // Loads run two steps ahead; the diagonal first touched eight
+                // steps ahead (the init column's) is pulled into L2 now.
+                Loads n1 = fetch<false>(T, 32 * p + 1);
+#pragma unroll 1
+                for (int ss = 0; ss < 32; ss += 2) {
+                    const int s = 32 * p + ss;
+                    prefetch_l2(T, s + 8);
+                    const Loads n2 = fetch<false>(T, s + 2);
+                    step<NB, false>(T, s, cur, win, E, stage, recip);
+                    prefetch_l2(T, s + 9);
+                    const Loads n3 = fetch<false>(T, s + 3);
+                    step<NB, false>(T, s + 1, n1, win, E, stage, recip);
+                    cur = n2;
+                    n1 = n3;
                 }
-                {  // one row of the from-scratch build of E(vi, yb)
-                    const int k = (s - lane) & 31;
-                    const int vi = s - k + 32;
-                    if (k < w2 && vi >= 0 && vi < NV) {
-                        const int slot = vi % kSlots;
-                        rmw_add(E, slot, cur.i1);
-                        if (vi >= w2) rmw_sub(E, slot, cur.i2);
-                    }
+            } else {
+#pragma unroll 1
+                for (int ss = 0; ss < 32; ++ss) {
+                    const int s = 32 * p + ss;
+                    const Loads nxt = fetch<true>(T, s + 1);
+                    step<NB, true>(T, s, cur, win, E, stage, recip);
+                    cur = nxt;
                 }
-                __syncwarp();
-                // Row fr just completed the 32-column block ending at v = s - fr.
-                const int fr = (s + 1) & 31;
-                const int vv = s - fr - 31 + lane;
-                if (vv >= w2 && vv < NV && yb + fr < a.y_hi) {
-                    const std::uint32_t rgb = stage[fr * kStageStride + lane];
-                    std::uint8_t* o = out + static_cast<std::size_t>(yb + fr - a.out_row0) * stride +
-                                      static_cast<std::size_t>(X0 + vv) * 3;
-                    o[0] = static_cast<std::uint8_t>(rgb);
-                    o[1] = static_cast<std::uint8_t>(rgb >> 8);
-                    o[2] = static_cast<std::uint8_t>(rgb >> 16);
-                }
-                __syncwarp();
-                cur = nxt;
             }
         }
     }
