@@ -36,8 +36,8 @@ namespace opc {
 
 namespace {
 
-constexpr int kMaxWarps = 8;
-constexpr int kSlots = 128;  // E ring slots (power of two)
+constexpr int kMaxWarps = 12;
+constexpr int kSlots = 96;  // E ring slots
 constexpr int kStageStride = 33;
 constexpr int kRecipBytes = 1024 * 4;
 constexpr int kShearRows = 32;
@@ -224,7 +224,7 @@ __device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
     const int v = s - t;
     const int w2 = T.w2;
     if (!EDGE || (v >= 0 && v < T.NV)) {
-        const int slot = v & (kSlots - 1);
+        const int slot = v % kSlots;
         unsigned long long e[NB];
 #pragma unroll
         for (int b = 0; b < NB; ++b) e[b] = E[b * kSlots + slot];
@@ -244,7 +244,7 @@ __device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
     {  // one row of the from-scratch build of E(vi, yb)
         const int k = (s - t) & 31;
         const int vi = s - k + 32;
-        const int islot = vi & (kSlots - 1);
+        const int islot = vi % kSlots;
         if (EDGE) {
             if (k < w2 && vi >= 0 && vi < T.NV) {
                 rmw_add(E, islot, cur.i1);
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
         Loads cur = fetch<true>(T, -32);
         for (int p = -1; p < nphases; ++p) {
             {  // zero the E slots of the columns initialised during this phase
-                const int slot = (32 * (p + 1) + lane) & (kSlots - 1);
+                const int slot = (32 * (p + 1) + lane) % kSlots;
 #pragma unroll
                 for (int b = 0; b < NB; ++b) E[b * kSlots + slot] = 0ull;
             }
