@@ -71,10 +71,14 @@ __host__ inline ShearGeom shear_geom(const BandArgs& a) {
     return g;
 }
 
+// Sheared-plane entry of one pixel: B | R << 8 | G << 18 | bin << 26.  The
+// layout is chosen so that the packed 64-bit contribution (count 1, R, G, B)
+// costs two ALU ops: lo = e & 0x03FC00FF (B | G << 18) and the byte permute
+// R + 2^18, whose x16 is the hi word R << 4 | 1 << 22.
 __device__ __forceinline__ std::uint32_t make_entry(std::uint32_t r, std::uint32_t g,
                                                     std::uint32_t b, std::uint32_t bin_mul) {
     const std::uint32_t bin = __umulhi(r + g + b, bin_mul);  // filter.hpp:31-35
-    return r | (g << 8) | (b << 16) | (bin << 24);
+    return b | (r << 8) | (g << 18) | (bin << 26);
 }
 
 // Sheared entry plane.  Block: 32 rows x 128 columns staged through shared
@@ -118,21 +122,59 @@ __global__ void __launch_bounds__(256) shear_kernel(BandArgs a, std::uint32_t* S
     }
 }
 
-// Packed single-pixel contribution (count 1, R, G, B) of an entry.
-__device__ __forceinline__ unsigned long long packed_of(std::uint32_t e) {
-    const std::uint32_t lo = ((e >> 16) & 0xFFu) | ((e & 0xFF00u) << 10);  // B | G << 18
-    const std::uint32_t hi = ((e & 0xFFu) << 4) | 0x400000u;                // R << 36, 1 << 54
-    return (static_cast<unsigned long long>(hi) << 32) | lo;
+// ---- packed 64-bit updates ----
+// Multipliers come from a kernel argument (Mul) so that ptxas keeps the
+// "r1 * 16 + hi (+ carry)" as one IMAD.X on the FMA pipe instead of folding it
+// into shifts on the ALU pipe, which is the kernel's binding resource.
+struct Mul {
+    std::uint32_t m16, negm16;  // 16, -16
+};
+
+__device__ __forceinline__ std::uint32_t entry_lo(std::uint32_t e) { return e & 0x03FC00FFu; }
+__device__ __forceinline__ std::uint32_t entry_r1(std::uint32_t e) {
+    return __byte_perm(e, 0x00040000u, 0x7641);  // R + 2^18; x16 = R << 4 | 1 << 22
 }
 
-__device__ __forceinline__ void rmw_add(unsigned long long* E, int slot, std::uint32_t e) {
-    unsigned long long* p = E + (e >> 24) * kSlots + slot;
-    *p += packed_of(e);
+// p += (r1 * mul) << 32 | lo   (64-bit, carry from the low word)
+__device__ __forceinline__ void packed_add(unsigned long long* p, std::uint32_t lo, std::uint32_t r1,
+                                           std::uint32_t mul) {
+    std::uint32_t wl, wh;
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(wl), "=r"(wh) : "l"(*p));
+    asm("add.cc.u32 %0, %0, %2;\n\tmadc.lo.u32 %1, %3, %4, %1;"
+        : "+r"(wl), "+r"(wh) : "r"(lo), "r"(r1), "r"(mul));
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(wl), "r"(wh));
+    *p = r;
+}
+// p -= (r1 * 16) << 32 | lo
+__device__ __forceinline__ void packed_sub(unsigned long long* p, std::uint32_t lo, std::uint32_t r1,
+                                           std::uint32_t negmul) {
+    std::uint32_t wl, wh;
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(wl), "=r"(wh) : "l"(*p));
+    // wl - lo with borrow; hi - 16*r1 - borrow == hi + (-16)*r1 - borrow
+    asm("sub.cc.u32 %0, %0, %2;\n\tsubc.u32 %1, %1, 0;\n\tmad.lo.u32 %1, %3, %4, %1;"
+        : "+r"(wl), "+r"(wh) : "r"(lo), "r"(r1), "r"(negmul));
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(wl), "r"(wh));
+    *p = r;
 }
 
-__device__ __forceinline__ void rmw_sub(unsigned long long* E, int slot, std::uint32_t e) {
-    unsigned long long* p = E + (e >> 24) * kSlots + slot;
-    *p -= packed_of(e);
+// E[bin(e)][slot] += / -= packed(e).  Es = E + slot.
+__device__ __forceinline__ void rmw_add(unsigned long long* Es, std::uint32_t e, const Mul& M) {
+    packed_add(Es + (e >> 26) * kSlots, entry_lo(e), entry_r1(e), M.m16);
+}
+__device__ __forceinline__ void rmw_sub(unsigned long long* Es, std::uint32_t e, const Mul& M) {
+    packed_sub(Es + (e >> 26) * kSlots, entry_lo(e), entry_r1(e), M.negm16);
+}
+// Masked forms for the branch-free init: mask = all ones or zero, m16 = 16 or
+// 0, nm16 = -16 or 0.
+__device__ __forceinline__ void rmw_add_m(unsigned long long* Es, std::uint32_t e, std::uint32_t mask,
+                                          std::uint32_t m16) {
+    packed_add(Es + (e >> 26) * kSlots, entry_lo(e) & mask, entry_r1(e), m16);
+}
+__device__ __forceinline__ void rmw_sub_m(unsigned long long* Es, std::uint32_t e, std::uint32_t mask,
+                                          std::uint32_t nm16) {
+    packed_sub(Es + (e >> 26) * kSlots, entry_lo(e) & mask, entry_r1(e), nm16);
 }
 
 template <int NB>
@@ -173,6 +215,7 @@ struct Loads {
 };
 
 struct Task {
+    Mul M;
     const std::uint32_t* P0;  // sheared plane at diagonal D0 (ring column 0), ring row 0
     std::uint8_t* out_row0;   // output row yb (band row 0), column 0
     long long Hs;             // elements per diagonal
@@ -234,11 +277,12 @@ __device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
 #pragma unroll
         for (int b = 0; b < NB; ++b) win[b] += e[b];
         // Advance E(v) from row yb+t to yb+t+1 for lane t+1.
-        rmw_add(E, slot, cur.a);
-        rmw_sub(E, slot, cur.b);
+        unsigned long long* Es = E + slot;
+        rmw_add(Es, cur.a, T.M);
+        rmw_sub(Es, cur.b, T.M);
         if (!EDGE || v >= w2) {
-            rmw_sub(E, slot, cur.c);
-            rmw_add(E, slot, cur.d);
+            rmw_sub(Es, cur.c, T.M);
+            rmw_add(Es, cur.d, T.M);
         }
     }
     {  // one row of the from-scratch build of E(vi, yb)
@@ -247,17 +291,15 @@ __device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
         const int islot = vi % kSlots;
         if (EDGE) {
             if (k < w2 && vi >= 0 && vi < T.NV) {
-                rmw_add(E, islot, cur.i1);
-                if (vi >= w2) rmw_sub(E, islot, cur.i2);
+                rmw_add(E + islot, cur.i1, T.M);
+                if (vi >= w2) rmw_sub(E + islot, cur.i2, T.M);
             }
         } else {
             // Branch-free: rows k >= w2 contribute zero (their entries are valid
             // memory, so the bin index stays in range).
-            const unsigned long long m = k < w2 ? ~0ull : 0ull;
-            unsigned long long* p1 = E + (cur.i1 >> 24) * kSlots + islot;
-            *p1 += packed_of(cur.i1) & m;
-            unsigned long long* p2 = E + (cur.i2 >> 24) * kSlots + islot;
-            *p2 -= packed_of(cur.i2) & m;
+            const std::uint32_t m = k < w2 ? ~0u : 0u;
+            rmw_add_m(E + islot, cur.i1, m, m & T.M.m16);
+            rmw_sub_m(E + islot, cur.i2, m, m & T.M.negm16);
         }
     }
     __syncwarp();
@@ -278,7 +320,7 @@ __device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
 template <int NB>
 __global__ void __launch_bounds__(kMaxWarps * 32)
     skew_kernel(BandArgs a, const std::uint32_t* __restrict__ S, ShearGeom sg, int* task_counter,
-                TaskGeom g) {
+                TaskGeom g, Mul M) {
     extern __shared__ __align__(16) unsigned char smem[];
     std::uint32_t* recip = reinterpret_cast<std::uint32_t*>(smem);
     const int lane = threadIdx.x & 31;
@@ -295,6 +337,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
 
     const int per_frame = g.nbands * g.nsegs;
     Task T;
+    T.M = M;
     T.Hs = sg.Hs;
     T.w2 = 2 * r + 1;
     T.lane = lane;
@@ -416,7 +459,8 @@ cudaError_t launch_nb(const BandArgs& a, int* counter, void* scratch, int num_sm
 
     e = cudaMemsetAsync(counter, 0, sizeof(int), s);
     if (e != cudaSuccess) return e;
-    skew_kernel<NB><<<static_cast<unsigned>(blocks), warps * 32, smem, s>>>(a, S, sg, counter, g);
+    const Mul M{16u, 0xFFFFFFF0u};
+    skew_kernel<NB><<<static_cast<unsigned>(blocks), warps * 32, smem, s>>>(a, S, sg, counter, g, M);
     return cudaGetLastError();
 }
 
