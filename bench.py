@@ -61,35 +61,46 @@ def colhist_ops_per_px(bins: int) -> int:
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons, sampled every 20 ms from before the
+    warm-up to after the timed region; summary() keeps the samples whose
+    timestamps fall inside the timed region [mark_start(), mark_end()]."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device: int):
         self.device = device
         self.proc = None
-        self.lines: list[str] = []
+        self.lines: list[tuple[float, str]] = []
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
+            time.sleep(0.3)  # let the sampler start before the measured region
         except (FileNotFoundError, OSError):
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
 
     def __exit__(self, *exc):
         if self.proc is not None:
+            time.sleep(0.1)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -98,23 +109,27 @@ class ClockSampler:
             self._t.join(timeout=2)
 
     def summary(self) -> dict:
-        mhz, max_mhz, reasons = [], 0.0, set()
+        mhz, max_mhz, reasons, power = [], 0.0, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for t, ln in self.lines:
+            # the line arrives <= 20 ms after it was sampled
+            if self.t0 is not None and not (self.t0 <= t <= self.t1 + 0.04):
+                continue
             f = [x.strip() for x in ln.split(",")]
-            if len(f) < 9:
+            if len(f) < 10:
                 continue
             try:
-                mhz.append(float(f[1]))
-                max_mhz = max(max_mhz, float(f[2]))
+                mhz.append(float(f[2]))
+                max_mhz = max(max_mhz, float(f[3]))
+                power.append(float(f[4]))
             except ValueError:
                 continue
-            for name, v in zip(names, f[5:9]):
+            for name, v in zip(names, f[6:10]):
                 if v.lower() == "active":
                     reasons.add(name)
         return {"sm_mhz": statistics.median(mhz) if mhz else None,
                 "sm_max_mhz": max_mhz or None, "reasons": sorted(reasons),
-                "samples": len(mhz)}
+                "samples": len(mhz), "power_w_max": max(power) if power else None}
 
 
 # ----------------------------------------------------------------------------
@@ -167,14 +182,21 @@ class CpuEngine:
             out[y0:y1] = tmp[radius:radius + (y1 - y0)]
 
     def calibrate_rows(self, img, out, cfg, threads, target_s) -> tuple[int, float]:
+        """Rows of the image whose filtering takes about target_s on `threads`
+        threads: probe with >= 4 rows per thread, grow until the probe takes
+        >= 0.5 s, then scale."""
         r = cfg.radius
-        y0 = r
-        rows = max(1, min(8, cfg.height - 2 * r))
-        t = time.perf_counter()
-        self.band(img, out, r, cfg.levels, y0, y0 + rows, threads)
-        dt = time.perf_counter() - t
+        interior = cfg.height - 2 * r
+        rows = max(1, min(interior, 4 * threads))
+        while True:
+            t = time.perf_counter()
+            self.band(img, out, r, cfg.levels, r, r + rows, threads)
+            dt = time.perf_counter() - t
+            if dt >= 0.5 or rows >= interior:
+                break
+            rows = min(interior, rows * 4)
         rate = rows / max(dt, 1e-6)
-        want = int(max(1, min(cfg.height - 2 * r, rate * target_s)))
+        want = int(max(1, min(interior, rate * target_s)))
         return want, rate
 
 
@@ -237,7 +259,7 @@ def workload_config(cfg, n: int) -> dict:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c4")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
@@ -314,12 +336,14 @@ def main() -> None:
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
+        clocks.mark_start()
         with torch.cuda.stream(stream):
             ev[0].record(stream)
             for i in range(args.steps):
                 step_device()
                 ev[i + 1].record(stream)
         stream.synchronize()
+        clocks.mark_end()
     torch.cuda.synchronize()
     barrier()
     launches = opc.kernel_launches() - launches0

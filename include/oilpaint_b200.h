@@ -96,6 +96,20 @@ int opc_filter_rgb8_band(const uint8_t* in_rows, uint8_t* out_rows, int32_t widt
                          int32_t height, int32_t y_begin, int32_t y_end, int32_t radius,
                          int32_t levels, int32_t border, const opc_config* cfg);
 
+/* Multi-GPU host path.  frames == 1: the output rows are split
+ * into ndevices contiguous bands [opc_band_begin(h,n,k), opc_band_begin(h,n,k+1))
+ * and each device filters its band from its halo'd input rows; frames > 1: the
+ * frames are split the same way.  One host thread per device, each with its
+ * own device buffers and streams; no collective (the gather is the disjoint
+ * writes into `out`).  Output is byte-identical to opc_filter_rgb8 / _batch.
+ * devices: ndevices CUDA ordinals (repeats allowed, e.g. {0,0} on one GPU). */
+int opc_filter_rgb8_multi(const uint8_t* in, uint8_t* out, int32_t frames, int32_t width,
+                          int32_t height, int32_t radius, int32_t levels, int32_t border,
+                          const int32_t* devices, int32_t ndevices, const opc_config* cfg);
+
+/* First row (or frame) of part k of n equal contiguous parts of [0, total). */
+int32_t opc_band_begin(int32_t total, int32_t parts, int32_t k);
+
 /* Helpers for the band protocol: first input row and input row count. */
 int32_t opc_band_in_row0(int32_t height, int32_t y_begin, int32_t radius);
 int32_t opc_band_in_rows(int32_t height, int32_t y_begin, int32_t y_end, int32_t radius);

@@ -22,7 +22,7 @@ EXPORTS = (
     "opc_validate", "opc_filter_rgb8", "opc_filter_rgb8_batch", "opc_filter_rgb8_band",
     "opc_band_in_row0", "opc_band_in_rows", "opc_last_error", "opc_version",
     "opc_kernel_launches", "opc_device_count", "opc_synchronize", "opc_plan_kernel",
-    "opc_release", "opc_generate",
+    "opc_release", "opc_generate", "opc_filter_rgb8_multi", "opc_band_begin",
 )
 
 
@@ -56,6 +56,11 @@ def _load() -> ctypes.CDLL:
     lib.opc_filter_rgb8_batch.restype = ctypes.c_int
     lib.opc_filter_rgb8_band.argtypes = [u8p, u8p, i32, i32, i32, i32, i32, i32, i32, cfgp]
     lib.opc_filter_rgb8_band.restype = ctypes.c_int
+    lib.opc_filter_rgb8_multi.argtypes = [u8p, u8p, i32, i32, i32, i32, i32, i32,
+                                          ctypes.POINTER(ctypes.c_int32), i32, cfgp]
+    lib.opc_filter_rgb8_multi.restype = ctypes.c_int
+    lib.opc_band_begin.argtypes = [i32, i32, i32]
+    lib.opc_band_begin.restype = i32
     lib.opc_band_in_row0.argtypes = [i32, i32, i32]
     lib.opc_band_in_row0.restype = i32
     lib.opc_band_in_rows.argtypes = [i32, i32, i32, i32]

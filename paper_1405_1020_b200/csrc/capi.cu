@@ -8,6 +8,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/oilpaint_b200.h"
@@ -343,6 +344,55 @@ int opc_filter_rgb8_band(const uint8_t* in_rows, uint8_t* out_rows, int32_t widt
                          int32_t levels, int32_t border, const opc_config* cfg) {
     return filter_core(in_rows, out_rows, 1, width, height, y_begin, y_end, radius, levels, border,
                        cfg);
+}
+
+int32_t opc_band_begin(int32_t total, int32_t parts, int32_t k) {
+    if (parts < 1) return 0;
+    return static_cast<int32_t>(static_cast<long long>(total) * k / parts);
+}
+
+int opc_filter_rgb8_multi(const uint8_t* in, uint8_t* out, int32_t frames, int32_t width,
+                          int32_t height, int32_t radius, int32_t levels, int32_t border,
+                          const int32_t* devices, int32_t ndevices, const opc_config* cfg) {
+    const unsigned flags = cfg ? cfg->flags : 0u;
+    int rc = validate_params(width, height, 3ull * width * height, radius, levels, flags);
+    if (rc != OPC_OK) return rc;
+    if (flags & OPC_FLAG_DEVICE_POINTERS) {
+        return set_error(OPC_EINVAL, "opc_filter_rgb8_multi takes host buffers only");
+    }
+    if (!devices || ndevices < 1) return set_error(OPC_EINVAL, "ndevices must be >= 1");
+    if (frames < 1) return set_error(OPC_EINVAL, "frames must be >= 1, got " + std::to_string(frames));
+    const std::size_t row_bytes = static_cast<std::size_t>(width) * 3;
+    const std::size_t frame_bytes = row_bytes * height;
+    const int total = frames == 1 ? height : frames;
+    int parts = ndevices < total ? ndevices : total;
+    std::vector<int> status(parts, OPC_OK);
+    std::vector<std::string> msg(parts);
+    std::vector<std::thread> pool;
+    for (int k = 0; k < parts; ++k) {
+        pool.emplace_back([&, k] {
+            opc_config c = cfg ? *cfg : opc_config{};
+            c.device = devices[k];
+            c.stream = nullptr;
+            const int b = opc_band_begin(total, parts, k), e = opc_band_begin(total, parts, k + 1);
+            if (frames == 1) {
+                const int lo = opc_band_in_row0(height, b, radius);
+                status[k] = filter_core(in + row_bytes * lo, out + row_bytes * b, 1, width, height,
+                                        b, e, radius, levels, border, &c);
+            } else {
+                status[k] = filter_core(in + frame_bytes * b, out + frame_bytes * b, e - b, width,
+                                        height, 0, height, radius, levels, border, &c);
+            }
+            if (status[k] != OPC_OK) msg[k] = g_last_error;
+        });
+    }
+    for (auto& t : pool) t.join();
+    for (int k = 0; k < parts; ++k) {
+        if (status[k] != OPC_OK) {
+            return set_error(status[k], "device " + std::to_string(devices[k]) + ": " + msg[k]);
+        }
+    }
+    return OPC_OK;
 }
 
 int32_t opc_band_in_row0(int32_t height, int32_t y_begin, int32_t radius) {

@@ -42,6 +42,7 @@ class FilterParams:
 class CudaConfig:
     """Engine configuration (the CUDA analogue of ParallelConfig, parallel.hpp:10-17)."""
     device: int = -1           # -1: current device
+    devices: tuple = ()        # >1 entries: rows (or frames) split across these GPUs
     stream: Optional[int] = None   # cudaStream_t handle for device-pointer calls
     kernel: int = _lib.OPC_KERNEL_AUTO
     allow_levels_256: bool = False  # documented C-ABI extension (config 3)
@@ -96,9 +97,19 @@ def apply_cuda(img: np.ndarray, params: FilterParams = FilterParams(),
     h, w, _ = img.shape
     out = np.empty_like(img)
     c = cfg.to_c()
+    if len(cfg.devices) > 1:
+        _multi(img, out, 1, w, h, params, cfg, c)
+        return out
     _raise(LIB.opc_filter_rgb8(img.ctypes.data, out.ctypes.data, w, h, params.radius,
                                params.intensity_levels, int(params.border), ctypes.byref(c)))
     return out
+
+
+def _multi(src, dst, frames, w, h, params, cfg, c) -> None:
+    devs = (ctypes.c_int32 * len(cfg.devices))(*cfg.devices)
+    _raise(LIB.opc_filter_rgb8_multi(src.ctypes.data, dst.ctypes.data, frames, w, h,
+                                     params.radius, params.intensity_levels, int(params.border),
+                                     devs, len(cfg.devices), ctypes.byref(c)))
 
 
 def apply_cuda_batch(frames: np.ndarray, params: FilterParams = FilterParams(),
@@ -111,6 +122,9 @@ def apply_cuda_batch(frames: np.ndarray, params: FilterParams = FilterParams(),
     f, h, w, _ = frames.shape
     out = np.empty_like(frames)
     c = cfg.to_c()
+    if len(cfg.devices) > 1:
+        _multi(frames, out, f, w, h, params, cfg, c)
+        return out
     _raise(LIB.opc_filter_rgb8_batch(frames.ctypes.data, out.ctypes.data, f, w, h, params.radius,
                                      params.intensity_levels, int(params.border), ctypes.byref(c)))
     return out
@@ -156,6 +170,11 @@ def apply_cuda_band_device(in_ptr: int, out_ptr: int, width: int, height: int, y
     _raise(LIB.opc_filter_rgb8_band(in_ptr, out_ptr, width, height, y_begin, y_end,
                                     params.radius, params.intensity_levels, int(params.border),
                                     ctypes.byref(c)))
+
+
+def band_begin(total: int, parts: int, k: int) -> int:
+    """First row (or frame) of part k of `parts` equal contiguous parts of [0, total)."""
+    return LIB.opc_band_begin(total, parts, k)
 
 
 def synchronize(cfg: Optional[CudaConfig] = None) -> None:
