@@ -38,7 +38,7 @@ namespace {
 
 constexpr int kMaxWarps = 12;
 constexpr int kSlots = 96;  // E ring slots
-constexpr int kStageStride = 33;
+constexpr int kStageStride = 34;  // == 2 (mod 32): skewed (row t, column s-t) writes hit distinct banks
 constexpr int kRecipBytes = 1024 * 4;
 constexpr int kShearRows = 32;
 constexpr int kShearCols = 128;
