@@ -155,7 +155,9 @@ int plan(int levels, int radius, int forced) {
 
 // Runs the filter on device buffers already holding the band input.
 int run_device(const opc::BandArgs& a, int border, int kernel, DevCtx* ctx, cudaStream_t s) {
+    // (a frame too large for the skew family's 32-bit plane offsets takes the direct family)
     cudaError_t e = cudaSuccess;
+    if (kernel == OPC_KERNEL_SKEW && !opc::skew_fits(a)) kernel = OPC_KERNEL_DIRECT;
     if (kernel == OPC_KERNEL_SKEW) {
         // Rotate over 64 task counters so kernels in flight on different
         // streams never share one.

@@ -48,6 +48,7 @@ cudaError_t launch_border(const BandArgs& a, int border_policy, cudaStream_t s);
 // Skew family also needs device scratch (the sheared entry plane) of
 // skew_scratch_bytes(a) bytes.
 bool skew_supported(int levels, int radius);
+bool skew_fits(const BandArgs& a);  // sheared plane addressable with 32-bit offsets
 std::size_t skew_scratch_bytes(const BandArgs& a);
 cudaError_t launch_skew(const BandArgs& a, int* task_counter, void* scratch, int num_sms,
                         cudaStream_t s);

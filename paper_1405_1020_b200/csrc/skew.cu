@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(256) shear_kernel(BandArgs a, std::uint32_t* S
 // "r1 * 16 + hi (+ carry)" as one IMAD.X on the FMA pipe instead of folding it
 // into shifts on the ALU pipe, which is the kernel's binding resource.
 struct Mul {
-    std::uint32_t m16, negm16;  // 16, -16
+    std::uint32_t m16, negm16, four;  // 16, -16, 4
 };
 
 __device__ __forceinline__ std::uint32_t entry_lo(std::uint32_t e) { return e & 0x03FC00FFu; }
@@ -216,17 +216,33 @@ struct Loads {
 
 struct Task {
     Mul M;
-    const std::uint32_t* P0;  // sheared plane at diagonal D0 (ring column 0), ring row 0
+    const std::uint32_t* Sf;  // sheared plane of this frame
+    std::uint32_t o0;         // element offset of diagonal D0 (ring column 0), ring row 0
+    std::uint32_t Hs;         // elements per diagonal
+    std::uint32_t dA, dD, dI, dI2;  // w2*Hs + w2, w2*Hs, 32*Hs, (32-w2)*Hs
     std::uint8_t* out_row0;   // output row yb (band row 0), column 0
-    long long Hs;             // elements per diagonal
     int NV, X0, w2, lane;
     bool rows_ok;             // all 32 rows of the band are interior rows
     int y_rows;               // valid rows in the band (<= 32)
     std::size_t stride;
 };
 
-// Loads of step s.  Ring column c, ring row rho live at P0[(c + rho) * Hs + rho],
-// so every access of a step is on diagonal D0 + s (+ a step-independent shift).
+// 32-bit element offset from a 64-bit base: one IMAD.WIDE (FMA pipe; the
+// runtime multiplier four = 4 keeps ptxas from turning it into ALU LEAs) and the load.
+__device__ __forceinline__ std::uint32_t ld_off(const std::uint32_t* base, std::uint32_t off,
+                                                std::uint32_t four) {
+    std::uint32_t v;
+    asm volatile(
+        "{\n\t.reg .u64 a;\n\tmad.wide.u32 a, %1, %2, %3;\n\tld.global.nc.u32 %0, [a];\n\t}"
+        : "=r"(v)
+        : "r"(off), "r"(four), "l"(base));
+    return v;
+}
+
+// Loads of step s.  Ring column c, ring row rho live at offset
+// o0 + (c + rho) * Hs + rho, so every access of a step is on diagonal D0 + s
+// (+ a step-independent shift); 32-bit offsets from the frame base let ptxas
+// form each address with one IMAD.WIDE.
 template <bool EDGE>
 __device__ __forceinline__ Loads fetch(const Task& T, int s) {
     Loads L{0, 0, 0, 0, 0, 0};
@@ -234,27 +250,28 @@ __device__ __forceinline__ Loads fetch(const Task& T, int s) {
     const int v = s - t;
     const int k = (s - t) & 31;
     const int w2 = T.w2;
-    const std::uint32_t* P = T.P0 + static_cast<long long>(s) * T.Hs;  // diagonal D0 + s
-    const long long h = T.Hs;
+    const std::uint32_t ob = T.o0 + static_cast<std::uint32_t>(s) * T.Hs + t;  // diag D0+s, row t
     if (!EDGE || (v >= 0 && v < T.NV)) {
-        L.a = P[w2 * h + t + w2];  // new row t+w2, entering column v
-        L.b = P[t];                // old row t,    entering column v
+        L.a = ld_off(T.Sf, ob + T.dA, T.M.four);  // new row t+w2, entering column v
+        L.b = ld_off(T.Sf, ob, T.M.four);         // old row t,    entering column v
         if (!EDGE || v >= w2) {
-            L.c = P[t + w2];          // new row, leaving column v - w2
-            L.d = P[-w2 * h + t];     // old row, leaving column v - w2
+            L.c = ld_off(T.Sf, ob + w2, T.M.four);     // new row, leaving column v - w2
+            L.d = ld_off(T.Sf, ob - T.dD, T.M.four);   // old row, leaving column v - w2
         }
     }
     const int vi = s - k + 32;
     if (!EDGE || (k < w2 && vi >= 0 && vi < T.NV)) {
-        L.i1 = P[32 * h + k];  // init: column vi, row k
-        if (!EDGE || vi >= w2) L.i2 = P[(32 - w2) * h + k];
+        const std::uint32_t oi = ob - t + k;
+        L.i1 = ld_off(T.Sf, oi + T.dI, T.M.four);  // init: column vi, row k
+        if (!EDGE || vi >= w2) L.i2 = ld_off(T.Sf, oi + T.dI2, T.M.four);
     }
     return L;
 }
 
 // L2 prefetch of the 64 band rows of the diagonal the init reads at step s.
 __device__ __forceinline__ void prefetch_l2(const Task& T, int s) {
-    const std::uint32_t* p = T.P0 + (static_cast<long long>(s) + 32) * T.Hs + T.lane;
+    const std::uint32_t o = T.o0 + static_cast<std::uint32_t>(s) * T.Hs + T.dI + T.lane;
+    const std::uint32_t* p = T.Sf + o;
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 32));
 }
@@ -338,8 +355,12 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
     const int per_frame = g.nbands * g.nsegs;
     Task T;
     T.M = M;
-    T.Hs = sg.Hs;
+    T.Hs = static_cast<std::uint32_t>(sg.Hs);
     T.w2 = 2 * r + 1;
+    T.dA = T.w2 * T.Hs + T.w2;
+    T.dD = T.w2 * T.Hs;
+    T.dI = 32u * T.Hs;
+    T.dI2 = (32u - T.w2) * T.Hs;
     T.lane = lane;
     T.stride = static_cast<std::size_t>(a.width) * 3;
 
@@ -364,8 +385,9 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
         // ring column c = image column xs - r + c, ring row rho = image row yb - r + rho;
         // element (d, y) of the plane at d * Hs + (y - y_base), d = x + (y - y_base).
         const int R0 = yb - r - sg.y_base;
-        const long long D0 = static_cast<long long>(xs - r) + R0;
-        T.P0 = S + sg.frame_elems * f + D0 * T.Hs + R0;
+        const std::uint32_t D0 = static_cast<std::uint32_t>(xs - r + R0);
+        T.Sf = S + sg.frame_elems * f;
+        T.o0 = D0 * T.Hs + R0;
 
         unsigned long long win[NB];
 #pragma unroll
@@ -459,12 +481,16 @@ cudaError_t launch_nb(const BandArgs& a, int* counter, void* scratch, int num_sm
 
     e = cudaMemsetAsync(counter, 0, sizeof(int), s);
     if (e != cudaSuccess) return e;
-    const Mul M{16u, 0xFFFFFFF0u};
+    const Mul M{16u, 0xFFFFFFF0u, 4u};
     skew_kernel<NB><<<static_cast<unsigned>(blocks), warps * 32, smem, s>>>(a, S, sg, counter, g, M);
     return cudaGetLastError();
 }
 
 }  // namespace
+
+bool skew_fits(const BandArgs& a) {
+    return shear_geom(a).frame_elems < (1ull << 32) - 64;
+}
 
 bool skew_supported(int levels, int radius) {
     return levels >= 1 && levels + 1 <= 32 && radius >= 0 && radius <= 15 &&

@@ -4,6 +4,10 @@ usage: python scripts/sass_loop_mix.py <object> <mangled-kernel-name> [min_len m
 import collections, re, subprocess, sys
 
 obj, fn = sys.argv[1], sys.argv[2]
+if not fn.startswith("_Z"):  # a regex: resolve the mangled name
+    names = re.findall(r"Function : (\S+)", subprocess.run(["cuobjdump", "-sass", obj],
+                       capture_output=True, text=True).stdout)
+    fn = next(n for n in names if re.search(fn, n))
 lo, hi = (int(sys.argv[3]), int(sys.argv[4])) if len(sys.argv) > 4 else (300, 2000)
 sass = subprocess.run(["cuobjdump", "-sass", "-fun", fn, obj], capture_output=True, text=True).stdout
 ins = []
