@@ -10,7 +10,8 @@ import ctypes
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "liboilpaint_b200.so"
+LIB_PATH = Path(os.environ.get("OILPAINT_B200_LIB",
+                               Path(__file__).resolve().parent / "liboilpaint_b200.so"))
 
 OPC_OK, OPC_EINVAL, OPC_ECUDA, OPC_ENOMEM = 0, 1, 2, 3
 OPC_FLAG_DEVICE_POINTERS = 0x1

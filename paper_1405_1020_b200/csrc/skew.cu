@@ -177,6 +177,11 @@ __device__ __forceinline__ void rmw_sub_m(unsigned long long* Es, std::uint32_t 
     packed_sub(Es + (e >> 26) * kSlots, entry_lo(e) & mask, entry_r1(e), nm16);
 }
 
+// Lowest-index bin with the largest count (filter.hpp:71-82) and its truncated
+// channel averages (filter.cpp:41-43), packed R | G << 8 | B << 16.  Static
+// tournament: hi_b > (hi_a | 0x3FFFFF) <=> count_b > count_a; ties keep the
+// left (lower-bin) operand.  (Moving part of the first level onto the FMA pipe
+// with IMAD-based selects was measured slower: profiles/r01_notes.md.)
 template <int NB>
 __device__ __forceinline__ std::uint32_t winner_rgb(const unsigned long long (&w)[NB],
                                                     const std::uint32_t* recip) {
