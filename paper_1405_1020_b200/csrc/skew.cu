@@ -83,8 +83,10 @@ __device__ __forceinline__ std::uint32_t make_entry(std::uint32_t r, std::uint32
 
 // Sheared entry plane.  Block: 32 rows x 128 columns staged through shared
 // memory, then written diagonal by diagonal (lane = row -> contiguous).
-__global__ void __launch_bounds__(256) shear_kernel(BandArgs a, std::uint32_t* S, ShearGeom g) {
+__global__ void __launch_bounds__(256)
+    shear_kernel(BandArgs a, std::uint32_t* S, ShearGeom g, int vec_ok) {
     __shared__ std::uint32_t tile[kShearRows * kShearStride];
+    __shared__ uint4 raw[kShearRows * (kShearCols * 3 / 16)];  // 32 rows x 384 B
     const int x0 = blockIdx.x * kShearCols;
     const int y0 = g.y_base + blockIdx.y * kShearRows;
     const int frame = blockIdx.z;
@@ -93,21 +95,45 @@ __global__ void __launch_bounds__(256) shear_kernel(BandArgs a, std::uint32_t* S
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const std::size_t stride = static_cast<std::size_t>(a.width) * 3;
     const int in_hi = a.in_row0 + a.in_rows;
+    constexpr int kQ = kShearCols * 3 / 16;  // 24 uint4 per tile row
+    if (vec_ok && x0 + kShearCols <= a.width && y0 + kShearRows <= in_hi) {
+        // Interior tile: 16-byte loads of the raw rows, then split into entries.
+        for (int i = threadIdx.x; i < kShearRows * kQ; i += blockDim.x) {
+            const int row = i / kQ, q = i - row * kQ;
+            const uint4* src = reinterpret_cast<const uint4*>(
+                in + static_cast<std::size_t>(y0 + row - a.in_row0) * stride +
+                static_cast<std::size_t>(x0) * 3);
+            raw[i] = __ldg(src + q);
+        }
+        __syncthreads();
+        const std::uint8_t* rb = reinterpret_cast<const std::uint8_t*>(raw);
 #pragma unroll
-    for (int k = 0; k < kShearRows / 8; ++k) {
-        const int row = warp + 8 * k;
-        const int y = y0 + row;
+        for (int k = 0; k < kShearRows / 8; ++k) {
+            const int row = warp + 8 * k;
 #pragma unroll
-        for (int j = 0; j < kShearCols / 32; ++j) {
-            const int c = lane + 32 * j;
-            const int x = x0 + c;
-            std::uint32_t e = 0;
-            if (x < a.width && y < in_hi) {
-                const std::uint8_t* p = in + static_cast<std::size_t>(y - a.in_row0) * stride +
-                                        static_cast<std::size_t>(x) * 3;
-                e = make_entry(p[0], p[1], p[2], a.bin_mul);
+            for (int j = 0; j < kShearCols / 32; ++j) {
+                const int c = lane + 32 * j;
+                const std::uint8_t* p = rb + row * (kShearCols * 3) + c * 3;
+                tile[row * kShearStride + c] = make_entry(p[0], p[1], p[2], a.bin_mul);
             }
-            tile[row * kShearStride + c] = e;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kShearRows / 8; ++k) {
+            const int row = warp + 8 * k;
+            const int y = y0 + row;
+#pragma unroll
+            for (int j = 0; j < kShearCols / 32; ++j) {
+                const int c = lane + 32 * j;
+                const int x = x0 + c;
+                std::uint32_t e = 0;
+                if (x < a.width && y < in_hi) {
+                    const std::uint8_t* p = in + static_cast<std::size_t>(y - a.in_row0) * stride +
+                                            static_cast<std::size_t>(x) * 3;
+                    e = make_entry(p[0], p[1], p[2], a.bin_mul);
+                }
+                tile[row * kShearStride + c] = e;
+            }
         }
     }
     __syncthreads();
@@ -460,7 +486,10 @@ cudaError_t launch_nb(const BandArgs& a, int* counter, void* scratch, int num_sm
     {
         const dim3 grid(static_cast<unsigned>((a.width + kShearPad + kShearCols - 1) / kShearCols),
                         static_cast<unsigned>(sg.Hs / kShearRows), static_cast<unsigned>(a.frames));
-        shear_kernel<<<grid, 256, 0, s>>>(a, S, sg);
+        const int vec_ok = (reinterpret_cast<std::uintptr_t>(a.in) % 16 == 0) &&
+                           ((static_cast<std::size_t>(a.width) * 3) % 16 == 0) &&
+                           (a.in_frame_stride % 16 == 0);
+        shear_kernel<<<grid, 256, 0, s>>>(a, S, sg, vec_ok);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }

@@ -10,3 +10,8 @@ timeout 300 python scripts/prof_run.py --config c4 --steps 1 > gpurun_out/plain.
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:skew -c 1 -o gpurun_out/prof_skew_c4 -f python scripts/prof_run.py --config c4 --steps 1 > gpurun_out/ncu.log 2>&1
 echo "ncu rc=$?" >> gpurun_out/ncu.log
 fi
+if [ "$1" = "launches" ]; then
+timeout 300 python scripts/prof_run.py --config c4 --steps 2 > gpurun_out/plain.log 2>&1 && \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python scripts/prof_run.py --config c4 --steps 2 > gpurun_out/ncu_launch.log 2>&1
+echo "ncu rc=$?" >> gpurun_out/ncu_launch.log
+fi
