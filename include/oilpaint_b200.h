@@ -61,6 +61,7 @@ extern "C" {
 #define OPC_KERNEL_AUTO 0
 #define OPC_KERNEL_DIRECT 1 /* one thread per output pixel, O(r^2), any r and L  */
 #define OPC_KERNEL_SKEW 2   /* warp-skewed column-difference sliding, L+1 <= 32, r <= 15 */
+#define OPC_KERNEL_SLIDE 3  /* per-lane O(r) sliding histogram, any L, r <= 15 (L+1 > 32 default) */
 
 typedef struct opc_config {
     int32_t device;  /* CUDA device ordinal; -1 = current device              */

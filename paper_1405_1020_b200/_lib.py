@@ -16,7 +16,7 @@ LIB_PATH = Path(os.environ.get("OILPAINT_B200_LIB",
 OPC_OK, OPC_EINVAL, OPC_ECUDA, OPC_ENOMEM = 0, 1, 2, 3
 OPC_FLAG_DEVICE_POINTERS = 0x1
 OPC_FLAG_ALLOW_LEVELS_256 = 0x2
-OPC_KERNEL_AUTO, OPC_KERNEL_DIRECT, OPC_KERNEL_SKEW = 0, 1, 2
+OPC_KERNEL_AUTO, OPC_KERNEL_DIRECT, OPC_KERNEL_SKEW, OPC_KERNEL_SLIDE = 0, 1, 2, 3
 
 # Every symbol include/oilpaint_b200.h and include/oilpaint_b200_patterns.h declare.
 EXPORTS = (

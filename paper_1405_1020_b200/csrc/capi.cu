@@ -150,7 +150,12 @@ int ensure(void** p, std::size_t* cap, std::size_t need) {
 int plan(int levels, int radius, int forced) {
     if (forced == OPC_KERNEL_DIRECT) return OPC_KERNEL_DIRECT;
     if (forced == OPC_KERNEL_SKEW) return opc::skew_supported(levels, radius) ? OPC_KERNEL_SKEW : -1;
-    return opc::skew_supported(levels, radius) ? OPC_KERNEL_SKEW : OPC_KERNEL_DIRECT;
+    if (forced == OPC_KERNEL_SLIDE) {
+        return opc::slide_supported(levels, radius) ? OPC_KERNEL_SLIDE : -1;
+    }
+    if (opc::skew_supported(levels, radius)) return OPC_KERNEL_SKEW;
+    if (opc::slide_supported(levels, radius)) return OPC_KERNEL_SLIDE;
+    return OPC_KERNEL_DIRECT;
 }
 
 // Runs the filter on device buffers already holding the band input.
@@ -166,11 +171,19 @@ int run_device(const opc::BandArgs& a, int border, int kernel, DevCtx* ctx, cuda
         if (rc != OPC_OK) return rc;
         e = opc::launch_skew(a, counter, ctx->d_scratch, ctx->num_sms, s);
         if (e != cudaSuccess) return cuda_error(e, "skew kernel launch");
+    } else if (kernel == OPC_KERNEL_SLIDE) {
+        int* counter = ctx->d_counter + (ctx->counter_idx++ & 63u);
+        const int rc = ensure(&ctx->d_scratch, &ctx->scratch_cap, opc::slide_scratch_bytes(a));
+        if (rc != OPC_OK) return rc;
+        e = opc::launch_slide(a, counter, ctx->d_scratch, ctx->num_sms, s);
+        if (e != cudaSuccess) return cuda_error(e, "slide kernel launch");
     } else {
         e = opc::launch_direct(a, s);
         if (e != cudaSuccess) return cuda_error(e, "direct kernel launch");
     }
-    if (a.y_hi > a.y_lo && a.x_hi > a.x_lo) g_launches.fetch_add(kernel == OPC_KERNEL_SKEW ? 2 : 1);
+    if (a.y_hi > a.y_lo && a.x_hi > a.x_lo) {
+        g_launches.fetch_add(kernel == OPC_KERNEL_DIRECT ? 1 : 2);  // + the pre-pass
+    }
     e = opc::launch_border(a, border, s);
     if (e != cudaSuccess) return cuda_error(e, "border kernel launch");
     if (a.radius > 0) g_launches.fetch_add(1);

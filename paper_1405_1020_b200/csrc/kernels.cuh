@@ -53,4 +53,11 @@ std::size_t skew_scratch_bytes(const BandArgs& a);
 cudaError_t launch_skew(const BandArgs& a, int* task_counter, void* scratch, int num_sms,
                         cudaStream_t s);
 
+// Slide family (any L <= 256, r <= 15; the default for L+1 > 32): needs a
+// transposed entry plane of slide_scratch_bytes(a) bytes.
+bool slide_supported(int levels, int radius);
+std::size_t slide_scratch_bytes(const BandArgs& a);
+cudaError_t launch_slide(const BandArgs& a, int* task_counter, void* scratch, int num_sms,
+                         cudaStream_t s);
+
 }  // namespace opc

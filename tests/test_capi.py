@@ -105,7 +105,8 @@ def test_kernel_planner():
     assert opc.plan_kernel(640, 480, 2, 20) == _lib.OPC_KERNEL_SKEW
     assert opc.plan_kernel(16384, 16384, 15, 20) == _lib.OPC_KERNEL_SKEW
     assert opc.plan_kernel(3840, 2160, 7, 30) == _lib.OPC_KERNEL_SKEW
-    assert opc.plan_kernel(4096, 4096, 10, 256) == _lib.OPC_KERNEL_DIRECT
+    assert opc.plan_kernel(4096, 4096, 10, 256) == _lib.OPC_KERNEL_SLIDE
+    assert opc.plan_kernel(300, 300, 15, 100) == _lib.OPC_KERNEL_SLIDE
     assert opc.plan_kernel(100, 100, 16, 20) == _lib.OPC_KERNEL_DIRECT
     assert opc.plan_kernel(8, 8, 4, 20) == -1
 

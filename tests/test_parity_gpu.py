@@ -23,7 +23,7 @@ from test_oracle import load_cases, ppm_payload
 pytestmark = pytest.mark.gpu
 
 GOLDEN = Path(__file__).resolve().parent / "golden"
-AUTO, DIRECT, SKEW = 0, 1, 2
+AUTO, DIRECT, SKEW, SLIDE = 0, 1, 2, 3
 
 
 def run(opc, img, r, L, border=0, kernel=AUTO, allow256=False):
@@ -35,6 +35,10 @@ def skew_ok(r, L):
     return L + 1 <= 32 and r <= 15
 
 
+def slide_ok(r, L):
+    return r <= 15
+
+
 def test_reference_fixture_cases_all_kernels(gpu):
     n = 0
     for w, h, r, L, border, src, img, want in load_cases():
@@ -43,6 +47,8 @@ def test_reference_fixture_cases_all_kernels(gpu):
         assert np.array_equal(run(gpu, img, r, L, border, DIRECT, allow), want), (w, h, r, L)
         if skew_ok(r, L):
             assert np.array_equal(run(gpu, img, r, L, border, SKEW), want), (w, h, r, L, border)
+        if slide_ok(r, L):
+            assert np.array_equal(run(gpu, img, r, L, border, SLIDE, allow), want), (w, h, r, L)
         n += 1
     assert n == 296
 
@@ -50,7 +56,7 @@ def test_reference_fixture_cases_all_kernels(gpu):
 def test_golden_ppm(gpu):
     _, _, golden = ppm_payload(GOLDEN / "gradient8_r2_l20_zero.ppm")
     img = gpu.generate(gpu.Pattern.GRADIENT, 8, 8)
-    for k in (AUTO, DIRECT, SKEW):
+    for k in (AUTO, DIRECT, SKEW, SLIDE):
         assert np.array_equal(run(gpu, img, 2, 20, 1, k), golden)
 
 
@@ -89,6 +95,34 @@ def test_skew_radius_levels_grid(gpu, r, L):
     img = rng.integers(0, 256, (h, w, 3), dtype=np.uint8)
     want = oracle_lib.oracle_filter(img, r, L, 0, threads=4)
     assert np.array_equal(run(gpu, img, r, L, 0, SKEW), want)
+
+
+@pytest.mark.parametrize("r", [0, 1, 3, 10, 15])
+@pytest.mark.parametrize("L", [31, 40, 100, 255, 256])
+def test_slide_radius_levels_grid(gpu, r, L):
+    rng = np.random.default_rng(r * 1000 + L)
+    h = 2 * r + 1 + int(rng.integers(0, 70))
+    w = 2 * r + 1 + int(rng.integers(0, 300))
+    img = rng.integers(0, 256, (h, w, 3), dtype=np.uint8)
+    want = oracle_lib.oracle_filter(img, r, L, 0, threads=4)
+    assert np.array_equal(run(gpu, img, r, L, 0, SLIDE, L == 256), want)
+    if L + 1 > 32:
+        assert np.array_equal(run(gpu, img, r, L, 0, AUTO, L == 256), want)
+
+
+@pytest.mark.parametrize("L", [20, 255, 256])
+def test_slide_rectangles_and_ties(gpu, L):
+    """C3-like content: flat rectangles (winner changes at edges), plus
+    two-tone noise with many exact ties and pure white (bin L)."""
+    rng = np.random.default_rng(L)
+    img = gpu.generate(gpu.Pattern.RECTS, 300, 180, seed=L)
+    for r in (1, 4, 10, 15):
+        want = oracle_lib.oracle_filter(img, r, L, 0, threads=4)
+        assert np.array_equal(run(gpu, img, r, L, 0, SLIDE, L == 256), want), r
+    two = np.where(rng.random((90, 170, 1)) < 0.5, 255, 0).astype(np.uint8).repeat(3, 2)
+    for r in (2, 7):
+        want = oracle_lib.oracle_filter(two, r, L, 1, threads=4)
+        assert np.array_equal(run(gpu, two, r, L, 1, SLIDE, L == 256), want), r
 
 
 @pytest.mark.parametrize("content", ["flat", "smooth", "two_tone", "white"])
