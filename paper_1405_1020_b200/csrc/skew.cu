@@ -499,11 +499,14 @@ cudaError_t launch_nb(const BandArgs& a, int* counter, void* scratch, int num_sm
     const int iw = a.x_hi - a.x_lo;
     g.nbands = (rows + 31) / 32;
     const long long total_warps = static_cast<long long>(num_sms) * per_sm * warps;
-    // Aim for >= 4 tasks per resident warp, segments no narrower than 256.
+    // Aim for >= 4 tasks per resident warp with segments no narrower than 256
+    // columns (each task pays 2r+1 warm-up and 31 skew-fill steps); images too
+    // small to fill the GPU that way go down to 64-column segments.
     const long long want = 4 * total_warps;
     const long long per_seg = static_cast<long long>(g.nbands) * a.frames;
     int nsegs = static_cast<int>((want + per_seg - 1) / per_seg);
-    const int max_segs = (iw + 255) / 256;
+    const int min_w = per_seg * ((iw + 255) / 256) >= total_warps ? 256 : 64;
+    const int max_segs = (iw + min_w - 1) / min_w;
     if (nsegs > max_segs) nsegs = max_segs;
     if (nsegs < 1) nsegs = 1;
     g.segw = (iw + nsegs - 1) / nsegs;
