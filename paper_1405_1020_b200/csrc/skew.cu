@@ -37,7 +37,6 @@ namespace opc {
 namespace {
 
 constexpr int kMaxWarps = 12;
-constexpr int kSlots = 96;  // E ring slots
 constexpr int kStageStride = 34;  // == 2 (mod 32): skewed (row t, column s-t) writes hit distinct banks
 constexpr int kRecipBytes = 1024 * 4;
 constexpr int kShearRows = 32;
@@ -47,10 +46,6 @@ constexpr int kShearStride = kShearCols + 2;  // == 2 (mod 32): diagonal reads c
 // last output column (unused values) read up to column W + 32, and a zero
 // entry keeps their bin index in range.
 constexpr int kShearPad = 64;
-
-__host__ __device__ inline std::size_t per_warp_bytes(int nb) {
-    return static_cast<std::size_t>(nb) * kSlots * 8 + 32 * kStageStride * 4;
-}
 
 // Geometry of the sheared plane for a launch: rows [y_base, y_base + Hs) of
 // the image, diagonal d = x + (y - y_base), element (d, y) at d * Hs + (y - y_base).
@@ -64,8 +59,8 @@ struct ShearGeom {
 __host__ inline ShearGeom shear_geom(const BandArgs& a) {
     ShearGeom g{};
     g.y_base = a.y_lo - a.radius;
-    const int nbands = (a.y_hi - a.y_lo + 31) / 32;
-    g.Hs = 32 * nbands + 64;
+    const int nbands = (a.y_hi - a.y_lo + 63) / 64;  // 64-row bands cover 32-row ones too
+    g.Hs = 64 * nbands + 64;
     g.ndiag = a.width + kShearPad + g.Hs;
     g.frame_elems = static_cast<std::size_t>(g.ndiag) * g.Hs;
     return g;
@@ -185,22 +180,26 @@ __device__ __forceinline__ void packed_sub(unsigned long long* p, std::uint32_t 
     *p = r;
 }
 
-// E[bin(e)][slot] += / -= packed(e).  Es = E + slot.
+// E[bin(e)][slot] += / -= packed(e).  Es = E + slot, SL slots per bin row.
+template <int SL>
 __device__ __forceinline__ void rmw_add(unsigned long long* Es, std::uint32_t e, const Mul& M) {
-    packed_add(Es + (e >> 26) * kSlots, entry_lo(e), entry_r1(e), M.m16);
+    packed_add(Es + (e >> 26) * SL, entry_lo(e), entry_r1(e), M.m16);
 }
+template <int SL>
 __device__ __forceinline__ void rmw_sub(unsigned long long* Es, std::uint32_t e, const Mul& M) {
-    packed_sub(Es + (e >> 26) * kSlots, entry_lo(e), entry_r1(e), M.negm16);
+    packed_sub(Es + (e >> 26) * SL, entry_lo(e), entry_r1(e), M.negm16);
 }
 // Masked forms for the branch-free init: mask = all ones or zero, m16 = 16 or
 // 0, nm16 = -16 or 0.
+template <int SL>
 __device__ __forceinline__ void rmw_add_m(unsigned long long* Es, std::uint32_t e, std::uint32_t mask,
                                           std::uint32_t m16) {
-    packed_add(Es + (e >> 26) * kSlots, entry_lo(e) & mask, entry_r1(e), m16);
+    packed_add(Es + (e >> 26) * SL, entry_lo(e) & mask, entry_r1(e), m16);
 }
+template <int SL>
 __device__ __forceinline__ void rmw_sub_m(unsigned long long* Es, std::uint32_t e, std::uint32_t mask,
                                           std::uint32_t nm16) {
-    packed_sub(Es + (e >> 26) * kSlots, entry_lo(e) & mask, entry_r1(e), nm16);
+    packed_sub(Es + (e >> 26) * SL, entry_lo(e) & mask, entry_r1(e), nm16);
 }
 
 // Lowest-index bin with the largest count (filter.hpp:71-82) and its truncated
@@ -240,9 +239,26 @@ struct TaskGeom {
     int nbands, nsegs, segw, ntasks;
 };
 
-// Everything one step needs, per lane.
+// H halves per lane: lane t owns rows t + 32h (h < H) of a 32H-row band.  The
+// E chain runs down all 32H rows (lane 31 of half h hands column v to lane 0 of
+// half h+1 one step later), so E(v, band top) is built once per 32H rows and an
+// E slot lives 32 + 32H steps: 96 slots for H = 1, 128 for H = 2.
+template <int H>
+struct Halves {
+    static constexpr int kRows = 32 * H;
+    static constexpr int kSlots = H == 1 ? 96 : 128;
+    static constexpr int kMaxWarps = H == 1 ? 12 : 8;  // what fits 227 KB (NB = 21)
+};
+
+template <int NB, int H>
+__host__ __device__ inline std::size_t per_warp_bytes_h() {
+    return static_cast<std::size_t>(NB) * Halves<H>::kSlots * 8 + 32 * H * kStageStride * 4;
+}
+
+template <int H>
 struct Loads {
-    std::uint32_t a, b, c, d, i1, i2;
+    std::uint32_t a[H], b[H], c[H], d[H];
+    std::uint32_t i1, i2;
 };
 
 struct Task {
@@ -253,13 +269,13 @@ struct Task {
     std::uint32_t dA, dD, dI, dI2;  // w2*Hs + w2, w2*Hs, 32*Hs, (32-w2)*Hs
     std::uint8_t* out_row0;   // output row yb (band row 0), column 0
     int NV, X0, w2, lane;
-    bool rows_ok;             // all 32 rows of the band are interior rows
-    int y_rows;               // valid rows in the band (<= 32)
+    int y_rows;               // valid rows in the band (<= 32H)
     std::size_t stride;
 };
 
 // 32-bit element offset from a 64-bit base: one IMAD.WIDE (FMA pipe; the
-// runtime multiplier four = 4 keeps ptxas from turning it into ALU LEAs) and the load.
+// runtime multiplier four = 4 keeps ptxas from turning it into ALU LEAs) and the
+// load(s): rows r and r + 32 of the same diagonal share the address (+128 B).
 __device__ __forceinline__ std::uint32_t ld_off(const std::uint32_t* base, std::uint32_t off,
                                                 std::uint32_t four) {
     std::uint32_t v;
@@ -269,114 +285,154 @@ __device__ __forceinline__ std::uint32_t ld_off(const std::uint32_t* base, std::
         : "r"(off), "r"(four), "l"(base));
     return v;
 }
+__device__ __forceinline__ void ld_off2(const std::uint32_t* base, std::uint32_t off,
+                                        std::uint32_t four, std::uint32_t& v0,
+                                        std::uint32_t& v1) {
+    asm volatile(
+        "{\n\t.reg .u64 a;\n\tmad.wide.u32 a, %2, %3, %4;\n\tld.global.nc.u32 %0, [a];\n\t"
+        "ld.global.nc.u32 %1, [a+128];\n\t}"
+        : "=r"(v0), "=r"(v1)
+        : "r"(off), "r"(four), "l"(base));
+}
 
 // Loads of step s.  Ring column c, ring row rho live at offset
 // o0 + (c + rho) * Hs + rho, so every access of a step is on diagonal D0 + s
-// (+ a step-independent shift); 32-bit offsets from the frame base let ptxas
-// form each address with one IMAD.WIDE.
-template <bool EDGE>
-__device__ __forceinline__ Loads fetch(const Task& T, int s) {
-    Loads L{0, 0, 0, 0, 0, 0};
+// (+ a step-independent shift), 32 consecutive rows per access.
+template <int H, bool EDGE>
+__device__ __forceinline__ Loads<H> fetch(const Task& T, int s) {
+    Loads<H> L;
     const int t = T.lane;
-    const int v = s - t;
-    const int k = (s - t) & 31;
     const int w2 = T.w2;
     const std::uint32_t ob = T.o0 + static_cast<std::uint32_t>(s) * T.Hs + t;  // diag D0+s, row t
-    if (!EDGE || (v >= 0 && v < T.NV)) {
-        L.a = ld_off(T.Sf, ob + T.dA, T.M.four);  // new row t+w2, entering column v
-        L.b = ld_off(T.Sf, ob, T.M.four);         // old row t,    entering column v
-        if (!EDGE || v >= w2) {
-            L.c = ld_off(T.Sf, ob + w2, T.M.four);     // new row, leaving column v - w2
-            L.d = ld_off(T.Sf, ob - T.dD, T.M.four);   // old row, leaving column v - w2
+    const std::uint32_t four = T.M.four;
+    if (!EDGE && H == 2) {
+        ld_off2(T.Sf, ob + T.dA, four, L.a[0], L.a[H - 1]);  // new rows t+w2 (+32), entering
+        ld_off2(T.Sf, ob, four, L.b[0], L.b[H - 1]);         // old rows t (+32), entering
+        ld_off2(T.Sf, ob + w2, four, L.c[0], L.c[H - 1]);    // new rows, leaving
+        ld_off2(T.Sf, ob - T.dD, four, L.d[0], L.d[H - 1]);  // old rows, leaving
+    } else {
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+            const int v = s - t - 32 * h;
+            const std::uint32_t o = ob + 32 * h;
+            L.a[h] = L.b[h] = L.c[h] = L.d[h] = 0;
+            if (!EDGE || (v >= 0 && v < T.NV)) {
+                L.a[h] = ld_off(T.Sf, o + T.dA, four);
+                L.b[h] = ld_off(T.Sf, o, four);
+                if (!EDGE || v >= w2) {
+                    L.c[h] = ld_off(T.Sf, o + w2, four);
+                    L.d[h] = ld_off(T.Sf, o - T.dD, four);
+                }
+            }
         }
     }
+    const int k = (s - t) & 31;
     const int vi = s - k + 32;
+    L.i1 = L.i2 = 0;
     if (!EDGE || (k < w2 && vi >= 0 && vi < T.NV)) {
         const std::uint32_t oi = ob - t + k;
-        L.i1 = ld_off(T.Sf, oi + T.dI, T.M.four);  // init: column vi, row k
-        if (!EDGE || vi >= w2) L.i2 = ld_off(T.Sf, oi + T.dI2, T.M.four);
+        L.i1 = ld_off(T.Sf, oi + T.dI, four);  // init: column vi, row k
+        if (!EDGE || vi >= w2) L.i2 = ld_off(T.Sf, oi + T.dI2, four);
     }
     return L;
 }
 
-// L2 prefetch of the 64 band rows of the diagonal the init reads at step s.
+// L2 prefetch of the band rows of the diagonal the init reads at step s.
+template <int H>
 __device__ __forceinline__ void prefetch_l2(const Task& T, int s) {
     const std::uint32_t o = T.o0 + static_cast<std::uint32_t>(s) * T.Hs + T.dI + T.lane;
     const std::uint32_t* p = T.Sf + o;
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 32));
+#pragma unroll
+    for (int q = 0; q < H + 1; ++q) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 32 * q));
 }
 
-template <int NB, bool EDGE>
-__device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
-                                     unsigned long long (&win)[NB], unsigned long long* E,
+template <int NB, int H, bool EDGE>
+__device__ __forceinline__ void step(const Task& T, int s, const Loads<H>& cur,
+                                     unsigned long long (&win)[H][NB], unsigned long long* E,
                                      std::uint32_t* stage, const std::uint32_t* recip) {
+    constexpr int SL = Halves<H>::kSlots;
     const int t = T.lane;
-    const int v = s - t;
     const int w2 = T.w2;
-    if (!EDGE || (v >= 0 && v < T.NV)) {
-        const int slot = v % kSlots;
-        unsigned long long e[NB];
+    // All halves' dense reads first (their slots were finished at the previous
+    // step), so the RMW chains below do not serialise them.
+    unsigned long long e[H][NB];
 #pragma unroll
-        for (int b = 0; b < NB; ++b) e[b] = E[b * kSlots + slot];
-        if (!EDGE || (v >= w2 && t < T.y_rows)) {
-            stage[t * kStageStride + (v & 31)] = winner_rgb<NB>(win, recip);
-        }
+    for (int h = 0; h < H; ++h) {
+        const int v = s - t - 32 * h;
+        if (!EDGE || (v >= 0 && v < T.NV)) {
+            const int slot = v % SL;
 #pragma unroll
-        for (int b = 0; b < NB; ++b) win[b] += e[b];
-        // Advance E(v) from row yb+t to yb+t+1 for lane t+1.
-        unsigned long long* Es = E + slot;
-        rmw_add(Es, cur.a, T.M);
-        rmw_sub(Es, cur.b, T.M);
-        if (!EDGE || v >= w2) {
-            rmw_sub(Es, cur.c, T.M);
-            rmw_add(Es, cur.d, T.M);
+            for (int b = 0; b < NB; ++b) e[h][b] = E[b * SL + slot];
         }
     }
-    {  // one row of the from-scratch build of E(vi, yb)
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+        const int v = s - t - 32 * h;
+        if (!EDGE || (v >= 0 && v < T.NV)) {
+            const int slot = v % SL;
+            if (!EDGE || (v >= w2 && t + 32 * h < T.y_rows)) {
+                stage[(t + 32 * h) * kStageStride + (v & 31)] = winner_rgb<NB>(win[h], recip);
+            }
+#pragma unroll
+            for (int b = 0; b < NB; ++b) win[h][b] += e[h][b];
+            // Advance E(v) from row t + 32h to the next row (lane t+1, or half h+1).
+            unsigned long long* Es = E + slot;
+            rmw_add<SL>(Es, cur.a[h], T.M);
+            rmw_sub<SL>(Es, cur.b[h], T.M);
+            if (!EDGE || v >= w2) {
+                rmw_sub<SL>(Es, cur.c[h], T.M);
+                rmw_add<SL>(Es, cur.d[h], T.M);
+            }
+        }
+    }
+    {  // one row of the from-scratch build of E(vi, band top)
         const int k = (s - t) & 31;
         const int vi = s - k + 32;
-        const int islot = vi % kSlots;
+        const int islot = vi % SL;
         if (EDGE) {
             if (k < w2 && vi >= 0 && vi < T.NV) {
-                rmw_add(E + islot, cur.i1, T.M);
-                if (vi >= w2) rmw_sub(E + islot, cur.i2, T.M);
+                rmw_add<SL>(E + islot, cur.i1, T.M);
+                if (vi >= w2) rmw_sub<SL>(E + islot, cur.i2, T.M);
             }
         } else {
             // Branch-free: rows k >= w2 contribute zero (their entries are valid
             // memory, so the bin index stays in range).
             const std::uint32_t m = k < w2 ? ~0u : 0u;
-            rmw_add_m(E + islot, cur.i1, m, m & T.M.m16);
-            rmw_sub_m(E + islot, cur.i2, m, m & T.M.negm16);
+            rmw_add_m<SL>(E + islot, cur.i1, m, m & T.M.m16);
+            rmw_sub_m<SL>(E + islot, cur.i2, m, m & T.M.negm16);
         }
     }
     __syncwarp();
-    // Row fr just completed the 32-column block ending at v = s - fr.
+    // Rows fr + 32h just completed the 32-column block ending at v = s - fr - 32h.
     const int fr = (s + 1) & 31;
-    const int vv = s - fr - 31 + t;
-    if (!EDGE || (vv >= w2 && vv < T.NV && fr < T.y_rows)) {
-        const std::uint32_t rgb = stage[fr * kStageStride + t];
-        std::uint8_t* o = T.out_row0 + static_cast<std::size_t>(fr) * T.stride +
-                          static_cast<std::size_t>(T.X0 + vv) * 3;
-        o[0] = static_cast<std::uint8_t>(rgb);
-        o[1] = static_cast<std::uint8_t>(rgb >> 8);
-        o[2] = static_cast<std::uint8_t>(rgb >> 16);
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+        const int vv = s - fr - 31 + t - 32 * h;
+        if (!EDGE || (vv >= w2 && vv < T.NV && fr + 32 * h < T.y_rows)) {
+            const std::uint32_t rgb = stage[(fr + 32 * h) * kStageStride + t];
+            std::uint8_t* o = T.out_row0 + static_cast<std::size_t>(fr + 32 * h) * T.stride +
+                              static_cast<std::size_t>(T.X0 + vv) * 3;
+            o[0] = static_cast<std::uint8_t>(rgb);
+            o[1] = static_cast<std::uint8_t>(rgb >> 8);
+            o[2] = static_cast<std::uint8_t>(rgb >> 16);
+        }
     }
     __syncwarp();
 }
 
-template <int NB>
-__global__ void __launch_bounds__(kMaxWarps * 32)
+template <int NB, int H>
+__global__ void __launch_bounds__(Halves<H>::kMaxWarps * 32)
     skew_kernel(BandArgs a, const std::uint32_t* __restrict__ S, ShearGeom sg, int* task_counter,
                 TaskGeom g, Mul M) {
+    constexpr int SL = Halves<H>::kSlots;
     extern __shared__ __align__(16) unsigned char smem[];
     std::uint32_t* recip = reinterpret_cast<std::uint32_t*>(smem);
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int r = a.radius;
-    unsigned char* wbase = smem + kRecipBytes + warp * per_warp_bytes(NB);
+    unsigned char* wbase = smem + kRecipBytes + warp * per_warp_bytes_h<NB, H>();
     unsigned long long* E = reinterpret_cast<unsigned long long*>(wbase);
-    std::uint32_t* stage = reinterpret_cast<std::uint32_t*>(wbase + std::size_t(NB) * kSlots * 8);
+    std::uint32_t* stage = reinterpret_cast<std::uint32_t*>(wbase + std::size_t(NB) * SL * 8);
 
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
         recip[i] = i ? 0x80000000u / static_cast<std::uint32_t>(i) + 1u : 0u;
@@ -404,13 +460,12 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
         const int rem = task - f * per_frame;
         const int kb = rem / g.nsegs;
         const int js = rem - kb * g.nsegs;
-        const int yb = a.y_lo + 32 * kb;
+        const int yb = a.y_lo + Halves<H>::kRows * kb;
         const int xs = a.x_lo + js * g.segw;
         const int xe = min(xs + g.segw, a.x_hi);
         T.NV = T.w2 + (xe - xs);  // virtual columns: w2 warm-up + outputs
         T.X0 = xs - T.w2;         // image column of virtual column 0
-        T.y_rows = min(32, a.y_hi - yb);
-        T.rows_ok = T.y_rows == 32;
+        T.y_rows = min(Halves<H>::kRows, a.y_hi - yb);
         T.out_row0 = a.out + a.out_frame_stride * f +
                      static_cast<std::size_t>(yb - a.out_row0) * T.stride;
         // ring column c = image column xs - r + c, ring row rho = image row yb - r + rho;
@@ -420,34 +475,38 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
         T.Sf = S + sg.frame_elems * f;
         T.o0 = D0 * T.Hs + R0;
 
-        unsigned long long win[NB];
+        unsigned long long win[H][NB];
 #pragma unroll
-        for (int b = 0; b < NB; ++b) win[b] = 0ull;
+        for (int h = 0; h < H; ++h)
+#pragma unroll
+            for (int b = 0; b < NB; ++b) win[h][b] = 0ull;
 
-        const int nphases = ((T.NV - 1) >> 5) + 2;
-        const int p_steady_lo = (T.w2 + 62 + 31) >> 5;  // all lanes past warm-up and flush start
-        Loads cur = fetch<true>(T, -32);
+        const int nphases = ((T.NV - 1) >> 5) + 1 + H;
+        // steady: every lane of every half past warm-up, flush and band rows valid
+        const int p_steady_lo = (T.w2 + 62 + 32 * (H - 1) + 31) >> 5;
+        const bool rows_ok = T.y_rows == Halves<H>::kRows;
+        Loads<H> cur = fetch<H, true>(T, -32);
         for (int p = -1; p < nphases; ++p) {
             {  // zero the E slots of the columns initialised during this phase
-                const int slot = (32 * (p + 1) + lane) % kSlots;
+                const int slot = (32 * (p + 1) + lane) % SL;
 #pragma unroll
-                for (int b = 0; b < NB; ++b) E[b * kSlots + slot] = 0ull;
+                for (int b = 0; b < NB; ++b) E[b * SL + slot] = 0ull;
             }
             __syncwarp();
-            const bool steady = T.rows_ok && p >= p_steady_lo && 32 * p + 31 < T.NV;
+            const bool steady = rows_ok && p >= p_steady_lo && 32 * p + 31 < T.NV;
             if (steady) {
                 // Loads run two steps ahead; the diagonal first touched eight
                 // steps ahead (the init column's) is pulled into L2 now.
-                Loads n1 = fetch<false>(T, 32 * p + 1);
+                Loads<H> n1 = fetch<H, false>(T, 32 * p + 1);
 #pragma unroll 1
                 for (int ss = 0; ss < 32; ss += 2) {
                     const int s = 32 * p + ss;
-                    prefetch_l2(T, s + 8);
-                    const Loads n2 = fetch<false>(T, s + 2);
-                    step<NB, false>(T, s, cur, win, E, stage, recip);
-                    prefetch_l2(T, s + 9);
-                    const Loads n3 = fetch<false>(T, s + 3);
-                    step<NB, false>(T, s + 1, n1, win, E, stage, recip);
+                    prefetch_l2<H>(T, s + 8);
+                    const Loads<H> n2 = fetch<H, false>(T, s + 2);
+                    step<NB, H, false>(T, s, cur, win, E, stage, recip);
+                    prefetch_l2<H>(T, s + 9);
+                    const Loads<H> n3 = fetch<H, false>(T, s + 3);
+                    step<NB, H, false>(T, s + 1, n1, win, E, stage, recip);
                     cur = n2;
                     n1 = n3;
                 }
@@ -455,8 +514,8 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
 #pragma unroll 1
                 for (int ss = 0; ss < 32; ++ss) {
                     const int s = 32 * p + ss;
-                    const Loads nxt = fetch<true>(T, s + 1);
-                    step<NB, true>(T, s, cur, win, E, stage, recip);
+                    const Loads<H> nxt = fetch<H, true>(T, s + 1);
+                    step<NB, H, true>(T, s, cur, win, E, stage, recip);
                     cur = nxt;
                 }
             }
@@ -464,20 +523,21 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
     }
 }
 
-template <int NB>
-cudaError_t launch_nb(const BandArgs& a, int* counter, void* scratch, int num_sms,
-                      cudaStream_t s) {
-    const std::size_t pw = per_warp_bytes(NB);
+template <int NB, int H>
+cudaError_t launch_nbh(const BandArgs& a, int* counter, void* scratch, int num_sms,
+                       cudaStream_t s) {
+    const std::size_t pw = per_warp_bytes_h<NB, H>();
     const std::size_t limit = 227 * 1024;
-    int warps = kMaxWarps;
+    int warps = Halves<H>::kMaxWarps;
     while (warps > 1 && kRecipBytes + warps * pw > limit) --warps;
     const std::size_t smem = kRecipBytes + warps * pw;
-    cudaError_t e = cudaFuncSetAttribute(skew_kernel<NB>,
+    cudaError_t e = cudaFuncSetAttribute(skew_kernel<NB, H>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, skew_kernel<NB>, warps * 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, skew_kernel<NB, H>, warps * 32,
+                                                      smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
 
@@ -497,11 +557,11 @@ cudaError_t launch_nb(const BandArgs& a, int* counter, void* scratch, int num_sm
     TaskGeom g{};
     const int rows = a.y_hi - a.y_lo;
     const int iw = a.x_hi - a.x_lo;
-    g.nbands = (rows + 31) / 32;
+    g.nbands = (rows + Halves<H>::kRows - 1) / Halves<H>::kRows;
     const long long total_warps = static_cast<long long>(num_sms) * per_sm * warps;
     // Aim for >= 4 tasks per resident warp with segments no narrower than 256
-    // columns (each task pays 2r+1 warm-up and 31 skew-fill steps); images too
-    // small to fill the GPU that way go down to 64-column segments.
+    // columns (each task pays 2r+1 warm-up and 31 + 32(H-1) skew-fill steps);
+    // images too small to fill the GPU that way go down to 64-column segments.
     const long long want = 4 * total_warps;
     const long long per_seg = static_cast<long long>(g.nbands) * a.frames;
     int nsegs = static_cast<int>((want + per_seg - 1) / per_seg);
@@ -519,8 +579,19 @@ cudaError_t launch_nb(const BandArgs& a, int* counter, void* scratch, int num_sm
     e = cudaMemsetAsync(counter, 0, sizeof(int), s);
     if (e != cudaSuccess) return e;
     const Mul M{16u, 0xFFFFFFF0u, 4u};
-    skew_kernel<NB><<<static_cast<unsigned>(blocks), warps * 32, smem, s>>>(a, S, sg, counter, g, M);
+    skew_kernel<NB, H><<<static_cast<unsigned>(blocks), warps * 32, smem, s>>>(a, S, sg, counter,
+                                                                               g, M);
     return cudaGetLastError();
+}
+
+#ifndef OPC_SKEW_HALVES
+#define OPC_SKEW_HALVES 1  // H = 2 (64-row bands) measured slower: profiles/r01_notes.md
+#endif
+
+template <int NB>
+cudaError_t launch_nb(const BandArgs& a, int* counter, void* scratch, int num_sms,
+                      cudaStream_t s) {
+    return launch_nbh<NB, OPC_SKEW_HALVES>(a, counter, scratch, num_sms, s);
 }
 
 }  // namespace
