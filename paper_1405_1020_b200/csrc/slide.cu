@@ -25,7 +25,7 @@ namespace opc {
 
 namespace {
 
-constexpr int kWarps = 4;
+constexpr int kWarps = 8;  // upper bound; the launcher fits as many as 227 KB allows
 constexpr int kRingCols = 96;
 constexpr int kStageStride = 33;
 constexpr int kRecipBytes = 1024 * 4;
