@@ -36,12 +36,13 @@ namespace opc {
 
 namespace {
 
-constexpr int kMaxWarps = 12;
 constexpr int kStageStride = 34;  // == 2 (mod 32): skewed (row t, column s-t) writes hit distinct banks
 constexpr int kRecipBytes = 1024 * 4;
 constexpr int kShearRows = 32;
 constexpr int kShearCols = 128;
-constexpr int kShearStride = kShearCols + 2;  // == 2 (mod 32): diagonal reads conflict-free
+// Row stride 132 words: multiple of 4 (16-byte tile stores) and the diagonal
+// read address lane * 131 + dd hits 32 distinct banks (131 is odd).
+constexpr int kShearStride = kShearCols + 4;
 // Zero entries are written for columns [W, W + kShearPad): E columns past the
 // last output column (unused values) read up to column W + 32, and a zero
 // entry keeps their bin index in range.
@@ -76,12 +77,20 @@ __device__ __forceinline__ std::uint32_t make_entry(std::uint32_t r, std::uint32
     return b | (r << 8) | (g << 18) | (bin << 26);
 }
 
+// Entry from t = B | R << 8 | G << 16 (byte 3 ignored).
+__device__ __forceinline__ std::uint32_t entry_from_brg(std::uint32_t t, std::uint32_t bin_mul) {
+    const std::uint32_t bin = __umulhi(__dp4a(t, 0x00010101u, 0u), bin_mul);
+    return (t & 0xFFFFu) | ((t & 0x00FF0000u) << 2) | (bin << 26);
+}
+
 // Sheared entry plane.  Block: 32 rows x 128 columns staged through shared
 // memory, then written diagonal by diagonal (lane = row -> contiguous).
+// Interior tiles: each thread loads 3 words (4 pixels) per row straight from
+// global memory and splits them with byte permutes; row stride 132 words keeps
+// both the 16-byte tile stores and the diagonal reads conflict-free.
 __global__ void __launch_bounds__(256)
     shear_kernel(BandArgs a, std::uint32_t* S, ShearGeom g, int vec_ok) {
-    __shared__ std::uint32_t tile[kShearRows * kShearStride];
-    __shared__ uint4 raw[kShearRows * (kShearCols * 3 / 16)];  // 32 rows x 384 B
+    __shared__ __align__(16) std::uint32_t tile[kShearRows * kShearStride];
     const int x0 = blockIdx.x * kShearCols;
     const int y0 = g.y_base + blockIdx.y * kShearRows;
     const int frame = blockIdx.z;
@@ -90,27 +99,25 @@ __global__ void __launch_bounds__(256)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const std::size_t stride = static_cast<std::size_t>(a.width) * 3;
     const int in_hi = a.in_row0 + a.in_rows;
-    constexpr int kQ = kShearCols * 3 / 16;  // 24 uint4 per tile row
     if (vec_ok && x0 + kShearCols <= a.width && y0 + kShearRows <= in_hi) {
-        // Interior tile: 16-byte loads of the raw rows, then split into entries.
-        for (int i = threadIdx.x; i < kShearRows * kQ; i += blockDim.x) {
-            const int row = i / kQ, q = i - row * kQ;
-            const uint4* src = reinterpret_cast<const uint4*>(
-                in + static_cast<std::size_t>(y0 + row - a.in_row0) * stride +
-                static_cast<std::size_t>(x0) * 3);
-            raw[i] = __ldg(src + q);
-        }
-        __syncthreads();
-        const std::uint8_t* rb = reinterpret_cast<const std::uint8_t*>(raw);
+        std::uint32_t w[kShearRows / 8][3];
 #pragma unroll
         for (int k = 0; k < kShearRows / 8; ++k) {
-            const int row = warp + 8 * k;
+            const std::uint32_t* src = reinterpret_cast<const std::uint32_t*>(
+                in + static_cast<std::size_t>(y0 + warp + 8 * k - a.in_row0) * stride +
+                static_cast<std::size_t>(x0) * 3) + 3 * lane;
 #pragma unroll
-            for (int j = 0; j < kShearCols / 32; ++j) {
-                const int c = lane + 32 * j;
-                const std::uint8_t* p = rb + row * (kShearCols * 3) + c * 3;
-                tile[row * kShearStride + c] = make_entry(p[0], p[1], p[2], a.bin_mul);
-            }
+            for (int q = 0; q < 3; ++q) w[k][q] = __ldg(src + q);
+        }
+#pragma unroll
+        for (int k = 0; k < kShearRows / 8; ++k) {
+            // bytes R0 G0 B0 R1 | G1 B1 R2 G2 | B2 R3 G3 B3
+            uint4 e;
+            e.x = entry_from_brg(__byte_perm(w[k][0], w[k][1], 0x0102), a.bin_mul);
+            e.y = entry_from_brg(__byte_perm(w[k][0], w[k][1], 0x0435), a.bin_mul);
+            e.z = entry_from_brg(__byte_perm(w[k][1], w[k][2], 0x0324), a.bin_mul);
+            e.w = entry_from_brg(__byte_perm(w[k][2], w[k][2], 0x0213), a.bin_mul);
+            *reinterpret_cast<uint4*>(&tile[(warp + 8 * k) * kShearStride + 4 * lane]) = e;
         }
     } else {
 #pragma unroll
@@ -132,14 +139,25 @@ __global__ void __launch_bounds__(256)
         }
     }
     __syncthreads();
-    const int ymax = g.y_base + g.Hs;
-    for (int dd = warp; dd < kShearCols + kShearRows - 1; dd += 8) {
-        const int c = dd - lane;
-        const int x = x0 + c, y = y0 + lane;
-        if (c >= 0 && c < kShearCols && x < a.width + kShearPad && y < ymax) {
-            const std::size_t d = static_cast<std::size_t>(x + (y - g.y_base));
-            Sf[d * g.Hs + (y - g.y_base)] = tile[lane * kShearStride + c];
-        }
+    // Element (x, y) -> (x + yo) * Hs + yo with yo = y - y_base; for row lane of
+    // the tile and diagonal dd = c + lane that is base + dd * Hs.  The grid
+    // covers exactly Hs rows, so only the column range needs a check.
+    // (32-bit element offsets: skew_fits() bounds the plane of a frame.)
+    const int yoff = y0 - g.y_base;
+    const std::uint32_t Hs = static_cast<std::uint32_t>(g.Hs);
+    std::uint32_t off = static_cast<std::uint32_t>(x0 + yoff + warp) * Hs + yoff + lane;
+    const std::uint32_t* src = tile + lane * (kShearStride - 1) + warp;
+    const unsigned cmax = static_cast<unsigned>(min(kShearCols, a.width + kShearPad - x0));
+    const int c0 = warp - lane;
+#pragma unroll
+    for (int i = 0; i < (kShearCols + kShearRows + 6) / 8; ++i) {  // dd = warp + 8i <= 158
+        const std::uint32_t v = src[8 * i];
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t.reg .u64 a;\n\tsetp.lt.u32 p, %0, %1;\n\t"
+            "mad.wide.u32 a, %2, 4, %3;\n\t@p st.global.u32 [a], %4;\n\t}"
+            ::"r"(static_cast<unsigned>(c0 + 8 * i)), "r"(cmax), "r"(off), "l"(Sf), "r"(v)
+            : "memory");
+        off += 8 * Hs;
     }
 }
 
@@ -546,9 +564,9 @@ cudaError_t launch_nbh(const BandArgs& a, int* counter, void* scratch, int num_s
     {
         const dim3 grid(static_cast<unsigned>((a.width + kShearPad + kShearCols - 1) / kShearCols),
                         static_cast<unsigned>(sg.Hs / kShearRows), static_cast<unsigned>(a.frames));
-        const int vec_ok = (reinterpret_cast<std::uintptr_t>(a.in) % 16 == 0) &&
-                           ((static_cast<std::size_t>(a.width) * 3) % 16 == 0) &&
-                           (a.in_frame_stride % 16 == 0);
+        const int vec_ok = (reinterpret_cast<std::uintptr_t>(a.in) % 4 == 0) &&
+                           ((static_cast<std::size_t>(a.width) * 3) % 4 == 0) &&
+                           (a.in_frame_stride % 4 == 0);
         shear_kernel<<<grid, 256, 0, s>>>(a, S, sg, vec_ok);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
