@@ -166,8 +166,22 @@ __global__ void __launch_bounds__(256)
 // "r1 * 16 + hi (+ carry)" as one IMAD.X on the FMA pipe instead of folding it
 // into shifts on the ALU pipe, which is the kernel's binding resource.
 struct Mul {
-    std::uint32_t m16, negm16, four;  // 16, -16, 4
+    std::uint32_t m16, negm16, four, one;  // 16, -16, 4, 1
 };
+
+#ifndef OPC_SKEW_WIDE_BINS
+#define OPC_SKEW_WIDE_BINS 0
+#endif
+
+// w += e entirely on the FMA pipe: IMAD.WIDE.U32 adds the low word with its
+// carry into the 64-bit w, IMAD adds the high word (one = 1 at run time).
+__device__ __forceinline__ void wide_add(unsigned long long& w, unsigned long long e,
+                                         std::uint32_t one) {
+    asm("{\n\t.reg .u32 el, eh, wl, wh;\n\t.reg .u64 t;\n\t"
+        "mov.b64 {el, eh}, %1;\n\tmad.wide.u32 t, el, %2, %0;\n\t"
+        "mov.b64 {wl, wh}, t;\n\tmad.lo.u32 wh, eh, %2, wh;\n\tmov.b64 %0, {wl, wh};\n\t}"
+        : "+l"(w) : "l"(e), "r"(one));
+}
 
 __device__ __forceinline__ std::uint32_t entry_lo(std::uint32_t e) { return e & 0x03FC00FFu; }
 __device__ __forceinline__ std::uint32_t entry_r1(std::uint32_t e) {
@@ -225,9 +239,78 @@ __device__ __forceinline__ void rmw_sub_m(unsigned long long* Es, std::uint32_t 
 // tournament: hi_b > (hi_a | 0x3FFFFF) <=> count_b > count_a; ties keep the
 // left (lower-bin) operand.  (Moving part of the first level onto the FMA pipe
 // with IMAD-based selects was measured slower: profiles/r01_notes.md.)
+#ifndef OPC_ARGMAX_SCAN
+#define OPC_ARGMAX_SCAN 1
+#endif
+#ifndef OPC_ARGMAX_SEL_BINS
+#define OPC_ARGMAX_SEL_BINS 0
+#endif
+#ifndef OPC_ARGMAX_GROUPS
+#define OPC_ARGMAX_GROUPS 1  // 3, 4, 7 measured slower (more instructions)
+#endif
+
+// Conditional copy on the FMA pipe: if (p) d = a * one (one = 1 at run time,
+// so ptxas cannot turn the predicated IMAD into an ALU select).
+__device__ __forceinline__ void pick_if_ge(std::uint32_t& lo, std::uint32_t& hi, std::uint32_t bl,
+                                           std::uint32_t bh, std::uint32_t T, std::uint32_t one) {
+    asm("{\n\t.reg .pred p;\n\tsetp.ge.u32 p, %3, %4;\n\t"
+        "@p mad.lo.u32 %0, %2, %5, 0;\n\t@p mad.lo.u32 %1, %3, %5, 0;\n\t}"
+        : "+r"(lo), "+r"(hi)
+        : "r"(bl), "r"(bh), "r"(T), "r"(one));
+}
+
 template <int NB>
 __device__ __forceinline__ std::uint32_t winner_rgb(const unsigned long long (&w)[NB],
-                                                    const std::uint32_t* recip) {
+                                                    const std::uint32_t* recip, std::uint32_t one) {
+#if OPC_ARGMAX_SCAN
+    // Max-scan: the largest hi word carries the largest count c* (its low 22
+    // bits are sums, irrelevant to the count).  T = c* << 22; then a scan from
+    // the top bin down keeps the last (= lowest-index) bin with hi >= T, i.e.
+    // count == c*.  The max is an ALU min/max tree; the conditional copies are
+    // predicated IMADs on the FMA pipe, which has the spare issue slots.
+    // Balanced max tree (short dependency chains: few warps per scheduler).
+    std::uint32_t mx[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) mx[b] = static_cast<std::uint32_t>(w[b] >> 32);
+#pragma unroll
+    for (int step = 1; step < NB; step *= 3) {
+#pragma unroll
+        for (int i = 0; i + step < NB; i += 3 * step) {
+            mx[i] = max(mx[i], mx[i + step]);
+            if (i + 2 * step < NB) mx[i] = max(mx[i], mx[i + 2 * step]);
+        }
+    }
+    const std::uint32_t T = mx[0] & 0xFFC00000u;
+    // G independent scans over groups of bins, then the groups merged the
+    // same way (a group without a hit keeps its top bin, whose hi < T).
+    constexpr int G = OPC_ARGMAX_GROUPS;
+    constexpr int GS = (NB + G - 1) / G;
+    std::uint32_t glo[G], ghi[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const int b0 = g * GS, b1 = min(NB, b0 + GS) - 1;
+        if (b0 > b1) continue;
+        glo[g] = static_cast<std::uint32_t>(w[b1]);
+        ghi[g] = static_cast<std::uint32_t>(w[b1] >> 32);
+#pragma unroll
+        for (int b = b1 - 1; b >= b0; --b) {
+            const std::uint32_t bl = static_cast<std::uint32_t>(w[b]);
+            const std::uint32_t bh = static_cast<std::uint32_t>(w[b] >> 32);
+            if (b < OPC_ARGMAX_SEL_BINS) {
+                const bool p = bh >= T;
+                glo[g] = p ? bl : glo[g];
+                ghi[g] = p ? bh : ghi[g];
+            } else {
+                pick_if_ge(glo[g], ghi[g], bl, bh, T, one);
+            }
+        }
+    }
+    int last = G - 1;
+    while (last * GS >= NB) --last;
+    std::uint32_t lo = glo[last], hi = ghi[last];
+#pragma unroll
+    for (int g = last - 1; g >= 0; --g) pick_if_ge(lo, hi, glo[g], ghi[g], T, one);
+#else
     unsigned long long t[NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b) t[b] = w[b];
@@ -242,6 +325,7 @@ __device__ __forceinline__ std::uint32_t winner_rgb(const unsigned long long (&w
     }
     const std::uint32_t lo = static_cast<std::uint32_t>(t[0]);
     const std::uint32_t hi = static_cast<std::uint32_t>(t[0] >> 32);
+#endif
     const std::uint32_t count = hi >> 22;
     const std::uint32_t m = recip[count];
     const std::uint32_t sr = (hi >> 4) & 0x3FFFFu;
@@ -253,30 +337,52 @@ __device__ __forceinline__ std::uint32_t winner_rgb(const unsigned long long (&w
     return qr | (qg << 8) | (qb << 16);
 }
 
+// Work split.  The units are band columns, linearised (frame, band, column);
+// chunk i < nstatic is [i*s1, (i+1)*s1) -- one per resident warp, taken at
+// launch, together most of the work -- and the rest is handed out in chunks of
+// s2 units by the same atomic counter.  Every warp runs at the same rate (the
+// step costs do not depend on the pixels), so equal static shares leave no
+// tail; the dynamic remainder absorbs per-SM speed differences.  A chunk that
+// crosses a band end is run as two passes.
 struct TaskGeom {
-    int nbands, nsegs, segw, ntasks;
+    int nbands, iw, pitch;  // pitch >= iw: units per band (segment-aligned chunks)
+    int nstatic, nchunks;
+    long long units, s1, s2;
 };
 
-// H halves per lane: lane t owns rows t + 32h (h < H) of a 32H-row band.  The
-// E chain runs down all 32H rows (lane 31 of half h hands column v to lane 0 of
-// half h+1 one step later), so E(v, band top) is built once per 32H rows and an
-// E slot lives 32 + 32H steps: 96 slots for H = 1, 128 for H = 2.
-template <int H>
-struct Halves {
-    static constexpr int kRows = 32 * H;
-    static constexpr int kSlots = H == 1 ? 96 : 128;
-    static constexpr int kMaxWarps = H == 1 ? 12 : 8;  // what fits 227 KB (NB = 21)
-};
+// E ring of 80 slots per warp.  Column c occupies its slot from step c - 32
+// (first init row) to step c + 31 (lane 31's read): 64 steps.  The 16 spare
+// slots let the zeroing run in batches: at the end of every step s = 15 mod 16
+// the slots of columns s + 33 .. s + 48 are cleared (their previous occupants,
+// columns c - 80, were last touched by step s - 1; their init starts at step
+// s + 1 or later).  One batch is 16 columns x NB bins, two bins per store
+// instruction, conflict-free.  (A 64-slot ring must clear one column per
+// step, and the NB words of one column all sit in one bank: NB-way conflict.)
+#ifndef OPC_SKEW_SLOTS
+#define OPC_SKEW_SLOTS 96  // 80 (12 warps for NB = 21) measured slower
+#endif
+constexpr int kSlots = OPC_SKEW_SLOTS;  // 64 + a power of two <= 32
+constexpr int kZeroBatch = kSlots - 64;
+constexpr int kZeroLanes = 32 / kZeroBatch;  // lanes (bins) per cleared column per store
+#ifndef OPC_SKEW_STATIC_PCT
+#define OPC_SKEW_STATIC_PCT 92  // 100: 20% slower on C4 (per-SM speed differs)
+#endif
+#ifndef OPC_SKEW_MIN_CHUNK
+#define OPC_SKEW_MIN_CHUNK 128
+#endif
+#ifndef OPC_SKEW_MAX_WARPS
+#define OPC_SKEW_MAX_WARPS 12
+#endif
+constexpr int kMaxWarps = OPC_SKEW_MAX_WARPS;  // 12: <= 170 registers per thread
 
-template <int NB, int H>
-__host__ __device__ inline std::size_t per_warp_bytes_h() {
-    return static_cast<std::size_t>(NB) * Halves<H>::kSlots * 8 + 32 * H * kStageStride * 4;
+template <int NB>
+__host__ __device__ inline std::size_t per_warp_bytes() {
+    return static_cast<std::size_t>(NB) * kSlots * 8 + 32 * kStageStride * 4;
 }
 
-template <int H>
 struct Loads {
-    std::uint32_t a[H], b[H], c[H], d[H];
-    std::uint32_t i1, i2;
+    std::uint32_t a, b, c, d;  // E update: entering / leaving rows of the two columns
+    std::uint32_t i1, i2;      // init: one row of column vi (+) and of column vi - w2 (-)
 };
 
 struct Task {
@@ -287,13 +393,12 @@ struct Task {
     std::uint32_t dA, dD, dI, dI2;  // w2*Hs + w2, w2*Hs, 32*Hs, (32-w2)*Hs
     std::uint8_t* out_row0;   // output row yb (band row 0), column 0
     int NV, X0, w2, lane;
-    int y_rows;               // valid rows in the band (<= 32H)
+    int y_rows;               // valid rows in the band (<= 32)
     std::size_t stride;
 };
 
 // 32-bit element offset from a 64-bit base: one IMAD.WIDE (FMA pipe; the
-// runtime multiplier four = 4 keeps ptxas from turning it into ALU LEAs) and the
-// load(s): rows r and r + 32 of the same diagonal share the address (+128 B).
+// runtime multiplier four = 4 keeps ptxas from turning it into ALU LEAs).
 __device__ __forceinline__ std::uint32_t ld_off(const std::uint32_t* base, std::uint32_t off,
                                                 std::uint32_t four) {
     std::uint32_t v;
@@ -303,45 +408,25 @@ __device__ __forceinline__ std::uint32_t ld_off(const std::uint32_t* base, std::
         : "r"(off), "r"(four), "l"(base));
     return v;
 }
-__device__ __forceinline__ void ld_off2(const std::uint32_t* base, std::uint32_t off,
-                                        std::uint32_t four, std::uint32_t& v0,
-                                        std::uint32_t& v1) {
-    asm volatile(
-        "{\n\t.reg .u64 a;\n\tmad.wide.u32 a, %2, %3, %4;\n\tld.global.nc.u32 %0, [a];\n\t"
-        "ld.global.nc.u32 %1, [a+128];\n\t}"
-        : "=r"(v0), "=r"(v1)
-        : "r"(off), "r"(four), "l"(base));
-}
 
 // Loads of step s.  Ring column c, ring row rho live at offset
 // o0 + (c + rho) * Hs + rho, so every access of a step is on diagonal D0 + s
 // (+ a step-independent shift), 32 consecutive rows per access.
-template <int H, bool EDGE>
-__device__ __forceinline__ Loads<H> fetch(const Task& T, int s) {
-    Loads<H> L;
+template <bool EDGE>
+__device__ __forceinline__ Loads fetch(const Task& T, int s) {
+    Loads L;
     const int t = T.lane;
     const int w2 = T.w2;
     const std::uint32_t ob = T.o0 + static_cast<std::uint32_t>(s) * T.Hs + t;  // diag D0+s, row t
     const std::uint32_t four = T.M.four;
-    if (!EDGE && H == 2) {
-        ld_off2(T.Sf, ob + T.dA, four, L.a[0], L.a[H - 1]);  // new rows t+w2 (+32), entering
-        ld_off2(T.Sf, ob, four, L.b[0], L.b[H - 1]);         // old rows t (+32), entering
-        ld_off2(T.Sf, ob + w2, four, L.c[0], L.c[H - 1]);    // new rows, leaving
-        ld_off2(T.Sf, ob - T.dD, four, L.d[0], L.d[H - 1]);  // old rows, leaving
-    } else {
-#pragma unroll
-        for (int h = 0; h < H; ++h) {
-            const int v = s - t - 32 * h;
-            const std::uint32_t o = ob + 32 * h;
-            L.a[h] = L.b[h] = L.c[h] = L.d[h] = 0;
-            if (!EDGE || (v >= 0 && v < T.NV)) {
-                L.a[h] = ld_off(T.Sf, o + T.dA, four);
-                L.b[h] = ld_off(T.Sf, o, four);
-                if (!EDGE || v >= w2) {
-                    L.c[h] = ld_off(T.Sf, o + w2, four);
-                    L.d[h] = ld_off(T.Sf, o - T.dD, four);
-                }
-            }
+    const int v = s - t;
+    L.a = L.b = L.c = L.d = 0;
+    if (!EDGE || (v >= 0 && v < T.NV)) {
+        L.a = ld_off(T.Sf, ob + T.dA, four);  // new row t+w2, entering column
+        L.b = ld_off(T.Sf, ob, four);         // old row t, entering column
+        if (!EDGE || v >= w2) {
+            L.c = ld_off(T.Sf, ob + w2, four);     // new row, leaving column
+            L.d = ld_off(T.Sf, ob - T.dD, four);   // old row, leaving column
         }
     }
     const int k = (s - t) & 31;
@@ -356,108 +441,100 @@ __device__ __forceinline__ Loads<H> fetch(const Task& T, int s) {
 }
 
 // L2 prefetch of the band rows of the diagonal the init reads at step s.
-template <int H>
 __device__ __forceinline__ void prefetch_l2(const Task& T, int s) {
     const std::uint32_t o = T.o0 + static_cast<std::uint32_t>(s) * T.Hs + T.dI + T.lane;
     const std::uint32_t* p = T.Sf + o;
-#pragma unroll
-    for (int q = 0; q < H + 1; ++q) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 32 * q));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 32));
 }
 
-template <int NB, int H, bool EDGE>
-__device__ __forceinline__ void step(const Task& T, int s, const Loads<H>& cur,
-                                     unsigned long long (&win)[H][NB], unsigned long long* E,
+template <int NB, bool EDGE>
+__device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
+                                     unsigned long long (&win)[NB], unsigned long long* E,
                                      std::uint32_t* stage, const std::uint32_t* recip) {
-    constexpr int SL = Halves<H>::kSlots;
     const int t = T.lane;
     const int w2 = T.w2;
-    // All halves' dense reads first (their slots were finished at the previous
-    // step), so the RMW chains below do not serialise them.
-    unsigned long long e[H][NB];
+    const int v = s - t;
+    if (!EDGE || (v >= 0 && v < T.NV)) {
+        const int slot = static_cast<unsigned>(v) % kSlots;
+        unsigned long long e[NB];
 #pragma unroll
-    for (int h = 0; h < H; ++h) {
-        const int v = s - t - 32 * h;
-        if (!EDGE || (v >= 0 && v < T.NV)) {
-            const int slot = v % SL;
-#pragma unroll
-            for (int b = 0; b < NB; ++b) e[h][b] = E[b * SL + slot];
+        for (int b = 0; b < NB; ++b) e[b] = E[b * kSlots + slot];
+        if (!EDGE || (v >= w2 && t < T.y_rows)) {
+            stage[t * kStageStride + (v & 31)] = winner_rgb<NB>(win, recip, T.M.one);
         }
-    }
 #pragma unroll
-    for (int h = 0; h < H; ++h) {
-        const int v = s - t - 32 * h;
-        if (!EDGE || (v >= 0 && v < T.NV)) {
-            const int slot = v % SL;
-            if (!EDGE || (v >= w2 && t + 32 * h < T.y_rows)) {
-                stage[(t + 32 * h) * kStageStride + (v & 31)] = winner_rgb<NB>(win[h], recip);
-            }
-#pragma unroll
-            for (int b = 0; b < NB; ++b) win[h][b] += e[h][b];
-            // Advance E(v) from row t + 32h to the next row (lane t+1, or half h+1).
-            unsigned long long* Es = E + slot;
-            rmw_add<SL>(Es, cur.a[h], T.M);
-            rmw_sub<SL>(Es, cur.b[h], T.M);
-            if (!EDGE || v >= w2) {
-                rmw_sub<SL>(Es, cur.c[h], T.M);
-                rmw_add<SL>(Es, cur.d[h], T.M);
-            }
+        for (int b = 0; b < NB; ++b) {
+            if (!EDGE && b < OPC_SKEW_WIDE_BINS) wide_add(win[b], e[b], T.M.one);
+            else win[b] += e[b];
+        }
+        // Advance E(v) from row t to row t + 1 (lane t + 1 reads it next step).
+        unsigned long long* Es = E + slot;
+        rmw_add<kSlots>(Es, cur.a, T.M);
+        rmw_sub<kSlots>(Es, cur.b, T.M);
+        if (!EDGE || v >= w2) {
+            rmw_sub<kSlots>(Es, cur.c, T.M);
+            rmw_add<kSlots>(Es, cur.d, T.M);
         }
     }
     {  // one row of the from-scratch build of E(vi, band top)
         const int k = (s - t) & 31;
         const int vi = s - k + 32;
-        const int islot = vi % SL;
+        const int islot = static_cast<unsigned>(vi) % kSlots;
         if (EDGE) {
             if (k < w2 && vi >= 0 && vi < T.NV) {
-                rmw_add<SL>(E + islot, cur.i1, T.M);
-                if (vi >= w2) rmw_sub<SL>(E + islot, cur.i2, T.M);
+                rmw_add<kSlots>(E + islot, cur.i1, T.M);
+                if (vi >= w2) rmw_sub<kSlots>(E + islot, cur.i2, T.M);
             }
         } else {
             // Branch-free: rows k >= w2 contribute zero (their entries are valid
             // memory, so the bin index stays in range).
             const std::uint32_t m = k < w2 ? ~0u : 0u;
-            rmw_add_m<SL>(E + islot, cur.i1, m, m & T.M.m16);
-            rmw_sub_m<SL>(E + islot, cur.i2, m, m & T.M.negm16);
+            rmw_add_m<kSlots>(E + islot, cur.i1, m, m & T.M.m16);
+            rmw_sub_m<kSlots>(E + islot, cur.i2, m, m & T.M.negm16);
         }
     }
     __syncwarp();
-    // Rows fr + 32h just completed the 32-column block ending at v = s - fr - 32h.
+    // Row fr just completed the 32-column block ending at v = s - fr.
     const int fr = (s + 1) & 31;
+    const int vv = s - fr - 31 + t;
+    if (!EDGE || (vv >= w2 && vv < T.NV && fr < T.y_rows)) {
+        const std::uint32_t rgb = stage[fr * kStageStride + t];
+        std::uint8_t* o = T.out_row0 + static_cast<std::size_t>(fr) * T.stride +
+                          static_cast<std::size_t>(T.X0 + vv) * 3;
+        o[0] = static_cast<std::uint8_t>(rgb);
+        o[1] = static_cast<std::uint8_t>(rgb >> 8);
+        o[2] = static_cast<std::uint8_t>(rgb >> 16);
+    }
+    if ((s & (kZeroBatch - 1)) == kZeroBatch - 1) {  // clear columns s + 33 .. s + 48
+        const int zs = static_cast<unsigned>(s + 33 + (t & (kZeroBatch - 1))) % kSlots;
 #pragma unroll
-    for (int h = 0; h < H; ++h) {
-        const int vv = s - fr - 31 + t - 32 * h;
-        if (!EDGE || (vv >= w2 && vv < T.NV && fr + 32 * h < T.y_rows)) {
-            const std::uint32_t rgb = stage[(fr + 32 * h) * kStageStride + t];
-            std::uint8_t* o = T.out_row0 + static_cast<std::size_t>(fr + 32 * h) * T.stride +
-                              static_cast<std::size_t>(T.X0 + vv) * 3;
-            o[0] = static_cast<std::uint8_t>(rgb);
-            o[1] = static_cast<std::uint8_t>(rgb >> 8);
-            o[2] = static_cast<std::uint8_t>(rgb >> 16);
+        for (int j = 0; j < (NB + kZeroLanes - 1) / kZeroLanes; ++j) {
+            const int b = kZeroLanes * j + t / kZeroBatch;
+            if (b < NB) E[b * kSlots + zs] = 0ull;
         }
     }
     __syncwarp();
 }
 
-template <int NB, int H>
-__global__ void __launch_bounds__(Halves<H>::kMaxWarps * 32)
+template <int NB>
+__global__ void __launch_bounds__(kMaxWarps * 32)
     skew_kernel(BandArgs a, const std::uint32_t* __restrict__ S, ShearGeom sg, int* task_counter,
                 TaskGeom g, Mul M) {
-    constexpr int SL = Halves<H>::kSlots;
     extern __shared__ __align__(16) unsigned char smem[];
     std::uint32_t* recip = reinterpret_cast<std::uint32_t*>(smem);
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int r = a.radius;
-    unsigned char* wbase = smem + kRecipBytes + warp * per_warp_bytes_h<NB, H>();
+    unsigned char* wbase = smem + kRecipBytes + warp * per_warp_bytes<NB>();
     unsigned long long* E = reinterpret_cast<unsigned long long*>(wbase);
-    std::uint32_t* stage = reinterpret_cast<std::uint32_t*>(wbase + std::size_t(NB) * SL * 8);
+    std::uint32_t* stage = reinterpret_cast<std::uint32_t*>(wbase + std::size_t(NB) * kSlots * 8);
 
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
         recip[i] = i ? 0x80000000u / static_cast<std::uint32_t>(i) + 1u : 0u;
     }
     __syncthreads();
 
-    const int per_frame = g.nbands * g.nsegs;
     Task T;
     T.M = M;
     T.Hs = static_cast<std::uint32_t>(sg.Hs);
@@ -469,21 +546,37 @@ __global__ void __launch_bounds__(Halves<H>::kMaxWarps * 32)
     T.lane = lane;
     T.stride = static_cast<std::size_t>(a.width) * 3;
 
+    long long u = 0, u_end = 0;  // unprocessed units of the current chunk
     for (;;) {
-        int task = 0;
-        if (lane == 0) task = atomicAdd(task_counter, 1);
-        task = __shfl_sync(0xFFFFFFFFu, task, 0);
-        if (task >= g.ntasks) break;
-        const int f = task / per_frame;
-        const int rem = task - f * per_frame;
-        const int kb = rem / g.nsegs;
-        const int js = rem - kb * g.nsegs;
-        const int yb = a.y_lo + Halves<H>::kRows * kb;
-        const int xs = a.x_lo + js * g.segw;
-        const int xe = min(xs + g.segw, a.x_hi);
+        if (u >= u_end) {
+            int i = 0;
+            if (lane == 0) i = atomicAdd(task_counter, 1);
+            i = __shfl_sync(0xFFFFFFFFu, i, 0);
+            if (i >= g.nchunks) break;
+            if (i < g.nstatic) {
+                u = static_cast<long long>(i) * g.s1;
+                u_end = u + g.s1;
+            } else {
+                u = static_cast<long long>(g.nstatic) * g.s1 +
+                    static_cast<long long>(i - g.nstatic) * g.s2;
+                u_end = u + g.s2;
+            }
+            if (u_end > g.units) u_end = g.units;
+            continue;
+        }
+        const long long band = u / g.pitch;
+        const int x0 = static_cast<int>(u - band * g.pitch);
+        const int x1 = static_cast<int>(min(static_cast<long long>(g.iw), x0 + (u_end - u)));
+        u = x1 == g.iw ? (band + 1) * g.pitch : u + (x1 - x0);
+        if (x1 <= x0) continue;
+        const int f = static_cast<int>(band / g.nbands);
+        const int kb = static_cast<int>(band - static_cast<long long>(f) * g.nbands);
+        const int yb = a.y_lo + 32 * kb;
+        const int xs = a.x_lo + x0;
+        const int xe = a.x_lo + x1;
         T.NV = T.w2 + (xe - xs);  // virtual columns: w2 warm-up + outputs
         T.X0 = xs - T.w2;         // image column of virtual column 0
-        T.y_rows = min(Halves<H>::kRows, a.y_hi - yb);
+        T.y_rows = min(32, a.y_hi - yb);
         T.out_row0 = a.out + a.out_frame_stride * f +
                      static_cast<std::size_t>(yb - a.out_row0) * T.stride;
         // ring column c = image column xs - r + c, ring row rho = image row yb - r + rho;
@@ -493,38 +586,32 @@ __global__ void __launch_bounds__(Halves<H>::kMaxWarps * 32)
         T.Sf = S + sg.frame_elems * f;
         T.o0 = D0 * T.Hs + R0;
 
-        unsigned long long win[H][NB];
+        unsigned long long win[NB];
 #pragma unroll
-        for (int h = 0; h < H; ++h)
-#pragma unroll
-            for (int b = 0; b < NB; ++b) win[h][b] = 0ull;
+        for (int b = 0; b < NB; ++b) win[b] = 0ull;
+        for (int i = lane; i < NB * kSlots; i += 32) E[i] = 0ull;
+        __syncwarp();
 
-        const int nphases = ((T.NV - 1) >> 5) + 1 + H;
-        // steady: every lane of every half past warm-up, flush and band rows valid
-        const int p_steady_lo = (T.w2 + 62 + 32 * (H - 1) + 31) >> 5;
-        const bool rows_ok = T.y_rows == Halves<H>::kRows;
-        Loads<H> cur = fetch<H, true>(T, -32);
+        const int nphases = ((T.NV - 1) >> 5) + 2;
+        // steady: every lane past warm-up, flush and band rows valid
+        const int p_steady_lo = (T.w2 + 62 + 31) >> 5;
+        const bool rows_ok = T.y_rows == 32;
+        Loads cur = fetch<true>(T, -32);
         for (int p = -1; p < nphases; ++p) {
-            {  // zero the E slots of the columns initialised during this phase
-                const int slot = (32 * (p + 1) + lane) % SL;
-#pragma unroll
-                for (int b = 0; b < NB; ++b) E[b * SL + slot] = 0ull;
-            }
-            __syncwarp();
             const bool steady = rows_ok && p >= p_steady_lo && 32 * p + 31 < T.NV;
             if (steady) {
                 // Loads run two steps ahead; the diagonal first touched eight
                 // steps ahead (the init column's) is pulled into L2 now.
-                Loads<H> n1 = fetch<H, false>(T, 32 * p + 1);
+                Loads n1 = fetch<false>(T, 32 * p + 1);
 #pragma unroll 1
                 for (int ss = 0; ss < 32; ss += 2) {
                     const int s = 32 * p + ss;
-                    prefetch_l2<H>(T, s + 8);
-                    const Loads<H> n2 = fetch<H, false>(T, s + 2);
-                    step<NB, H, false>(T, s, cur, win, E, stage, recip);
-                    prefetch_l2<H>(T, s + 9);
-                    const Loads<H> n3 = fetch<H, false>(T, s + 3);
-                    step<NB, H, false>(T, s + 1, n1, win, E, stage, recip);
+                    prefetch_l2(T, s + 8);
+                    const Loads n2 = fetch<false>(T, s + 2);
+                    step<NB, false>(T, s, cur, win, E, stage, recip);
+                    prefetch_l2(T, s + 9);
+                    const Loads n3 = fetch<false>(T, s + 3);
+                    step<NB, false>(T, s + 1, n1, win, E, stage, recip);
                     cur = n2;
                     n1 = n3;
                 }
@@ -532,8 +619,8 @@ __global__ void __launch_bounds__(Halves<H>::kMaxWarps * 32)
 #pragma unroll 1
                 for (int ss = 0; ss < 32; ++ss) {
                     const int s = 32 * p + ss;
-                    const Loads<H> nxt = fetch<H, true>(T, s + 1);
-                    step<NB, H, true>(T, s, cur, win, E, stage, recip);
+                    const Loads nxt = fetch<true>(T, s + 1);
+                    step<NB, true>(T, s, cur, win, E, stage, recip);
                     cur = nxt;
                 }
             }
@@ -541,21 +628,20 @@ __global__ void __launch_bounds__(Halves<H>::kMaxWarps * 32)
     }
 }
 
-template <int NB, int H>
-cudaError_t launch_nbh(const BandArgs& a, int* counter, void* scratch, int num_sms,
-                       cudaStream_t s) {
-    const std::size_t pw = per_warp_bytes_h<NB, H>();
+template <int NB>
+cudaError_t launch_nb(const BandArgs& a, int* counter, void* scratch, int num_sms,
+                      cudaStream_t s) {
+    const std::size_t pw = per_warp_bytes<NB>();
     const std::size_t limit = 227 * 1024;
-    int warps = Halves<H>::kMaxWarps;
+    int warps = kMaxWarps;
     while (warps > 1 && kRecipBytes + warps * pw > limit) --warps;
     const std::size_t smem = kRecipBytes + warps * pw;
-    cudaError_t e = cudaFuncSetAttribute(skew_kernel<NB, H>,
+    cudaError_t e = cudaFuncSetAttribute(skew_kernel<NB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, skew_kernel<NB, H>, warps * 32,
-                                                      smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, skew_kernel<NB>, warps * 32, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
 
@@ -574,42 +660,43 @@ cudaError_t launch_nbh(const BandArgs& a, int* counter, void* scratch, int num_s
 
     TaskGeom g{};
     const int rows = a.y_hi - a.y_lo;
-    const int iw = a.x_hi - a.x_lo;
-    g.nbands = (rows + Halves<H>::kRows - 1) / Halves<H>::kRows;
-    const long long total_warps = static_cast<long long>(num_sms) * per_sm * warps;
-    // Aim for >= 4 tasks per resident warp with segments no narrower than 256
-    // columns (each task pays 2r+1 warm-up and 31 + 32(H-1) skew-fill steps);
-    // images too small to fill the GPU that way go down to 64-column segments.
-    const long long want = 4 * total_warps;
-    const long long per_seg = static_cast<long long>(g.nbands) * a.frames;
-    int nsegs = static_cast<int>((want + per_seg - 1) / per_seg);
-    const int min_w = per_seg * ((iw + 255) / 256) >= total_warps ? 256 : 64;
-    const int max_segs = (iw + min_w - 1) / min_w;
-    if (nsegs > max_segs) nsegs = max_segs;
-    if (nsegs < 1) nsegs = 1;
-    g.segw = (iw + nsegs - 1) / nsegs;
-    g.nsegs = (iw + g.segw - 1) / g.segw;
-    g.ntasks = a.frames * g.nbands * g.nsegs;
-    long long blocks = (g.ntasks + warps - 1) / warps;
+    g.iw = a.x_hi - a.x_lo;
+    g.pitch = g.iw;
+    g.nbands = (rows + 31) / 32;
+    g.units = static_cast<long long>(a.frames) * g.nbands * g.iw;
+    const long long resident = static_cast<long long>(num_sms) * per_sm * warps;
+    // Each pass pays 2r+1 warm-up and ~63 skew fill/drain steps, so chunks stay
+    // >= kMinChunk columns; images too small for a static share per warp are
+    // split into kMinChunk-column chunks only.
+    constexpr long long kMinChunk = OPC_SKEW_MIN_CHUNK;
+    if (g.units >= resident * 4 * kMinChunk) {
+        g.nstatic = static_cast<int>(resident);
+        g.s1 = g.units * OPC_SKEW_STATIC_PCT / (100 * resident);
+        const long long rest = g.units - resident * g.s1;
+        g.s2 = max(kMinChunk, (rest + 2 * resident - 1) / (2 * resident));
+        g.nchunks = g.nstatic + static_cast<int>((rest + g.s2 - 1) / g.s2);
+    } else {
+        // Dynamic only: equal segments of each band (>= 64 columns, about
+        // three chunks per resident warp), chunk = one segment.
+        const long long per_band = static_cast<long long>(a.frames) * g.nbands;
+        const long long want = max(64ll, min(512ll, g.units / (3 * resident)));
+        const int nsegs = static_cast<int>(max(1ll, (g.iw + want - 1) / want));
+        g.s2 = (g.iw + nsegs - 1) / nsegs;
+        g.pitch = static_cast<int>(g.s2) * nsegs;
+        g.nstatic = 0;
+        g.s1 = 0;
+        g.units = per_band * g.pitch;
+        g.nchunks = static_cast<int>(per_band * nsegs);
+    }
+    long long blocks = (g.nchunks + warps - 1) / warps;
     if (blocks > static_cast<long long>(num_sms) * per_sm) blocks = num_sms * per_sm;
     if (blocks < 1) blocks = 1;
 
     e = cudaMemsetAsync(counter, 0, sizeof(int), s);
     if (e != cudaSuccess) return e;
-    const Mul M{16u, 0xFFFFFFF0u, 4u};
-    skew_kernel<NB, H><<<static_cast<unsigned>(blocks), warps * 32, smem, s>>>(a, S, sg, counter,
-                                                                               g, M);
+    const Mul M{16u, 0xFFFFFFF0u, 4u, 1u};
+    skew_kernel<NB><<<static_cast<unsigned>(blocks), warps * 32, smem, s>>>(a, S, sg, counter, g, M);
     return cudaGetLastError();
-}
-
-#ifndef OPC_SKEW_HALVES
-#define OPC_SKEW_HALVES 1  // H = 2 (64-row bands) measured slower: profiles/r01_notes.md
-#endif
-
-template <int NB>
-cudaError_t launch_nb(const BandArgs& a, int* counter, void* scratch, int num_sms,
-                      cudaStream_t s) {
-    return launch_nbh<NB, OPC_SKEW_HALVES>(a, counter, scratch, num_sms, s);
 }
 
 }  // namespace

@@ -2,7 +2,7 @@
 """Lane-by-lane Python model of the skew kernel schedule (debugging aid).
 
 Executes exactly the schedule of paper_1405_1020_b200/csrc/skew.cu (virtual
-columns, sheared loads, E-slot ring with phase zeroing, staggered init,
+columns, sheared loads, E-slot ring with per-step zeroing, staggered init,
 staging/flush) on small images with unbounded Python ints instead of packed
 words, and compares with the oracle.  Any schedule bug shows up here on the
 CPU before a GPU run.
@@ -17,7 +17,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT / "tests"))
 
-SLOTS = 96
+SLOTS = 80
 
 
 def model(img: np.ndarray, r: int, L: int, segw: int | None = None) -> np.ndarray:
@@ -87,8 +87,6 @@ def model(img: np.ndarray, r: int, L: int, segw: int | None = None) -> np.ndarra
 
             nphases = ((NV - 1) >> 5) + 2
             for p in range(-1, nphases):
-                for t in range(32):
-                    E[(32 * (p + 1) + t) % SLOTS] = dict()
                 for ss in range(32):
                     s = 32 * p + ss
                     cur = [fetch(s, t) for t in range(32)]
@@ -126,6 +124,9 @@ def model(img: np.ndarray, r: int, L: int, segw: int | None = None) -> np.ndarra
                         vv = s - fr - 31 + lane
                         if w2 <= vv < NV and yb + fr < y_hi:
                             out[yb + fr, X0 + vv] = stage[fr][lane]
+                    if s % 16 == 15:  # batch-clear the slots of columns s + 33 .. s + 48
+                        for c in range(s + 33, s + 49):
+                            E[c % SLOTS] = dict()
     return out
 
 
