@@ -365,7 +365,7 @@ constexpr int kSlots = OPC_SKEW_SLOTS;  // 64 + a power of two <= 32
 constexpr int kZeroBatch = kSlots - 64;
 constexpr int kZeroLanes = 32 / kZeroBatch;  // lanes (bins) per cleared column per store
 #ifndef OPC_SKEW_STATIC_PCT
-#define OPC_SKEW_STATIC_PCT 92  // 100: 20% slower on C4 (per-SM speed differs)
+#define OPC_SKEW_STATIC_PCT 98  // 90-100 within 2% on C4; C5 best at 97-100
 #endif
 #ifndef OPC_SKEW_MIN_CHUNK
 #define OPC_SKEW_MIN_CHUNK 128
@@ -498,7 +498,7 @@ __device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
     // Row fr just completed the 32-column block ending at v = s - fr.
     const int fr = (s + 1) & 31;
     const int vv = s - fr - 31 + t;
-    if (!EDGE || (vv >= w2 && vv < T.NV && fr < T.y_rows)) {
+    if (fr < T.y_rows && (!EDGE || (vv >= w2 && vv < T.NV))) {
         const std::uint32_t rgb = stage[fr * kStageStride + t];
         std::uint8_t* o = T.out_row0 + static_cast<std::size_t>(fr) * T.stride +
                           static_cast<std::size_t>(T.X0 + vv) * 3;
@@ -593,12 +593,13 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
         __syncwarp();
 
         const int nphases = ((T.NV - 1) >> 5) + 2;
-        // steady: every lane past warm-up, flush and band rows valid
+        // steady: every lane past warm-up and every flushed column valid
         const int p_steady_lo = (T.w2 + 62 + 31) >> 5;
-        const bool rows_ok = T.y_rows == 32;
         Loads cur = fetch<true>(T, -32);
         for (int p = -1; p < nphases; ++p) {
-            const bool steady = rows_ok && p >= p_steady_lo && 32 * p + 31 < T.NV;
+            // (A partial last band runs the steady path too: its rows past
+            // y_rows read valid plane rows and are never flushed.)
+            const bool steady = p >= p_steady_lo && 32 * p + 31 < T.NV;
             if (steady) {
                 // Loads run two steps ahead; the diagonal first touched eight
                 // steps ahead (the init column's) is pulled into L2 now.
