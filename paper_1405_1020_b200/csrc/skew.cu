@@ -31,6 +31,7 @@
 //  * Output: a 32x32 staging tile; each step one row completes a 32-pixel
 //    block, written as one coalesced 96-byte run.
 #include "kernels.cuh"
+#include "worksplit.cuh"
 
 namespace opc {
 
@@ -337,18 +338,6 @@ __device__ __forceinline__ std::uint32_t winner_rgb(const unsigned long long (&w
     return qr | (qg << 8) | (qb << 16);
 }
 
-// Work split.  The units are band columns, linearised (frame, band, column);
-// chunk i < nstatic is [i*s1, (i+1)*s1) -- one per resident warp, taken at
-// launch, together most of the work -- and the rest is handed out in chunks of
-// s2 units by the same atomic counter.  Every warp runs at the same rate (the
-// step costs do not depend on the pixels), so equal static shares leave no
-// tail; the dynamic remainder absorbs per-SM speed differences.  A chunk that
-// crosses a band end is run as two passes.
-struct TaskGeom {
-    int nbands, iw, pitch;  // pitch >= iw: units per band (segment-aligned chunks)
-    int nstatic, nchunks;
-    long long units, s1, s2;
-};
 
 // E ring of 80 slots per warp.  Column c occupies its slot from step c - 32
 // (first init row) to step c + 31 (lane 31's read): 64 steps.  The 16 spare
@@ -520,7 +509,7 @@ __device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
 template <int NB>
 __global__ void __launch_bounds__(kMaxWarps * 32)
     skew_kernel(BandArgs a, const std::uint32_t* __restrict__ S, ShearGeom sg, int* task_counter,
-                TaskGeom g, Mul M) {
+                WorkSplit g, Mul M) {
     extern __shared__ __align__(16) unsigned char smem[];
     std::uint32_t* recip = reinterpret_cast<std::uint32_t*>(smem);
     const int lane = threadIdx.x & 31;
@@ -547,30 +536,8 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
     T.stride = static_cast<std::size_t>(a.width) * 3;
 
     long long u = 0, u_end = 0;  // unprocessed units of the current chunk
-    for (;;) {
-        if (u >= u_end) {
-            int i = 0;
-            if (lane == 0) i = atomicAdd(task_counter, 1);
-            i = __shfl_sync(0xFFFFFFFFu, i, 0);
-            if (i >= g.nchunks) break;
-            if (i < g.nstatic) {
-                u = static_cast<long long>(i) * g.s1;
-                u_end = u + g.s1;
-            } else {
-                u = static_cast<long long>(g.nstatic) * g.s1 +
-                    static_cast<long long>(i - g.nstatic) * g.s2;
-                u_end = u + g.s2;
-            }
-            if (u_end > g.units) u_end = g.units;
-            continue;
-        }
-        const long long band = u / g.pitch;
-        const int x0 = static_cast<int>(u - band * g.pitch);
-        const int x1 = static_cast<int>(min(static_cast<long long>(g.iw), x0 + (u_end - u)));
-        u = x1 == g.iw ? (band + 1) * g.pitch : u + (x1 - x0);
-        if (x1 <= x0) continue;
-        const int f = static_cast<int>(band / g.nbands);
-        const int kb = static_cast<int>(band - static_cast<long long>(f) * g.nbands);
+    int f, kb, x0, x1;
+    while (next_pass(g, task_counter, lane, u, u_end, f, kb, x0, x1)) {
         const int yb = a.y_lo + 32 * kb;
         const int xs = a.x_lo + x0;
         const int xe = a.x_lo + x1;
@@ -659,36 +626,9 @@ cudaError_t launch_nb(const BandArgs& a, int* counter, void* scratch, int num_sm
         if (e != cudaSuccess) return e;
     }
 
-    TaskGeom g{};
-    const int rows = a.y_hi - a.y_lo;
-    g.iw = a.x_hi - a.x_lo;
-    g.pitch = g.iw;
-    g.nbands = (rows + 31) / 32;
-    g.units = static_cast<long long>(a.frames) * g.nbands * g.iw;
     const long long resident = static_cast<long long>(num_sms) * per_sm * warps;
-    // Each pass pays 2r+1 warm-up and ~63 skew fill/drain steps, so chunks stay
-    // >= kMinChunk columns; images too small for a static share per warp are
-    // split into kMinChunk-column chunks only.
-    constexpr long long kMinChunk = OPC_SKEW_MIN_CHUNK;
-    if (g.units >= resident * 4 * kMinChunk) {
-        g.nstatic = static_cast<int>(resident);
-        g.s1 = g.units * OPC_SKEW_STATIC_PCT / (100 * resident);
-        const long long rest = g.units - resident * g.s1;
-        g.s2 = max(kMinChunk, (rest + 2 * resident - 1) / (2 * resident));
-        g.nchunks = g.nstatic + static_cast<int>((rest + g.s2 - 1) / g.s2);
-    } else {
-        // Dynamic only: equal segments of each band (>= 64 columns, about
-        // three chunks per resident warp), chunk = one segment.
-        const long long per_band = static_cast<long long>(a.frames) * g.nbands;
-        const long long want = max(64ll, min(512ll, g.units / (3 * resident)));
-        const int nsegs = static_cast<int>(max(1ll, (g.iw + want - 1) / want));
-        g.s2 = (g.iw + nsegs - 1) / nsegs;
-        g.pitch = static_cast<int>(g.s2) * nsegs;
-        g.nstatic = 0;
-        g.s1 = 0;
-        g.units = per_band * g.pitch;
-        g.nchunks = static_cast<int>(per_band * nsegs);
-    }
+    const WorkSplit g = make_split(a.frames, (a.y_hi - a.y_lo + 31) / 32, a.x_hi - a.x_lo, resident,
+                                   OPC_SKEW_STATIC_PCT, OPC_SKEW_MIN_CHUNK);
     long long blocks = (g.nchunks + warps - 1) / warps;
     if (blocks > static_cast<long long>(num_sms) * per_sm) blocks = num_sms * per_sm;
     if (blocks < 1) blocks = 1;

@@ -20,10 +20,15 @@
 // shared pre-pass, so a ring column (32+2r rows) is one contiguous run that
 // cp.async copies 16 bytes at a time, one 32-column phase ahead.
 #include "kernels.cuh"
+#include "worksplit.cuh"
 
 namespace opc {
 
 namespace {
+
+#ifndef OPC_SLIDE_STATIC_PCT
+#define OPC_SLIDE_STATIC_PCT 50  // content-dependent step costs: 90 measured 20% slower on C3
+#endif
 
 constexpr int kWarps = 8;  // upper bound; the launcher fits as many as 227 KB allows
 constexpr int kRingCols = 96;
@@ -109,13 +114,9 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;"); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;"); }
 
-struct TaskGeom {
-    int nbands, nsegs, segw, ntasks;
-};
-
 __global__ void __launch_bounds__(kWarps * 32)
     slide_kernel(BandArgs a, const std::uint32_t* __restrict__ T, TGeom tg, int* task_counter,
-                 TaskGeom g) {
+                 WorkSplit g) {
     extern __shared__ __align__(16) unsigned char smem[];
     std::uint32_t* recip = reinterpret_cast<std::uint32_t*>(smem);
     const int lane = threadIdx.x & 31;
@@ -138,22 +139,15 @@ __global__ void __launch_bounds__(kWarps * 32)
     __syncthreads();
 
     const std::size_t stride = static_cast<std::size_t>(a.width) * 3;
-    const int per_frame = g.nbands * g.nsegs;
     const std::uint32_t bm = a.bin_mul;
     const unsigned FULL = 0xFFFFFFFFu;
 
-    for (;;) {
-        int task = 0;
-        if (lane == 0) task = atomicAdd(task_counter, 1);
-        task = __shfl_sync(FULL, task, 0);
-        if (task >= g.ntasks) break;
-        const int f = task / per_frame;
-        const int rem = task - f * per_frame;
-        const int kb = rem / g.nsegs;
-        const int js = rem - kb * g.nsegs;
+    long long u = 0, u_end = 0;
+    int f, kb, x0, x1;
+    while (next_pass(g, task_counter, lane, u, u_end, f, kb, x0, x1)) {
         const int yb = a.y_lo + 32 * kb;
-        const int xs = a.x_lo + js * g.segw;
-        const int xe = min(xs + g.segw, a.x_hi);
+        const int xs = a.x_lo + x0;
+        const int xe = a.x_lo + x1;
         const int ncols = xe - xs + 2 * r;  // ring-relative columns [0, ncols]: image xs-r ..
         const bool row_ok = yb + lane < a.y_hi;
         const std::uint32_t* Tf = T + tg.frame_elems * f +
@@ -362,21 +356,12 @@ cudaError_t launch_slide(const BandArgs& a, int* counter, void* scratch, int num
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
-    TaskGeom g{};
-    const int rows = a.y_hi - a.y_lo;
-    const int iw = a.x_hi - a.x_lo;
-    g.nbands = (rows + 31) / 32;
-    const long long total_warps = static_cast<long long>(num_sms) * per_sm * warps;
-    const long long want = 4 * total_warps;
-    const long long per_seg = static_cast<long long>(g.nbands) * a.frames;
-    int nsegs = static_cast<int>((want + per_seg - 1) / per_seg);
-    const int max_segs = (iw + 63) / 64;
-    if (nsegs > max_segs) nsegs = max_segs;
-    if (nsegs < 1) nsegs = 1;
-    g.segw = (iw + nsegs - 1) / nsegs;
-    g.nsegs = (iw + g.segw - 1) / g.segw;
-    g.ntasks = a.frames * g.nbands * g.nsegs;
-    long long blocks = (g.ntasks + warps - 1) / warps;
+    const long long resident = static_cast<long long>(num_sms) * per_sm * warps;
+    // Each pass pays a full window build, rescan and window sums (~3(2r+1)^2 +
+    // L updates per lane): keep chunks >= 128 columns.
+    const WorkSplit g = make_split(a.frames, (a.y_hi - a.y_lo + 31) / 32, a.x_hi - a.x_lo, resident,
+                                   OPC_SLIDE_STATIC_PCT, 128);
+    long long blocks = (g.nchunks + warps - 1) / warps;
     if (blocks > static_cast<long long>(num_sms) * per_sm) blocks = num_sms * per_sm;
     if (blocks < 1) blocks = 1;
     e = cudaMemsetAsync(counter, 0, sizeof(int), s);

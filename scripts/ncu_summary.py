@@ -32,6 +32,11 @@ METRICS = {
     "launch__block_size": "block_size",
     "launch__grid_size": "grid_size",
     "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
+    "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed": "l1_data_pipe_pct",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed": "l1_data_pipe_shared_pct",
+    "sm__cycles_active.avg": "sm_cycles_active_avg",
+    "sm__cycles_active.max": "sm_cycles_active_max",
+    "sm__cycles_elapsed.avg": "sm_cycles_elapsed_avg",
 }
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
          "msecond": 1e-3, "second": 1, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1}
