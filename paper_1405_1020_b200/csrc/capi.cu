@@ -279,13 +279,38 @@ int filter_core(const std::uint8_t* in, std::uint8_t* out, int frames, int w, in
     std::vector<Unit> units;
     const int rows = y_end - y_begin;
     if (frames == 1) {
-        const std::size_t chunk_target = 48ull << 20;
-        int n = static_cast<int>((in_bytes + chunk_target - 1) / chunk_target);
-        n = n < 1 ? 1 : (n > 16 ? 16 : n);
-        if (n > rows) n = rows;
-        for (int k = 0; k < n; ++k) {
-            units.push_back({0, y_begin + static_cast<int>(static_cast<long long>(rows) * k / n),
-                             y_begin + static_cast<int>(static_cast<long long>(rows) * (k + 1) / n)});
+        // Row chunks of ~48 MB, with a geometric ramp (1/16, 1/8, ... of a chunk)
+        // at both ends: only the first chunk's H2D and the last chunk's kernels
+        // and D2H are not overlapped with transfers in the other direction.
+        const long long chunk_rows =
+            std::max<long long>(1, static_cast<long long>((48ull << 20) / row_bytes));
+        std::vector<int> sizes;
+        if (rows > 4 * chunk_rows) {
+            std::vector<int> ramp;
+            for (long long q = std::max<long long>(8, chunk_rows / 16); q < chunk_rows; q *= 2) {
+                ramp.push_back(static_cast<int>(q));
+            }
+            long long ramp_rows = 0;
+            for (int q : ramp) ramp_rows += 2 * q;
+            const long long mid = rows - ramp_rows;
+            const int nmid = static_cast<int>((mid + chunk_rows - 1) / chunk_rows);
+            sizes = ramp;
+            for (int k = 0; k < nmid; ++k) {
+                sizes.push_back(static_cast<int>(mid * (k + 1) / nmid - mid * k / nmid));
+            }
+            sizes.insert(sizes.end(), ramp.rbegin(), ramp.rend());
+        } else {
+            int n = static_cast<int>((rows + chunk_rows - 1) / chunk_rows);
+            n = n < 1 ? 1 : n;
+            for (int k = 0; k < n; ++k) {
+                sizes.push_back(static_cast<int>(static_cast<long long>(rows) * (k + 1) / n -
+                                                 static_cast<long long>(rows) * k / n));
+            }
+        }
+        int y = y_begin;
+        for (int q : sizes) {
+            units.push_back({0, y, y + q});
+            y += q;
         }
     } else if (in_bytes >= (4ull << 20)) {
         for (int f = 0; f < frames; ++f) units.push_back({f, y_begin, y_end});
