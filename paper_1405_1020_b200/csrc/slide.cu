@@ -26,6 +26,12 @@ namespace opc {
 
 namespace {
 
+#ifndef OPC_SLIDE_MIN_CHUNK
+#define OPC_SLIDE_MIN_CHUNK 128
+#endif
+#ifndef OPC_SLIDE_DYN_PER_WARP
+#define OPC_SLIDE_DYN_PER_WARP 2
+#endif
 #ifndef OPC_SLIDE_STATIC_PCT
 #define OPC_SLIDE_STATIC_PCT 50  // content-dependent step costs: 90 measured 20% slower on C3
 #endif
@@ -360,7 +366,7 @@ cudaError_t launch_slide(const BandArgs& a, int* counter, void* scratch, int num
     // Each pass pays a full window build, rescan and window sums (~3(2r+1)^2 +
     // L updates per lane): keep chunks >= 128 columns.
     const WorkSplit g = make_split(a.frames, (a.y_hi - a.y_lo + 31) / 32, a.x_hi - a.x_lo, resident,
-                                   OPC_SLIDE_STATIC_PCT, 128);
+                                   OPC_SLIDE_STATIC_PCT, OPC_SLIDE_MIN_CHUNK, OPC_SLIDE_DYN_PER_WARP);
     long long blocks = (g.nchunks + warps - 1) / warps;
     if (blocks > static_cast<long long>(num_sms) * per_sm) blocks = num_sms * per_sm;
     if (blocks < 1) blocks = 1;

@@ -33,7 +33,7 @@ struct WorkSplit {
 };
 
 inline WorkSplit make_split(int frames, int nbands, int iw, long long resident, int static_pct,
-                            long long min_chunk) {
+                            long long min_chunk, int dyn_per_warp = 2) {
     WorkSplit g{};
     g.nbands = nbands;
     g.iw = iw;
@@ -44,7 +44,9 @@ inline WorkSplit make_split(int frames, int nbands, int iw, long long resident, 
         g.nstatic = static_cast<int>(resident);
         g.s1 = g.units * static_pct / (100 * resident);
         const long long rest = g.units - resident * g.s1;
-        g.s2 = std::max(min_chunk, (rest + 2 * resident - 1) / (2 * resident));
+        // remainder: about dyn_per_warp chunks per resident warp
+        const long long d = static_cast<long long>(dyn_per_warp) * resident;
+        g.s2 = std::max(min_chunk, (rest + d - 1) / d);
         g.nchunks = g.nstatic + static_cast<int>((rest + g.s2 - 1) / g.s2);
     } else {
         // Dynamic only: equal segments of each band, >= 64 columns, about three
@@ -63,36 +65,54 @@ inline WorkSplit make_split(int frames, int nbands, int iw, long long resident, 
 }
 
 #ifdef __CUDACC__
-// Warp-uniform iterator over this warp's passes.  State (u, u_end) starts at
-// (0, 0); each call returns the next pass (frame f, band kb, interior columns
-// [x0, x1) relative to x_lo) or false when the launch's work is exhausted.
-__device__ __forceinline__ bool next_pass(const WorkSplit& g, int* counter, int lane, long long& u,
-                                          long long& u_end, int& f, int& kb, int& x0, int& x1) {
-    for (;;) {
-        if (u >= u_end) {
-            int i = 0;
-            if (lane == 0) i = atomicAdd(counter, 1);
-            i = __shfl_sync(0xFFFFFFFFu, i, 0);
-            if (i >= g.nchunks) return false;
-            if (i < g.nstatic) {
-                u = static_cast<long long>(i) * g.s1;
-                u_end = u + g.s1;
-            } else {
-                u = static_cast<long long>(g.nstatic) * g.s1 +
-                    static_cast<long long>(i - g.nstatic) * g.s2;
-                u_end = u + g.s2;
-            }
-            if (u_end > g.units) u_end = g.units;
-            continue;
-        }
+#define OPC_HD __host__ __device__
+#else
+#define OPC_HD
+#endif
+
+// Units [u, u_end) of chunk i (i < nchunks).
+OPC_HD inline void chunk_range(const WorkSplit& g, int i, long long& u, long long& u_end) {
+    if (i < g.nstatic) {
+        u = static_cast<long long>(i) * g.s1;
+        u_end = u + g.s1;
+    } else {
+        u = static_cast<long long>(g.nstatic) * g.s1 + static_cast<long long>(i - g.nstatic) * g.s2;
+        u_end = u + g.s2;
+    }
+    if (u_end > g.units) u_end = g.units;
+}
+
+// Next pass inside [u, u_end): frame f, band kb, interior columns [x0, x1)
+// (relative to x_lo); advances u.  False when the chunk is exhausted.  A pass
+// never crosses a band end; the padding of a pitch > iw linearisation is skipped.
+OPC_HD inline bool pass_in_chunk(const WorkSplit& g, long long& u, long long u_end, int& f, int& kb,
+                                 int& x0, int& x1) {
+    while (u < u_end) {
         const long long band = u / g.pitch;
         x0 = static_cast<int>(u - band * g.pitch);
-        x1 = static_cast<int>(min(static_cast<long long>(g.iw), x0 + (u_end - u)));
+        const long long rest = u_end - u;
+        x1 = static_cast<int>(g.iw < x0 + rest ? g.iw : x0 + rest);
         u = x1 == g.iw ? (band + 1) * g.pitch : u + (x1 - x0);
         f = static_cast<int>(band / g.nbands);
         kb = static_cast<int>(band - static_cast<long long>(f) * g.nbands);
-        if (x1 <= x0) continue;
-        return true;
+        if (x1 > x0) return true;
+    }
+    return false;
+}
+
+#ifdef __CUDACC__
+// Warp-uniform iterator over this warp's passes.  State (u, u_end) starts at
+// (0, 0); each call returns the next pass or false when the launch's work is
+// exhausted (chunks are claimed from `counter` by lane 0).
+__device__ __forceinline__ bool next_pass(const WorkSplit& g, int* counter, int lane, long long& u,
+                                          long long& u_end, int& f, int& kb, int& x0, int& x1) {
+    for (;;) {
+        if (pass_in_chunk(g, u, u_end, f, kb, x0, x1)) return true;
+        int i = 0;
+        if (lane == 0) i = atomicAdd(counter, 1);
+        i = __shfl_sync(0xFFFFFFFFu, i, 0);
+        if (i >= g.nchunks) return false;
+        chunk_range(g, i, u, u_end);
     }
 }
 #endif
