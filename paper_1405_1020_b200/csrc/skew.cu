@@ -353,6 +353,9 @@ __device__ __forceinline__ std::uint32_t winner_rgb(const unsigned long long (&w
 constexpr int kSlots = OPC_SKEW_SLOTS;  // 64 + a power of two <= 32
 constexpr int kZeroBatch = kSlots - 64;
 constexpr int kZeroLanes = 32 / kZeroBatch;  // lanes (bins) per cleared column per store
+#ifndef OPC_SKEW_PF_DIST
+#define OPC_SKEW_PF_DIST 8  // L2 prefetch distance (steps) of the init diagonal; 0 = off
+#endif
 #ifndef OPC_SKEW_STATIC_PCT
 #define OPC_SKEW_STATIC_PCT 98  // 90-100 within 2% on C4; C5 best at 97-100
 #endif
@@ -574,10 +577,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
 #pragma unroll 1
                 for (int ss = 0; ss < 32; ss += 2) {
                     const int s = 32 * p + ss;
-                    prefetch_l2(T, s + 8);
+                    if (OPC_SKEW_PF_DIST > 0) prefetch_l2(T, s + OPC_SKEW_PF_DIST);
                     const Loads n2 = fetch<false>(T, s + 2);
                     step<NB, false>(T, s, cur, win, E, stage, recip);
-                    prefetch_l2(T, s + 9);
+                    if (OPC_SKEW_PF_DIST > 0) prefetch_l2(T, s + OPC_SKEW_PF_DIST + 1);
                     const Loads n3 = fetch<false>(T, s + 3);
                     step<NB, false>(T, s + 1, n1, win, E, stage, recip);
                     cur = n2;

@@ -24,6 +24,10 @@
 #include <algorithm>
 #include <cstdint>
 
+#ifndef OPC_SPLIT_MIN_SEG
+#define OPC_SPLIT_MIN_SEG 32  // narrowest segment of the dynamic-only split
+#endif
+
 namespace opc {
 
 struct WorkSplit {
@@ -49,10 +53,14 @@ inline WorkSplit make_split(int frames, int nbands, int iw, long long resident, 
         g.s2 = std::max(min_chunk, (rest + d - 1) / d);
         g.nchunks = g.nstatic + static_cast<int>((rest + g.s2 - 1) / g.s2);
     } else {
-        // Dynamic only: equal segments of each band, >= 64 columns, about three
-        // chunks per resident warp.
+        // Dynamic only: equal segments of each band, as many as fill ~85% of
+        // the resident warps in one round (C2: 48-column segments, 13% faster
+        // than 64; narrower segments pay more warm-up and skew fill per
+        // output column, more chunks than warps add a round), 32..512 columns.
         const long long per_band = static_cast<long long>(frames) * nbands;
-        const long long want = std::max(64ll, std::min(512ll, g.units / (3 * resident)));
+        const long long fit = std::max(1ll, resident * 85 / (100 * per_band));
+        const long long want =
+            std::max<long long>(OPC_SPLIT_MIN_SEG, std::min(512ll, (iw + fit - 1) / fit));
         const int nsegs = static_cast<int>(std::max(1ll, (iw + want - 1) / want));
         g.s2 = (iw + nsegs - 1) / nsegs;
         g.pitch = static_cast<int>(g.s2) * nsegs;
