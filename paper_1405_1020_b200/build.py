@@ -72,6 +72,29 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+TOOL_SRC = ROOT / "tools" / "oilbench_cuda.cpp"
+TOOL = ROOT / "build" / "oilbench_cuda"
+
+
+def build_tools(force: bool = False) -> Path:
+    """The CLI front end (tools/oilbench_cuda.cpp), host C++ over the C-ABI,
+    linked against the in-tree library (rpath $ORIGIN/../paper_1405_1020_b200)."""
+    lib = build(force)
+    deps = [TOOL_SRC, lib, *(ROOT / "include").glob("*.h*")]
+    if force or _stale(TOOL, deps):
+        TOOL.parent.mkdir(parents=True, exist_ok=True)
+        cxx = shutil.which("g++") or "g++"
+        cmd = [cxx, "-std=c++20", "-O2", "-Wall", "-I", str(ROOT / "include"), str(TOOL_SRC),
+               "-o", str(TOOL), "-L", str(PKG), "-loilpaint_b200",
+               "-Wl,-rpath,$ORIGIN/../paper_1405_1020_b200"]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"building {TOOL.name} failed:\n{res.stdout}\n{res.stderr}")
+    return TOOL
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    build_tools()
     print(LIB)
+    print(TOOL)
