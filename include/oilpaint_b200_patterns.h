@@ -31,6 +31,13 @@ extern "C" {
 int opc_generate(int32_t kind, uint64_t seed, int32_t width, int32_t height, int32_t frame,
                  uint8_t* out, int32_t threads);
 
+/* The same bytes written into DEVICE memory `d_out` (3*width*height bytes) on
+ * `stream` (NULL: the library's stream of `device`; device < 0: current), for
+ * kinds 0-3.  Asynchronous.  Returns 0, 1 (invalid argument or a kind without a
+ * device generator) or 2 (CUDA error); opc_last_error() has the message. */
+int opc_generate_device(int32_t kind, uint64_t seed, int32_t width, int32_t height,
+                        uint8_t* d_out, int32_t device, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

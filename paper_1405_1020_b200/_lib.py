@@ -24,6 +24,7 @@ EXPORTS = (
     "opc_band_in_row0", "opc_band_in_rows", "opc_last_error", "opc_version",
     "opc_kernel_launches", "opc_device_count", "opc_synchronize", "opc_plan_kernel",
     "opc_release", "opc_generate", "opc_filter_rgb8_multi", "opc_band_begin",
+    "opc_generate_device",
 )
 
 
@@ -43,7 +44,7 @@ def _load() -> ctypes.CDLL:
             from . import build as _build
             _build.build()
         if not LIB_PATH.exists():
-            raise ImportError(f"{LIB_PATH} is missing: run python -m paper_1405_1020_b200.build "
+            raise ImportError(f"{LIB_PATH} is missing: run python paper_1405_1020_b200/build.py "
                               "(the CUDA library is the only implementation; no CPU fallback)")
     lib = ctypes.CDLL(str(LIB_PATH))
     u8p = ctypes.c_void_p
@@ -82,6 +83,8 @@ def _load() -> ctypes.CDLL:
     lib.opc_release.restype = None
     lib.opc_generate.argtypes = [i32, ctypes.c_uint64, i32, i32, i32, u8p, i32]
     lib.opc_generate.restype = ctypes.c_int
+    lib.opc_generate_device.argtypes = [i32, ctypes.c_uint64, i32, i32, u8p, i32, ctypes.c_void_p]
+    lib.opc_generate_device.restype = ctypes.c_int
     return lib
 
 

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "../../include/oilpaint_b200.h"
+#include "../../include/oilpaint_b200_patterns.h"
 #include "kernels.cuh"
 
 namespace {
@@ -481,6 +482,24 @@ int opc_synchronize(const opc_config* cfg) {
     cudaStream_t s = cfg && cfg->stream ? static_cast<cudaStream_t>(cfg->stream) : ctx->stream;
     e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return cuda_error(e, "cudaStreamSynchronize");
+    return OPC_OK;
+}
+
+int opc_generate_device(int32_t kind, uint64_t seed, int32_t width, int32_t height, uint8_t* d_out,
+                        int32_t device, void* stream) {
+    DevCtx* ctx = nullptr;
+    int rc = get_ctx(device, &ctx);
+    if (rc != OPC_OK) return rc;
+    cudaError_t e = cudaSetDevice(ctx->device);
+    if (e != cudaSuccess) return cuda_error(e, "cudaSetDevice");
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    rc = opc::launch_generate(kind, seed, width, height, d_out, s, &e);
+    if (rc == -1) {
+        return set_error(OPC_EINVAL, "pattern kind " + std::to_string(kind) +
+                                         " has no device generator (kinds 0-3 do)");
+    }
+    if (rc != 0) return set_error(OPC_EINVAL, "invalid pattern spec");
+    if (e != cudaSuccess) return cuda_error(e, "generator launch");
     return OPC_OK;
 }
 

@@ -1,0 +1,90 @@
+// gen.cu -- on-device input generation: the reference
+// patterns of proj/src/pattern.cpp:19-88 written straight into device memory,
+// byte-identical to opc_generate (patterns.cpp) on the host.  Harness code, not
+// on the measured path; it saves the host generation and the H2D copy of large
+// synthetic inputs (config 4: 805 MB).
+#include <cstdint>
+
+#include "../../include/oilpaint_b200_patterns.h"
+#include "kernels.cuh"
+
+namespace opc {
+
+namespace {
+
+constexpr std::uint64_t kGamma = 0x9E3779B97F4A7C15ull;
+
+__device__ __forceinline__ std::uint64_t mix64(std::uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// Noise{seed}: byte i = byte (i mod 8) of word i / 8 of the splitmix64 stream
+// seeded with `seed` (pattern.cpp:11-17, 64-76); word k = mix(seed + (k+1) gamma).
+// One thread per 8-byte word.
+__global__ void noise_kernel(std::uint64_t seed, std::uint8_t* out, std::size_t n) {
+    const std::size_t k = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x;
+    const std::size_t i0 = k * 8;
+    if (i0 >= n) return;
+    const std::uint64_t word = mix64(seed + (k + 1) * kGamma);
+    if (i0 + 8 <= n && (reinterpret_cast<std::uintptr_t>(out + i0) & 7) == 0) {
+        *reinterpret_cast<std::uint64_t*>(out + i0) = word;  // little-endian byte order
+        return;
+    }
+    for (std::size_t i = i0; i < n && i < i0 + 8; ++i) {
+        out[i] = static_cast<std::uint8_t>(word >> (8 * (i - i0)));
+    }
+}
+
+// Gradient, Uniform{rgb}, Checker{cell, white, black}: one thread per pixel,
+// the formulas of patterns.cpp (pattern.cpp:19-62).
+__global__ void pixel_kernel(int kind, std::uint64_t seed, int w, int h, std::uint8_t* out) {
+    const long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (p >= static_cast<long long>(w) * h) return;
+    const int y = static_cast<int>(p / w), x = static_cast<int>(p - static_cast<long long>(y) * w);
+    std::uint8_t r, g, b;
+    if (kind == OPC_PATTERN_GRADIENT) {
+        const int dx = w > 1 ? w - 1 : 1, dy = h > 1 ? h - 1 : 1;
+        const int dd = w + h > 2 ? w + h - 2 : 1;
+        r = static_cast<std::uint8_t>(x * 255 / dx);
+        g = static_cast<std::uint8_t>(y * 255 / dy);
+        b = static_cast<std::uint8_t>((x + y) * 255 / dd);
+    } else if (kind == OPC_PATTERN_UNIFORM) {
+        r = static_cast<std::uint8_t>(seed);
+        g = static_cast<std::uint8_t>(seed >> 8);
+        b = static_cast<std::uint8_t>(seed >> 16);
+    } else {  // checker, cell = seed
+        const int cell = static_cast<int>(seed);
+        r = g = b = ((x / cell) + (y / cell)) % 2 == 0 ? 255 : 0;
+    }
+    std::uint8_t* o = out + p * 3;
+    o[0] = r;
+    o[1] = g;
+    o[2] = b;
+}
+
+}  // namespace
+
+// -1: kind not available on the device; 1: invalid argument.
+int launch_generate(int kind, std::uint64_t seed, int w, int h, std::uint8_t* out, cudaStream_t s,
+                    cudaError_t* err) {
+    *err = cudaSuccess;
+    if (w < 1 || h < 1 || !out) return 1;
+    const std::size_t n = static_cast<std::size_t>(w) * h * 3;
+    if (kind == OPC_PATTERN_NOISE) {
+        const std::size_t words = (n + 7) / 8;
+        noise_kernel<<<static_cast<unsigned>((words + 255) / 256), 256, 0, s>>>(seed, out, n);
+    } else if (kind == OPC_PATTERN_GRADIENT || kind == OPC_PATTERN_UNIFORM ||
+               kind == OPC_PATTERN_CHECKER) {
+        if (kind == OPC_PATTERN_CHECKER && static_cast<long long>(seed) < 1) return 1;
+        const long long px = static_cast<long long>(w) * h;
+        pixel_kernel<<<static_cast<unsigned>((px + 255) / 256), 256, 0, s>>>(kind, seed, w, h, out);
+    } else {
+        return -1;
+    }
+    *err = cudaGetLastError();
+    return 0;
+}
+
+}  // namespace opc

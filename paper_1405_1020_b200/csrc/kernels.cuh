@@ -60,4 +60,9 @@ std::size_t slide_scratch_bytes(const BandArgs& a);
 cudaError_t launch_slide(const BandArgs& a, int* task_counter, void* scratch, int num_sms,
                          cudaStream_t s);
 
+// On-device pattern generation (gen.cu): 0 launched (*err = launch status),
+// 1 invalid argument, -1 no device generator for `kind`.
+int launch_generate(int kind, std::uint64_t seed, int w, int h, std::uint8_t* out, cudaStream_t s,
+                    cudaError_t* err);
+
 }  // namespace opc

@@ -36,6 +36,17 @@ def generate(kind: Pattern, width: int, height: int, seed: int = 0, frame: int =
     return out
 
 
+def generate_device(kind: Pattern, width: int, height: int, d_out: int, seed: int = 0,
+                    device: int = -1, stream: int | None = None) -> None:
+    """Write the pattern into device memory at address `d_out` (kinds NOISE,
+    GRADIENT, UNIFORM, CHECKER; asynchronous on `stream`)."""
+    rc = LIB.opc_generate_device(int(kind), seed & 0xFFFFFFFFFFFFFFFF, width, height, d_out,
+                                 device, stream or None)
+    if rc != 0:
+        msg = LIB.opc_last_error().decode()
+        raise (ValueError if rc == 1 else RuntimeError)(msg)
+
+
 @dataclass(frozen=True)
 class BenchConfig:
     name: str

@@ -158,3 +158,10 @@ def test_filter_without_gpu_fails_loudly():
         pytest.skip("a GPU is visible")
     with pytest.raises(opc.CudaError, match="no CUDA device"):
         opc.apply_cuda(np.zeros((8, 8, 3), np.uint8), opc.FilterParams(1, 20))
+
+
+def test_generate_device_without_gpu_fails_loudly():
+    if opc.device_count() > 0:
+        pytest.skip("a GPU is visible")
+    with pytest.raises(RuntimeError, match="no CUDA device"):
+        opc.generate_device(opc.Pattern.NOISE, 8, 8, 0)

@@ -16,6 +16,7 @@ import numpy as np
 import pytest
 
 import oracle_lib
+import paper_1405_1020_b200 as opc
 
 pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parent.parent
@@ -66,3 +67,22 @@ def test_pipelined_host_path_large_image(gpu):
         got = out[lo:hi, 2000:2400]
         rows = slice(15 if lo > 0 else 0, (hi - lo) - (15 if hi < 3000 else 0))
         assert np.array_equal(got[rows, 15:-15], want[rows, 15:-15]), y0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,seed", [(opc.Pattern.NOISE, 4), (opc.Pattern.NOISE, 42),
+                                       (opc.Pattern.GRADIENT, 0), (opc.Pattern.UNIFORM, 0x123456),
+                                       (opc.Pattern.CHECKER, 5)])
+@pytest.mark.parametrize("w,h,offset", [(1, 1, 0), (333, 97, 0), (257, 3, 5), (1024, 64, 3)])
+def test_generate_device_matches_host(gpu, kind, seed, w, h, offset):
+    """On-device generation writes the host generator's bytes,
+    also at unaligned destinations."""
+    import torch
+    buf = torch.full((w * h * 3 + offset + 8,), 0xAB, dtype=torch.uint8, device="cuda")
+    opc.generate_device(kind, w, h, buf.data_ptr() + offset, seed=seed, device=0,
+                        stream=torch.cuda.current_stream().cuda_stream or None)
+    torch.cuda.synchronize()
+    got = buf.cpu().numpy()
+    want = opc.generate(kind, w, h, seed=seed).reshape(-1)
+    assert np.array_equal(got[offset:offset + want.size], want)
+    assert (got[:offset] == 0xAB).all() and (got[offset + want.size:] == 0xAB).all()
