@@ -339,20 +339,19 @@ __device__ __forceinline__ std::uint32_t winner_rgb(const unsigned long long (&w
 }
 
 
-// E ring of 80 slots per warp.  Column c occupies its slot from step c - 32
-// (first init row) to step c + 31 (lane 31's read): 64 steps.  The 16 spare
-// slots let the zeroing run in batches: at the end of every step s = 15 mod 16
-// the slots of columns s + 33 .. s + 48 are cleared (their previous occupants,
-// columns c - 80, were last touched by step s - 1; their init starts at step
-// s + 1 or later).  One batch is 16 columns x NB bins, two bins per store
-// instruction, conflict-free.  (A 64-slot ring must clear one column per
-// step, and the NB words of one column all sit in one bank: NB-way conflict.)
-#ifndef OPC_SKEW_SLOTS
-#define OPC_SKEW_SLOTS 96  // 80 (12 warps for NB = 21) measured slower
-#endif
-constexpr int kSlots = OPC_SKEW_SLOTS;  // 64 + a power of two <= 32
-constexpr int kZeroBatch = kSlots - 64;
-constexpr int kZeroLanes = 32 / kZeroBatch;  // lanes (bins) per cleared column per store
+// E ring.  The init of column c adds its rows k < w2 at steps c - w2 .. c - 1
+// (row k of column s - k + w2 at step s, lane t on row k = (s - t) mod 32), and
+// lane 31 reads it last at step c + 31: a column lives 32 + w2 steps.  Slots
+// are cleared kBatch at a time (conflict-free) at the end of every step
+// s = -1 mod kBatch: columns s + 1 + w2 .. s + kBatch + w2, whose previous
+// occupants (c - SL) were last read by step s - 1 when SL >= kBatch + w2 + 32.
+//   r <= 7  (w2 <= 16): 64 slots, batches of 16 (used for NB >= 24: config 5 fits 11 warps/SM)
+//   r <= 15 (w2 <= 31): 96 slots, batches of 32
+template <int SL>
+struct Ring {
+    static constexpr int kBatch = SL == 64 ? 16 : 32;
+    static constexpr int kLanes = 32 / kBatch;  // bins cleared per column per store
+};
 #ifndef OPC_SKEW_PF_DIST
 #define OPC_SKEW_PF_DIST 8  // L2 prefetch distance (steps) of the init diagonal; 0 = off
 #endif
@@ -367,9 +366,9 @@ constexpr int kZeroLanes = 32 / kZeroBatch;  // lanes (bins) per cleared column 
 #endif
 constexpr int kMaxWarps = OPC_SKEW_MAX_WARPS;  // 12: <= 170 registers per thread
 
-template <int NB>
+template <int NB, int SL>
 __host__ __device__ inline std::size_t per_warp_bytes() {
-    return static_cast<std::size_t>(NB) * kSlots * 8 + 32 * kStageStride * 4;
+    return static_cast<std::size_t>(NB) * SL * 8 + 32 * kStageStride * 4;
 }
 
 struct Loads {
@@ -382,7 +381,7 @@ struct Task {
     const std::uint32_t* Sf;  // sheared plane of this frame
     std::uint32_t o0;         // element offset of diagonal D0 (ring column 0), ring row 0
     std::uint32_t Hs;         // elements per diagonal
-    std::uint32_t dA, dD, dI, dI2;  // w2*Hs + w2, w2*Hs, 32*Hs, (32-w2)*Hs
+    std::uint32_t dA, dD, dI;  // w2*Hs + w2, w2*Hs, w2*Hs
     std::uint8_t* out_row0;   // output row yb (band row 0), column 0
     int NV, X0, w2, lane;
     int y_rows;               // valid rows in the band (<= 32)
@@ -422,12 +421,12 @@ __device__ __forceinline__ Loads fetch(const Task& T, int s) {
         }
     }
     const int k = (s - t) & 31;
-    const int vi = s - k + 32;
+    const int vi = s - k + w2;
     L.i1 = L.i2 = 0;
     if (!EDGE || (k < w2 && vi >= 0 && vi < T.NV)) {
         const std::uint32_t oi = ob - t + k;
         L.i1 = ld_off(T.Sf, oi + T.dI, four);  // init: column vi, row k
-        if (!EDGE || vi >= w2) L.i2 = ld_off(T.Sf, oi + T.dI2, four);
+        if (!EDGE || vi >= w2) L.i2 = ld_off(T.Sf, oi, four);  // column vi - w2, row k
     }
     return L;
 }
@@ -440,7 +439,7 @@ __device__ __forceinline__ void prefetch_l2(const Task& T, int s) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 32));
 }
 
-template <int NB, bool EDGE>
+template <int NB, int SL, bool EDGE>
 __device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
                                      unsigned long long (&win)[NB], unsigned long long* E,
                                      std::uint32_t* stage, const std::uint32_t* recip) {
@@ -448,10 +447,10 @@ __device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
     const int w2 = T.w2;
     const int v = s - t;
     if (!EDGE || (v >= 0 && v < T.NV)) {
-        const int slot = static_cast<unsigned>(v) % kSlots;
+        const int slot = static_cast<unsigned>(v) % SL;
         unsigned long long e[NB];
 #pragma unroll
-        for (int b = 0; b < NB; ++b) e[b] = E[b * kSlots + slot];
+        for (int b = 0; b < NB; ++b) e[b] = E[b * SL + slot];
         if (!EDGE || (v >= w2 && t < T.y_rows)) {
             stage[t * kStageStride + (v & 31)] = winner_rgb<NB>(win, recip, T.M.one);
         }
@@ -462,28 +461,28 @@ __device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
         }
         // Advance E(v) from row t to row t + 1 (lane t + 1 reads it next step).
         unsigned long long* Es = E + slot;
-        rmw_add<kSlots>(Es, cur.a, T.M);
-        rmw_sub<kSlots>(Es, cur.b, T.M);
+        rmw_add<SL>(Es, cur.a, T.M);
+        rmw_sub<SL>(Es, cur.b, T.M);
         if (!EDGE || v >= w2) {
-            rmw_sub<kSlots>(Es, cur.c, T.M);
-            rmw_add<kSlots>(Es, cur.d, T.M);
+            rmw_sub<SL>(Es, cur.c, T.M);
+            rmw_add<SL>(Es, cur.d, T.M);
         }
     }
     {  // one row of the from-scratch build of E(vi, band top)
         const int k = (s - t) & 31;
-        const int vi = s - k + 32;
-        const int islot = static_cast<unsigned>(vi) % kSlots;
+        const int vi = s - k + w2;
+        const int islot = static_cast<unsigned>(vi) % SL;
         if (EDGE) {
             if (k < w2 && vi >= 0 && vi < T.NV) {
-                rmw_add<kSlots>(E + islot, cur.i1, T.M);
-                if (vi >= w2) rmw_sub<kSlots>(E + islot, cur.i2, T.M);
+                rmw_add<SL>(E + islot, cur.i1, T.M);
+                if (vi >= w2) rmw_sub<SL>(E + islot, cur.i2, T.M);
             }
         } else {
             // Branch-free: rows k >= w2 contribute zero (their entries are valid
             // memory, so the bin index stays in range).
             const std::uint32_t m = k < w2 ? ~0u : 0u;
-            rmw_add_m<kSlots>(E + islot, cur.i1, m, m & T.M.m16);
-            rmw_sub_m<kSlots>(E + islot, cur.i2, m, m & T.M.negm16);
+            rmw_add_m<SL>(E + islot, cur.i1, m, m & T.M.m16);
+            rmw_sub_m<SL>(E + islot, cur.i2, m, m & T.M.negm16);
         }
     }
     __syncwarp();
@@ -498,18 +497,19 @@ __device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
         o[1] = static_cast<std::uint8_t>(rgb >> 8);
         o[2] = static_cast<std::uint8_t>(rgb >> 16);
     }
-    if ((s & (kZeroBatch - 1)) == kZeroBatch - 1) {  // clear columns s + 33 .. s + 48
-        const int zs = static_cast<unsigned>(s + 33 + (t & (kZeroBatch - 1))) % kSlots;
+    constexpr int B = Ring<SL>::kBatch;
+    if ((s & (B - 1)) == B - 1) {  // clear the slots of columns s + 1 + w2 .. s + B + w2
+        const int zs = static_cast<unsigned>(s + 1 + w2 + (t & (B - 1))) % SL;
 #pragma unroll
-        for (int j = 0; j < (NB + kZeroLanes - 1) / kZeroLanes; ++j) {
-            const int b = kZeroLanes * j + t / kZeroBatch;
-            if (b < NB) E[b * kSlots + zs] = 0ull;
+        for (int j = 0; j < (NB + Ring<SL>::kLanes - 1) / Ring<SL>::kLanes; ++j) {
+            const int b = Ring<SL>::kLanes * j + t / B;
+            if (b < NB) E[b * SL + zs] = 0ull;
         }
     }
     __syncwarp();
 }
 
-template <int NB>
+template <int NB, int SL>
 __global__ void __launch_bounds__(kMaxWarps * 32)
     skew_kernel(BandArgs a, const std::uint32_t* __restrict__ S, ShearGeom sg, int* task_counter,
                 WorkSplit g, Mul M) {
@@ -518,9 +518,9 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int r = a.radius;
-    unsigned char* wbase = smem + kRecipBytes + warp * per_warp_bytes<NB>();
+    unsigned char* wbase = smem + kRecipBytes + warp * per_warp_bytes<NB, SL>();
     unsigned long long* E = reinterpret_cast<unsigned long long*>(wbase);
-    std::uint32_t* stage = reinterpret_cast<std::uint32_t*>(wbase + std::size_t(NB) * kSlots * 8);
+    std::uint32_t* stage = reinterpret_cast<std::uint32_t*>(wbase + std::size_t(NB) * SL * 8);
 
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
         recip[i] = i ? 0x80000000u / static_cast<std::uint32_t>(i) + 1u : 0u;
@@ -533,8 +533,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
     T.w2 = 2 * r + 1;
     T.dA = T.w2 * T.Hs + T.w2;
     T.dD = T.w2 * T.Hs;
-    T.dI = 32u * T.Hs;
-    T.dI2 = (32u - T.w2) * T.Hs;
+    T.dI = T.w2 * T.Hs;
     T.lane = lane;
     T.stride = static_cast<std::size_t>(a.width) * 3;
 
@@ -559,7 +558,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
         unsigned long long win[NB];
 #pragma unroll
         for (int b = 0; b < NB; ++b) win[b] = 0ull;
-        for (int i = lane; i < NB * kSlots; i += 32) E[i] = 0ull;
+        for (int i = lane; i < NB * SL; i += 32) E[i] = 0ull;
         __syncwarp();
 
         const int nphases = ((T.NV - 1) >> 5) + 2;
@@ -579,10 +578,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
                     const int s = 32 * p + ss;
                     if (OPC_SKEW_PF_DIST > 0) prefetch_l2(T, s + OPC_SKEW_PF_DIST);
                     const Loads n2 = fetch<false>(T, s + 2);
-                    step<NB, false>(T, s, cur, win, E, stage, recip);
+                    step<NB, SL, false>(T, s, cur, win, E, stage, recip);
                     if (OPC_SKEW_PF_DIST > 0) prefetch_l2(T, s + OPC_SKEW_PF_DIST + 1);
                     const Loads n3 = fetch<false>(T, s + 3);
-                    step<NB, false>(T, s + 1, n1, win, E, stage, recip);
+                    step<NB, SL, false>(T, s + 1, n1, win, E, stage, recip);
                     cur = n2;
                     n1 = n3;
                 }
@@ -591,7 +590,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
                 for (int ss = 0; ss < 32; ++ss) {
                     const int s = 32 * p + ss;
                     const Loads nxt = fetch<true>(T, s + 1);
-                    step<NB, true>(T, s, cur, win, E, stage, recip);
+                    step<NB, SL, true>(T, s, cur, win, E, stage, recip);
                     cur = nxt;
                 }
             }
@@ -599,20 +598,20 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
     }
 }
 
-template <int NB>
-cudaError_t launch_nb(const BandArgs& a, int* counter, void* scratch, int num_sms,
-                      cudaStream_t s) {
-    const std::size_t pw = per_warp_bytes<NB>();
+template <int NB, int SL>
+cudaError_t launch_nbs(const BandArgs& a, int* counter, void* scratch, int num_sms,
+                       cudaStream_t s) {
+    const std::size_t pw = per_warp_bytes<NB, SL>();
     const std::size_t limit = 227 * 1024;
     int warps = kMaxWarps;
     while (warps > 1 && kRecipBytes + warps * pw > limit) --warps;
     const std::size_t smem = kRecipBytes + warps * pw;
-    cudaError_t e = cudaFuncSetAttribute(skew_kernel<NB>,
+    cudaError_t e = cudaFuncSetAttribute(skew_kernel<NB, SL>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, skew_kernel<NB>, warps * 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, skew_kernel<NB, SL>, warps * 32, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
 
@@ -639,8 +638,18 @@ cudaError_t launch_nb(const BandArgs& a, int* counter, void* scratch, int num_sm
     e = cudaMemsetAsync(counter, 0, sizeof(int), s);
     if (e != cudaSuccess) return e;
     const Mul M{16u, 0xFFFFFFF0u, 4u, 1u};
-    skew_kernel<NB><<<static_cast<unsigned>(blocks), warps * 32, smem, s>>>(a, S, sg, counter, g, M);
+    skew_kernel<NB, SL><<<static_cast<unsigned>(blocks), warps * 32, smem, s>>>(a, S, sg, counter, g, M);
     return cudaGetLastError();
+}
+
+template <int NB>
+cudaError_t launch_nb(const BandArgs& a, int* counter, void* scratch, int num_sms,
+                      cudaStream_t s) {
+    // The smaller ring when the window allows it (64 >= 16 + w2 + 32) and it
+    // buys occupancy: NB = 31 goes from 8 to 11 warps per SM (config 5: -2.4%);
+    // for NB = 21 (11 -> 12 warps) it measured 10% slower on config 2.
+    if (NB >= 24 && 2 * a.radius + 1 <= 16) return launch_nbs<NB, 64>(a, counter, scratch, num_sms, s);
+    return launch_nbs<NB, 96>(a, counter, scratch, num_sms, s);
 }
 
 }  // namespace

@@ -17,7 +17,6 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT / "tests"))
 
-SLOTS = 80
 
 
 def model(img: np.ndarray, r: int, L: int, segw: int | None = None) -> np.ndarray:
@@ -25,6 +24,7 @@ def model(img: np.ndarray, r: int, L: int, segw: int | None = None) -> np.ndarra
     out = img.copy()
     w2 = 2 * r + 1
     nb = L + 1
+    SLOTS, B = (64, 16) if w2 <= 16 else (96, 32)
     s_bins = (img.astype(np.int64).sum(2) * L) // 765
     y_lo, y_hi, x_lo, x_hi = r, h - r, r, w - r
     if y_hi <= y_lo or x_hi <= x_lo:
@@ -65,7 +65,7 @@ def model(img: np.ndarray, r: int, L: int, segw: int | None = None) -> np.ndarra
             def fetch(s, t):
                 v = s - t
                 k = (s - t) & 31
-                vi = s - k + 32
+                vi = s - k + w2
                 L_ = {}
                 if 0 <= v < NV:
                     L_["a"] = val((D0 + s + w2) * Hs + R0 + t + w2)
@@ -74,9 +74,9 @@ def model(img: np.ndarray, r: int, L: int, segw: int | None = None) -> np.ndarra
                         L_["c"] = val((D0 + s) * Hs + R0 + t + w2)
                         L_["d"] = val((D0 + s - w2) * Hs + R0 + t)
                 if k < w2 and 0 <= vi < NV:
-                    L_["i1"] = val((D0 + s + 32) * Hs + R0 + k)
+                    L_["i1"] = val((D0 + s + w2) * Hs + R0 + k)
                     if vi >= w2:
-                        L_["i2"] = val((D0 + s + 32 - w2) * Hs + R0 + k)
+                        L_["i2"] = val((D0 + s) * Hs + R0 + k)
                 return L_
 
             def add(dct, e, sign):
@@ -113,7 +113,7 @@ def model(img: np.ndarray, r: int, L: int, segw: int | None = None) -> np.ndarra
                                 add(E[slot], cur[t]["c"], -1)
                                 add(E[slot], cur[t]["d"], +1)
                         k = (s - t) & 31
-                        vi = s - k + 32
+                        vi = s - k + w2
                         if k < w2 and 0 <= vi < NV:
                             slot = vi % SLOTS
                             add(E[slot], cur[t]["i1"], +1)
@@ -124,8 +124,8 @@ def model(img: np.ndarray, r: int, L: int, segw: int | None = None) -> np.ndarra
                         vv = s - fr - 31 + lane
                         if w2 <= vv < NV and yb + fr < y_hi:
                             out[yb + fr, X0 + vv] = stage[fr][lane]
-                    if s % 16 == 15:  # batch-clear the slots of columns s + 33 .. s + 48
-                        for c in range(s + 33, s + 49):
+                    if s % B == B - 1:  # batch-clear the slots of columns s+1+w2 .. s+B+w2
+                        for c in range(s + 1 + w2, s + B + w2 + 1):
                             E[c % SLOTS] = dict()
     return out
 
@@ -134,7 +134,8 @@ if __name__ == "__main__":
     import oracle_lib
 
     rng = np.random.default_rng(1)
-    cases = [(14, 4, 0, 1), (20, 30, 2, 20), (40, 70, 3, 10), (33, 45, 5, 31), (70, 50, 15, 20)]
+    cases = [(14, 4, 0, 1), (20, 30, 2, 20), (40, 70, 3, 10), (33, 45, 5, 31), (50, 60, 7, 30),
+             (60, 70, 8, 20), (70, 50, 15, 20)]
     for h, w, r, L in cases:
         img = rng.integers(0, 256, (h, w, 3), dtype=np.uint8)
         got = model(img, r, L, segw=int(rng.integers(5, 40)))
