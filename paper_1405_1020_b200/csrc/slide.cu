@@ -237,8 +237,13 @@ __global__ void __launch_bounds__(kWarps * 32)
                     // Slide: add ring column x + 2r (image x + r), remove x - 1 (image x - r - 1).
                     const std::uint32_t* cin = ringp(x + 2 * r);
                     const std::uint32_t* cout = ringp(x - 1);
-                    bool diff = false;
-                    for (int k = 0; k < w2; ++k) diff |= cin[k] != cout[k];
+                    // Warp-wide flat check: the lanes' windows cover ring rows
+                    // 0 .. 31 + 2r, two rows per lane (was 2r+1 per lane: 23% of
+                    // the kernel's stall samples on C3).
+                    const std::uint32_t* cinb = cin - lane;
+                    const std::uint32_t* coutb = cout - lane;
+                    bool diff = cinb[lane] != coutb[lane];
+                    if (lane < 2 * r) diff |= cinb[lane + 32] != coutb[lane + 32];
                     if (__any_sync(FULL, diff)) {
                         const int best0 = best;
                         bool lost = false, cand = false;
