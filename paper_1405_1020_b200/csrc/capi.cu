@@ -318,15 +318,15 @@ int run_device(const opc::BandArgs& a, int border, int kernel, DevCtx* ctx, cuda
     cudaError_t e = cudaSuccess;
     if (kernel == OPC_KERNEL_SKEW && !opc::skew_fits(a)) kernel = OPC_KERNEL_DIRECT;
     if (kernel == OPC_KERNEL_SKEW) {
-        // Rotate over 64 task counters so kernels in flight on different
-        // streams never share one.
-        int* counter = ctx->d_counter + (ctx->counter_idx++ & 63u);
+        // Rotate over 16 task counters (16 bytes each: chunk index + 64-bit
+        // unit count) so kernels in flight on different streams never share one.
+        int* counter = ctx->d_counter + 4 * (ctx->counter_idx++ & 15u);
         const int rc = ensure(&ctx->d_scratch, &ctx->scratch_cap, opc::skew_scratch_bytes(a));
         if (rc != OPC_OK) return rc;
         e = opc::launch_skew(a, counter, ctx->d_scratch, ctx->num_sms, s);
         if (e != cudaSuccess) return cuda_error(e, "skew kernel launch");
     } else if (kernel == OPC_KERNEL_SLIDE) {
-        int* counter = ctx->d_counter + (ctx->counter_idx++ & 63u);
+        int* counter = ctx->d_counter + 4 * (ctx->counter_idx++ & 15u);
         const int rc = ensure(&ctx->d_scratch, &ctx->scratch_cap, opc::slide_scratch_bytes(a));
         if (rc != OPC_OK) return rc;
         e = opc::launch_slide(a, counter, ctx->d_scratch, ctx->num_sms, s);

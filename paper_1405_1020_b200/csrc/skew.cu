@@ -635,7 +635,7 @@ cudaError_t launch_nbs(const BandArgs& a, int* counter, void* scratch, int num_s
     if (blocks > static_cast<long long>(num_sms) * per_sm) blocks = num_sms * per_sm;
     if (blocks < 1) blocks = 1;
 
-    e = cudaMemsetAsync(counter, 0, sizeof(int), s);
+    e = cudaMemsetAsync(counter, 0, 4 * sizeof(int), s);
     if (e != cudaSuccess) return e;
     const Mul M{16u, 0xFFFFFFF0u, 4u, 1u};
     skew_kernel<NB, SL><<<static_cast<unsigned>(blocks), warps * 32, smem, s>>>(a, S, sg, counter, g, M);

@@ -26,6 +26,9 @@ namespace opc {
 
 namespace {
 
+#ifndef OPC_SLIDE_GUIDED_K
+#define OPC_SLIDE_GUIDED_K 0  // > 0: guided claims of remaining / (k x resident warps); measured no gain on C3
+#endif
 #ifndef OPC_SLIDE_MIN_CHUNK
 #define OPC_SLIDE_MIN_CHUNK 128
 #endif
@@ -371,11 +374,12 @@ cudaError_t launch_slide(const BandArgs& a, int* counter, void* scratch, int num
     // Each pass pays a full window build, rescan and window sums (~3(2r+1)^2 +
     // L updates per lane): keep chunks >= 128 columns.
     const WorkSplit g = make_split(a.frames, (a.y_hi - a.y_lo + 31) / 32, a.x_hi - a.x_lo, resident,
-                                   OPC_SLIDE_STATIC_PCT, OPC_SLIDE_MIN_CHUNK, OPC_SLIDE_DYN_PER_WARP);
+                                   OPC_SLIDE_STATIC_PCT, OPC_SLIDE_MIN_CHUNK, OPC_SLIDE_DYN_PER_WARP,
+                                   OPC_SLIDE_GUIDED_K);
     long long blocks = (g.nchunks + warps - 1) / warps;
     if (blocks > static_cast<long long>(num_sms) * per_sm) blocks = num_sms * per_sm;
     if (blocks < 1) blocks = 1;
-    e = cudaMemsetAsync(counter, 0, sizeof(int), s);
+    e = cudaMemsetAsync(counter, 0, 4 * sizeof(int), s);
     if (e != cudaSuccess) return e;
     slide_kernel<<<static_cast<unsigned>(blocks), warps * 32, smem, s>>>(a, T, tg, counter, g);
     return cudaGetLastError();

@@ -34,10 +34,15 @@ struct WorkSplit {
     int nbands, iw, pitch;  // pitch >= iw: units per band (segment-aligned chunks)
     int nstatic, nchunks;
     long long units, s1, s2;
+    // Guided mode (guided_div > 0): after the static chunks, the remainder is
+    // claimed from a 64-bit unit counter in pieces of max(s2, remaining /
+    // guided_div) -- large first, small at the end -- for kernels whose step
+    // cost depends on the content (slide), where equal chunks leave a tail.
+    long long guided_div;
 };
 
 inline WorkSplit make_split(int frames, int nbands, int iw, long long resident, int static_pct,
-                            long long min_chunk, int dyn_per_warp = 2) {
+                            long long min_chunk, int dyn_per_warp = 2, int guided_k = 0) {
     WorkSplit g{};
     g.nbands = nbands;
     g.iw = iw;
@@ -52,6 +57,11 @@ inline WorkSplit make_split(int frames, int nbands, int iw, long long resident, 
         const long long d = static_cast<long long>(dyn_per_warp) * resident;
         g.s2 = std::max(min_chunk, (rest + d - 1) / d);
         g.nchunks = g.nstatic + static_cast<int>((rest + g.s2 - 1) / g.s2);
+        if (guided_k > 0) {
+            g.s2 = min_chunk;
+            g.guided_div = static_cast<long long>(guided_k) * resident;
+            g.nchunks = g.nstatic;
+        }
     } else {
         // Dynamic only: equal segments of each band, as many as fill ~85% of
         // the resident warps in one round (C2: 48-column segments, 13% faster
@@ -90,6 +100,15 @@ OPC_HD inline void chunk_range(const WorkSplit& g, int i, long long& u, long lon
     if (u_end > g.units) u_end = g.units;
 }
 
+// Guided claim: given the units already claimed from the dynamic region
+// (approximate is fine), the size of the next piece.
+OPC_HD inline long long guided_size(const WorkSplit& g, long long claimed) {
+    const long long dyn = g.units - static_cast<long long>(g.nstatic) * g.s1;
+    const long long rem = dyn - claimed;
+    const long long q = rem / g.guided_div;
+    return q > g.s2 ? q : g.s2;
+}
+
 // Next pass inside [u, u_end): frame f, band kb, interior columns [x0, x1)
 // (relative to x_lo); advances u.  False when the chunk is exhausted.  A pass
 // never crosses a band end; the padding of a pitch > iw linearisation is skipped.
@@ -111,16 +130,35 @@ OPC_HD inline bool pass_in_chunk(const WorkSplit& g, long long& u, long long u_e
 #ifdef __CUDACC__
 // Warp-uniform iterator over this warp's passes.  State (u, u_end) starts at
 // (0, 0); each call returns the next pass or false when the launch's work is
-// exhausted (chunks are claimed from `counter` by lane 0).
+// exhausted.  Chunks are claimed by lane 0 from counter[0] (chunk index) and,
+// in guided mode, counter[2..3] (64-bit unit count; 16-byte-aligned counter,
+// 16 bytes zeroed by the launcher).
 __device__ __forceinline__ bool next_pass(const WorkSplit& g, int* counter, int lane, long long& u,
                                           long long& u_end, int& f, int& kb, int& x0, int& x1) {
     for (;;) {
         if (pass_in_chunk(g, u, u_end, f, kb, x0, x1)) return true;
-        int i = 0;
-        if (lane == 0) i = atomicAdd(counter, 1);
-        i = __shfl_sync(0xFFFFFFFFu, i, 0);
-        if (i >= g.nchunks) return false;
-        chunk_range(g, i, u, u_end);
+        long long a = 0, b = 0;
+        int done = 0;
+        if (lane == 0) {
+            const int i = atomicAdd(counter, 1);
+            if (i < g.nchunks) {
+                chunk_range(g, i, a, b);  // (an empty static chunk: claim again)
+            } else if (g.guided_div > 0) {
+                // counter[2..3]: the 64-bit count of dynamic units claimed
+                unsigned long long* uc = reinterpret_cast<unsigned long long*>(counter + 2);
+                const long long seen = static_cast<long long>(*reinterpret_cast<volatile unsigned long long*>(uc));
+                const long long size = guided_size(g, seen);
+                const long long base = static_cast<long long>(g.nstatic) * g.s1;
+                a = base + static_cast<long long>(atomicAdd(uc, static_cast<unsigned long long>(size)));
+                b = a + size < g.units ? a + size : g.units;
+                done = a >= b;
+            } else {
+                done = 1;
+            }
+        }
+        if (__shfl_sync(0xFFFFFFFFu, done, 0)) return false;
+        u = __shfl_sync(0xFFFFFFFFu, a, 0);
+        u_end = __shfl_sync(0xFFFFFFFFu, b, 0);
     }
 }
 #endif

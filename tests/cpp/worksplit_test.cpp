@@ -9,13 +9,29 @@
 #include "worksplit.cuh"
 
 static int check(int frames, int nbands, int iw, long long blocks, int wpb, int pct, long long minc,
-                 int dyn) {
-    const opc::WorkSplit g = opc::make_split(frames, nbands, iw, blocks * wpb, pct, minc, dyn);
+                 int dyn, int guided) {
+    const opc::WorkSplit g = opc::make_split(frames, nbands, iw, blocks * wpb, pct, minc, dyn, guided);
     std::vector<unsigned char> seen(static_cast<std::size_t>(frames) * nbands * iw, 0);
     long long passes = 0;
+    // chunks as the kernels claim them: indexed chunks, then (guided mode)
+    // pieces of the unit counter, claimed one after another here
+    std::vector<std::pair<long long, long long>> chunks;
     for (int i = 0; i < g.nchunks; ++i) {
         long long u, u_end;
         opc::chunk_range(g, i, u, u_end);
+        chunks.push_back({u, u_end});
+    }
+    if (g.guided_div > 0) {
+        const long long base = static_cast<long long>(g.nstatic) * g.s1;
+        for (long long claimed = 0;;) {
+            const long long size = opc::guided_size(g, claimed);
+            const long long a = base + claimed, b = a + size < g.units ? a + size : g.units;
+            if (a >= b) break;
+            chunks.push_back({a, b});
+            claimed += size;
+        }
+    }
+    for (auto [u, u_end] : chunks) {
         int f, kb, x0, x1;
         while (opc::pass_in_chunk(g, u, u_end, f, kb, x0, x1)) {
             ++passes;
@@ -56,11 +72,13 @@ int main() {
             for (int iw : iw_)
                 for (int wpb : wpb_)
                     for (long long blocks : blocks_)
-                        for (int pct : {50, 98, 100}) {
-                            if (static_cast<long long>(frames) * nbands * iw > 20000000) continue;
-                            fails += check(frames, nbands, iw, blocks, wpb, pct, 128, pct == 50 ? 2 : 3);
-                            ++n;
-                        }
+                        for (int pct : {0, 50, 98, 100})
+                            for (int guided : {0, 4}) {
+                                if (static_cast<long long>(frames) * nbands * iw > 20000000) continue;
+                                fails += check(frames, nbands, iw, blocks, wpb, pct, 128,
+                                               pct == 50 ? 2 : 3, guided);
+                                ++n;
+                            }
     std::printf("%d shapes, %d failures\n", n, fails);
     return fails ? 1 : 0;
 }
