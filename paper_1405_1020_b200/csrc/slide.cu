@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(kWarps * 32)
 
     long long u = 0, u_end = 0;
     int f, kb, x0, x1;
-    while (next_pass(g, task_counter, lane, u, u_end, f, kb, x0, x1)) {
+    while (next_pass<(OPC_SLIDE_GUIDED_K > 0)>(g, task_counter, lane, u, u_end, f, kb, x0, x1)) {
         const int yb = a.y_lo + 32 * kb;
         const int xs = a.x_lo + x0;
         const int xe = a.x_lo + x1;

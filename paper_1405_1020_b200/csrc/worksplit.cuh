@@ -133,10 +133,21 @@ OPC_HD inline bool pass_in_chunk(const WorkSplit& g, long long& u, long long u_e
 // exhausted.  Chunks are claimed by lane 0 from counter[0] (chunk index) and,
 // in guided mode, counter[2..3] (64-bit unit count; 16-byte-aligned counter,
 // 16 bytes zeroed by the launcher).
+// GUIDED = false compiles the guided claim out (registers: the skew kernel for
+// NB = 31 spilled with it).
+template <bool GUIDED = false>
 __device__ __forceinline__ bool next_pass(const WorkSplit& g, int* counter, int lane, long long& u,
                                           long long& u_end, int& f, int& kb, int& x0, int& x1) {
     for (;;) {
         if (pass_in_chunk(g, u, u_end, f, kb, x0, x1)) return true;
+        if (!GUIDED) {
+            int i = 0;
+            if (lane == 0) i = atomicAdd(counter, 1);
+            i = __shfl_sync(0xFFFFFFFFu, i, 0);
+            if (i >= g.nchunks) return false;
+            chunk_range(g, i, u, u_end);
+            continue;
+        }
         long long a = 0, b = 0;
         int done = 0;
         if (lane == 0) {
