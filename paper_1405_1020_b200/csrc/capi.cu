@@ -251,11 +251,16 @@ std::mutex g_ctx_mu;
 std::vector<std::unique_ptr<DevCtx>> g_ctx;
 
 int get_ctx(int device, DevCtx** out) {
-    int count = 0;
-    cudaError_t e = cudaGetDeviceCount(&count);
-    if (e != cudaSuccess || count == 0) {
-        return set_error(OPC_ECUDA, std::string("no CUDA device available: ") +
-                                        (e == cudaSuccess ? "0 devices" : cudaGetErrorString(e)));
+    static std::atomic<int> known_count{0};  // device count once one was seen
+    int count = known_count.load();
+    cudaError_t e = cudaSuccess;
+    if (count == 0) {
+        e = cudaGetDeviceCount(&count);
+        if (e != cudaSuccess || count == 0) {
+            return set_error(OPC_ECUDA, std::string("no CUDA device available: ") +
+                                            (e == cudaSuccess ? "0 devices" : cudaGetErrorString(e)));
+        }
+        known_count.store(count);
     }
     if (device < 0) {
         e = cudaGetDevice(&device);

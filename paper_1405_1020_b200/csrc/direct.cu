@@ -78,6 +78,69 @@ __global__ void __launch_bounds__(kDirectThreads)
     o[2] = static_cast<std::uint8_t>(sb / best_count);
 }
 
+// Small windows (r <= 3) with few bins (L+1 <= 64): a 32x8 output tile per
+// block, its (32+2r) x (8+2r) input pixels loaded once into shared memory as
+// entries R | G << 8 | B << 16 | bin << 24 (bin computed once per pixel instead
+// of twice per window position), then the same two passes from shared memory.
+constexpr int kTileW = 32, kTileH = 8, kTileMaxR = 3, kTileMaxBins = 64;
+
+__global__ void __launch_bounds__(kTileW * kTileH)
+    direct_tile_kernel(BandArgs a) {
+    __shared__ std::uint32_t tile[(kTileH + 2 * kTileMaxR) * (kTileW + 2 * kTileMaxR)];
+    extern __shared__ std::uint32_t counts[];  // [bins][256]
+    const int r = a.radius;
+    const int tw = kTileW + 2 * r, th = kTileH + 2 * r;
+    const int x0 = a.x_lo + blockIdx.x * kTileW;  // first output column of the tile
+    const int y0 = a.y_lo + blockIdx.y * kTileH;
+    const int frame = blockIdx.z;
+    const std::size_t stride = static_cast<std::size_t>(a.width) * 3;
+    const std::uint8_t* in = a.in + a.in_frame_stride * frame;
+    const int tid = threadIdx.y * kTileW + threadIdx.x;
+    for (int i = tid; i < tw * th; i += kTileW * kTileH) {
+        const int ty = i / tw, tx = i - ty * tw;
+        const int x = min(x0 - r + tx, a.width - 1), y = min(y0 - r + ty, a.in_row0 + a.in_rows - 1);
+        const std::uint8_t* p = in + static_cast<std::size_t>(y - a.in_row0) * stride +
+                                static_cast<std::size_t>(x) * 3;
+        const unsigned R = p[0], G = p[1], B = p[2];
+        tile[i] = R | G << 8 | B << 16 | bin_of(R + G + B, a.levels, a.bin_mul) << 24;
+    }
+    __syncthreads();
+    const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
+    if (x >= a.x_hi || y >= a.y_hi) return;
+    const int bins = a.levels + 1;
+    constexpr int T = kTileW * kTileH;
+    for (int b = 0; b < bins; ++b) counts[b * T + tid] = 0;
+    const int w2 = 2 * r + 1;
+    const std::uint32_t* base = tile + threadIdx.y * tw + threadIdx.x;
+    for (int dy = 0; dy < w2; ++dy) {
+        for (int dx = 0; dx < w2; ++dx) counts[(base[dy * tw + dx] >> 24) * T + tid] += 1;
+    }
+    unsigned best = 0, best_count = counts[tid];
+    for (int b = 1; b < bins; ++b) {
+        const unsigned c = counts[b * T + tid];
+        if (c > best_count) {  // strict '>' keeps the lowest index on ties (filter.hpp:71-82)
+            best_count = c;
+            best = b;
+        }
+    }
+    unsigned sr = 0, sg = 0, sb = 0;
+    for (int dy = 0; dy < w2; ++dy) {
+        for (int dx = 0; dx < w2; ++dx) {
+            const std::uint32_t e = base[dy * tw + dx];
+            if ((e >> 24) == best) {
+                sr += e & 0xFFu;
+                sg += (e >> 8) & 0xFFu;
+                sb += (e >> 16) & 0xFFu;
+            }
+        }
+    }
+    std::uint8_t* o = a.out + a.out_frame_stride * frame +
+                      static_cast<std::size_t>(y - a.out_row0) * stride + static_cast<std::size_t>(x) * 3;
+    o[0] = static_cast<std::uint8_t>(sr / best_count);  // filter.cpp:41-43
+    o[1] = static_cast<std::uint8_t>(sg / best_count);
+    o[2] = static_cast<std::uint8_t>(sb / best_count);
+}
+
 // Border pixels of the output band (filter.cpp:54 / parallel.cpp:113):
 // CopyInput copies the input bytes, ZeroFill writes zeros.  The flat byte
 // index space is [full border rows][left+right strips of interior rows].
@@ -134,11 +197,20 @@ std::uint32_t bin_multiplier(int levels) {
 
 cudaError_t launch_direct(const BandArgs& a, cudaStream_t s) {
     if (a.y_hi <= a.y_lo || a.x_hi <= a.x_lo || a.frames <= 0) return cudaSuccess;
+    if (a.radius <= kTileMaxR && a.levels + 1 <= kTileMaxBins && a.levels <= 255) {
+        const std::size_t smem = static_cast<std::size_t>(a.levels + 1) * kTileW * kTileH * 4;
+        cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(direct_tile_kernel), static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        const dim3 grid(static_cast<unsigned>((a.x_hi - a.x_lo + kTileW - 1) / kTileW),
+                        static_cast<unsigned>((a.y_hi - a.y_lo + kTileH - 1) / kTileH),
+                        static_cast<unsigned>(a.frames));
+        direct_tile_kernel<<<grid, dim3(kTileW, kTileH), smem, s>>>(a);
+        return cudaGetLastError();
+    }
     const long long pixels = static_cast<long long>(a.y_hi - a.y_lo) * (a.x_hi - a.x_lo);
     const std::size_t smem =
         static_cast<std::size_t>(a.levels + 1) * kDirectThreads * sizeof(std::uint32_t);
-    cudaError_t e = cudaFuncSetAttribute(direct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+    cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(direct_kernel), static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     const dim3 grid(static_cast<unsigned>((pixels + kDirectThreads - 1) / kDirectThreads),
                     static_cast<unsigned>(a.frames));

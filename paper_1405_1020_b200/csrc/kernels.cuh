@@ -5,10 +5,47 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include <cuda_runtime.h>
 
 namespace opc {
+
+// Per-device caches of kernel attributes (the launchers run on every call;
+// cudaFuncSetAttribute / occupancy queries are a few microseconds each, which
+// small images feel).
+inline cudaError_t set_smem_attr(const void* func, int bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, int> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    int& have = done[{dev, func}];
+    if (have >= bytes) return cudaSuccess;
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) have = bytes;
+    return e;
+}
+
+inline cudaError_t blocks_per_sm(const void* func, int threads, std::size_t smem, int* out) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, const void*, int, std::size_t>, int> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = done.find({dev, func, threads, smem});
+    if (it != done.end()) {
+        *out = it->second;
+        return cudaSuccess;
+    }
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, func, threads, smem);
+    if (e == cudaSuccess) done[{dev, func, threads, smem}] = *out;
+    return e;
+}
 
 // One launch produces output rows [y_begin, y_end) of `frames` frames of a
 // width x height image.  Input buffer row 0 is image row in_row0 and holds

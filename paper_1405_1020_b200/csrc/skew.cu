@@ -606,12 +606,11 @@ cudaError_t launch_nbs(const BandArgs& a, int* counter, void* scratch, int num_s
     int warps = kMaxWarps;
     while (warps > 1 && kRecipBytes + warps * pw > limit) --warps;
     const std::size_t smem = kRecipBytes + warps * pw;
-    cudaError_t e = cudaFuncSetAttribute(skew_kernel<NB, SL>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+    cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(skew_kernel<NB, SL>),
+                                  static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, skew_kernel<NB, SL>, warps * 32, smem);
+    e = blocks_per_sm(reinterpret_cast<const void*>(skew_kernel<NB, SL>), warps * 32, smem, &per_sm);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
 

@@ -353,11 +353,10 @@ cudaError_t launch_slide(const BandArgs& a, int* counter, void* scratch, int num
     int warps = kWarps;
     while (warps > 1 && kRecipBytes + warps * pw > limit) --warps;
     const std::size_t smem = kRecipBytes + warps * pw;
-    cudaError_t e = cudaFuncSetAttribute(slide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+    cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(slide_kernel), static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, slide_kernel, warps * 32, smem);
+    e = blocks_per_sm(reinterpret_cast<const void*>(slide_kernel), warps * 32, smem, &per_sm);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
 
