@@ -16,16 +16,19 @@
 //    -- four dynamic-bin updates.  Lane t reads E(x,y) at step s and advances it
 //    to row y+1; lane t+1 consumes it at step s+1.  The skew turns the vertical
 //    recurrence into a pipeline across the lanes.
-//  * E(x, band top) is built from scratch (2(2r+1) updates per column), the
-//    lane of column vi working on row k = (s - t) mod 32 at step s, which
-//    finishes each column exactly one step before lane 0 first reads it.
+//  * E(x, band top) is built from scratch (2(2r+1) updates per column): at step
+//    s lane t adds row k = (s - t) mod 32 (if k < 2r+1) of column s - k + 2r+1,
+//    which finishes each column exactly one step before lane 0 first reads it.
 //  * Pixels come from a SHEARED entry plane S[d = x + y][y] written by
-//    shear_kernel (u32 = R | G<<8 | B<<16 | bin<<24): every pixel a warp needs
+//    shear_kernel (u32 = B | R<<8 | G<<18 | bin<<26): every pixel a warp needs
 //    at step s lies on one of six anti-diagonals, 32 consecutive rows each, so
 //    every access is a single coalesced 128-byte load.
-//  * Argmax: a static tournament over the NB words comparing counts only
-//    (hi word > other.hi | 0x3FFFFF <=> strictly larger count), left (lower
-//    bin) operand kept on ties -> lowest-index maximum, filter.hpp:71-82.
+//  * Argmax ("max-scan"): the largest hi word carries the largest count; a scan
+//    from the top bin down keeps the last (lowest-index) bin whose count equals
+//    it, filter.hpp:71-82.  The conditional copies are predicated IMADs (FMA
+//    pipe), the max a tree of 3-input integer max ops (ALU pipe).
+//  * Work split: persistent CTAs, equal static shares per warp plus a small
+//    dynamic remainder (worksplit.cuh).
 //  * Quotient: q = umulhi(2*sum, floor(2^31/c)+1), exact for c <= 1023,
 //    sum <= 255c (tests/test_oracle.py checks it exhaustively); filter.cpp:41-43.
 //  * Output: a 32x32 staging tile; each step one row completes a 32-pixel
