@@ -277,6 +277,7 @@ def main() -> None:
     import torch
     import torch.distributed as dist
     import paper_1405_1020_b200 as opc
+    from paper_1405_1020_b200 import _lib
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -335,6 +336,9 @@ def main() -> None:
     launches0 = opc.kernel_launches()
     barrier()
     torch.cuda.synchronize()
+    # live per-kernel timing: the library brackets each of its kernel launches
+    # with CUDA events on the launch stream (opc_kernel_timing)
+    opc.kernel_timing(True)
     with ClockSampler(local) as clocks:
         clocks.mark_start()
         with torch.cuda.stream(stream):
@@ -348,6 +352,11 @@ def main() -> None:
     barrier()
     launches = opc.kernel_launches() - launches0
     step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    family = opc.plan_kernel(W, H, r, L)  # kernel ids 1-3 = OPC_KERNEL_DIRECT/SKEW/SLIDE
+    kernel_total_ms, kernel_n = opc.kernel_timing_read(family)
+    pre_ms, _ = opc.kernel_timing_read(_lib.OPC_KID_PREPASS)
+    border_ms, _ = opc.kernel_timing_read(_lib.OPC_KID_BORDER)
+    opc.kernel_timing(False)
     total_ms = ev[0].elapsed_time(ev[args.steps])
     t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{local}")
     if world > 1:
@@ -392,8 +401,11 @@ def main() -> None:
     num_sms = torch.cuda.get_device_properties(local).multi_processor_count
     peak_ops = num_sms * 4 * 32 * sm_mhz * 1e6
     ops_px = colhist_ops_per_px(L + 1)
-    kernel_ms = statistics.mean(step_ms)
-    achieved_ops = ops_px * interior / (kernel_ms / 1e3)
+    # achieved = algorithmic lane-ops of the timed steps / time inside the
+    # dominant kernel (its launches, CUDA events on the launch stream)
+    kernel_ms = kernel_total_ms / max(1, kernel_n)
+    achieved_ops = ops_px * interior * args.steps / (kernel_total_ms / 1e3)
+    step_total_ms = sum(step_ms)
     traffic = None
     tp = ROOT / "profiles" / f"{cfg.name}_dram_bytes.json"
     if tp.exists():
@@ -406,10 +418,17 @@ def main() -> None:
         "frac": round(achieved_ops / peak_ops, 4), "traffic": traffic,
         "model": f"colhist {ops_px} lane-ops per interior pixel (SURVEY 8d, B={L + 1}); "
                  f"{num_sms} SMs x 4 x 32 x {sm_mhz:.0f} MHz ({peaks_kind} sm_max_mhz)",
-        "algorithmic_ops_per_launch": ops_px * interior,
+        "algorithmic_ops_per_launch": ops_px * interior * args.steps // max(1, kernel_n),
+        "kernel": {1: "direct", 2: "skew", 3: "slide"}.get(family, str(family)),
         "kernel_ms": round(kernel_ms, 4),
-        "hbm": {"achieved_gbs": round(alg_bytes / (kernel_ms / 1e3) / 1e9, 1),
-                "peak_gbs": hbm_gbs, "frac": round(alg_bytes / (kernel_ms / 1e3) / 1e9 / hbm_gbs, 4),
+        "kernel_launches": kernel_n,
+        "step_share": {"kernel": round(kernel_total_ms / step_total_ms, 4),
+                       "pre_pass": round(pre_ms / step_total_ms, 4),
+                       "border": round(border_ms / step_total_ms, 4)},
+        "frac_of_step": round(ops_px * interior * args.steps / (step_total_ms / 1e3) / peak_ops, 4),
+        "hbm": {"achieved_gbs": round(alg_bytes * args.steps / (step_total_ms / 1e3) / 1e9, 1),
+                "peak_gbs": hbm_gbs,
+                "frac": round(alg_bytes * args.steps / (step_total_ms / 1e3) / 1e9 / hbm_gbs, 4),
                 "bytes_per_launch": alg_bytes, "peak_kind": peaks_kind},
     }
 

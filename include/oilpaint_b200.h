@@ -128,6 +128,20 @@ int32_t opc_device_count(void);
 /* Blocks until all work the library queued on cfg's device/stream is done. */
 int opc_synchronize(const opc_config* cfg);
 
+/* Live kernel timing for benchmarks: with timing enabled every kernel launch
+ * of the library is bracketed by CUDA events on its stream.
+ * opc_kernel_timing(1) starts (and clears), opc_kernel_timing(0) stops;
+ * opc_kernel_timing_read sums the recorded launches of one kernel
+ * (synchronizing on their events).  Ids: 1 direct, 2 skew, 3 slide, 4 the
+ * pre-pass (shear / transpose), 5 border. */
+#define OPC_KID_DIRECT 1
+#define OPC_KID_SKEW 2
+#define OPC_KID_SLIDE 3
+#define OPC_KID_PREPASS 4
+#define OPC_KID_BORDER 5
+int opc_kernel_timing(int32_t enable);
+int opc_kernel_timing_read(int32_t kernel_id, double* ms_total, int64_t* launches);
+
 /* Which kernel family OPC_KERNEL_AUTO would use for these parameters
  * (OPC_KERNEL_*), or -1 if invalid.  Host logic only. */
 int32_t opc_plan_kernel(int32_t width, int32_t height, int32_t radius, int32_t levels);

@@ -24,8 +24,11 @@ EXPORTS = (
     "opc_band_in_row0", "opc_band_in_rows", "opc_last_error", "opc_version",
     "opc_kernel_launches", "opc_device_count", "opc_synchronize", "opc_plan_kernel",
     "opc_release", "opc_generate", "opc_filter_rgb8_multi", "opc_band_begin",
-    "opc_generate_device",
+    "opc_generate_device", "opc_kernel_timing", "opc_kernel_timing_read",
 )
+
+
+OPC_KID_DIRECT, OPC_KID_SKEW, OPC_KID_SLIDE, OPC_KID_PREPASS, OPC_KID_BORDER = 1, 2, 3, 4, 5
 
 
 class opc_config(ctypes.Structure):
@@ -85,6 +88,11 @@ def _load() -> ctypes.CDLL:
     lib.opc_generate.restype = ctypes.c_int
     lib.opc_generate_device.argtypes = [i32, ctypes.c_uint64, i32, i32, u8p, i32, ctypes.c_void_p]
     lib.opc_generate_device.restype = ctypes.c_int
+    lib.opc_kernel_timing.argtypes = [i32]
+    lib.opc_kernel_timing.restype = ctypes.c_int
+    lib.opc_kernel_timing_read.argtypes = [i32, ctypes.POINTER(ctypes.c_double),
+                                           ctypes.POINTER(ctypes.c_int64)]
+    lib.opc_kernel_timing_read.restype = ctypes.c_int
     return lib
 
 

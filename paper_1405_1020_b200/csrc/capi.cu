@@ -247,6 +247,41 @@ bool is_pinned_or_device(const void* p) {
     return attr.type != cudaMemoryTypeUnregistered;
 }
 
+// ---- live kernel timing (opc_kernel_timing) ----
+struct TimedLaunch {
+    int id;
+    cudaEvent_t start, stop;
+};
+std::mutex g_timing_mu;
+std::vector<TimedLaunch> g_timed;     // recorded launches
+std::vector<cudaEvent_t> g_ev_pool;   // spare events
+cudaEvent_t g_open_start[8] = {};     // per kernel id: start recorded, stop pending
+
+cudaEvent_t take_event() {
+    if (!g_ev_pool.empty()) {
+        cudaEvent_t e = g_ev_pool.back();
+        g_ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+void timing_hook(int id, int phase, cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(g_timing_mu);
+    if (id < 0 || id >= 8) return;
+    if (phase == 0) {
+        g_open_start[id] = take_event();
+        cudaEventRecord(g_open_start[id], s);
+    } else if (g_open_start[id]) {
+        cudaEvent_t stop = take_event();
+        cudaEventRecord(stop, s);
+        g_timed.push_back({id, g_open_start[id], stop});
+        g_open_start[id] = nullptr;
+    }
+}
+
 std::mutex g_ctx_mu;
 std::vector<std::unique_ptr<DevCtx>> g_ctx;
 
@@ -650,7 +685,40 @@ int filter_core(const std::uint8_t* in, std::uint8_t* out, int frames, int w, in
 
 }  // namespace
 
+namespace opc {
+TimingHook g_timing_hook = nullptr;
+}  // namespace opc
+
 extern "C" {
+
+int opc_kernel_timing(int32_t enable) {
+    std::lock_guard<std::mutex> lk(g_timing_mu);
+    for (const TimedLaunch& t : g_timed) {
+        g_ev_pool.push_back(t.start);
+        g_ev_pool.push_back(t.stop);
+    }
+    g_timed.clear();
+    opc::g_timing_hook = enable ? timing_hook : nullptr;
+    return OPC_OK;
+}
+
+int opc_kernel_timing_read(int32_t kernel_id, double* ms_total, int64_t* launches) {
+    std::lock_guard<std::mutex> lk(g_timing_mu);
+    double total = 0;
+    long long n = 0;
+    for (const TimedLaunch& t : g_timed) {
+        if (t.id != kernel_id) continue;
+        cudaError_t e = cudaEventSynchronize(t.stop);
+        float ms = 0;
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, t.start, t.stop);
+        if (e != cudaSuccess) return cuda_error(e, "cudaEventElapsedTime");
+        total += ms;
+        ++n;
+    }
+    if (ms_total) *ms_total = total;
+    if (launches) *launches = n;
+    return OPC_OK;
+}
 
 int opc_validate(int32_t width, int32_t height, uint64_t nbytes, int32_t radius, int32_t levels,
                  uint32_t flags) {

@@ -204,7 +204,9 @@ cudaError_t launch_direct(const BandArgs& a, cudaStream_t s) {
         const dim3 grid(static_cast<unsigned>((a.x_hi - a.x_lo + kTileW - 1) / kTileW),
                         static_cast<unsigned>((a.y_hi - a.y_lo + kTileH - 1) / kTileH),
                         static_cast<unsigned>(a.frames));
+        timing_mark(kIdDirect, 0, s);
         direct_tile_kernel<<<grid, dim3(kTileW, kTileH), smem, s>>>(a);
+        timing_mark(kIdDirect, 1, s);
         return cudaGetLastError();
     }
     const long long pixels = static_cast<long long>(a.y_hi - a.y_lo) * (a.x_hi - a.x_lo);
@@ -214,7 +216,9 @@ cudaError_t launch_direct(const BandArgs& a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     const dim3 grid(static_cast<unsigned>((pixels + kDirectThreads - 1) / kDirectThreads),
                     static_cast<unsigned>(a.frames));
+    timing_mark(kIdDirect, 0, s);
     direct_kernel<<<grid, kDirectThreads, smem, s>>>(a, pixels);
+    timing_mark(kIdDirect, 1, s);
     return cudaGetLastError();
 }
 
@@ -234,8 +238,10 @@ cudaError_t launch_border(const BandArgs& a, int policy, cudaStream_t s) {
     const int threads = 256;
     const dim3 grid(static_cast<unsigned>((per_frame + threads - 1) / threads),
                     static_cast<unsigned>(a.frames));
+    timing_mark(kIdBorder, 0, s);
     border_kernel<<<grid, threads, 0, s>>>(a, policy, full_bytes, strip_bytes, top_rows, top_lo,
                                            bot_lo);
+    timing_mark(kIdBorder, 1, s);
     return cudaGetLastError();
 }
 

@@ -47,6 +47,16 @@ inline cudaError_t blocks_per_sm(const void* func, int threads, std::size_t smem
     return e;
 }
 
+// Live kernel timing (opc_kernel_timing in the C-ABI): when a hook is set, the
+// launchers call it right before (phase 0) and after (phase 1) each kernel
+// launch, on the launch's stream, and the C-ABI records CUDA events there.
+enum KernelId { kIdDirect = 1, kIdSkew = 2, kIdSlide = 3, kIdPrePass = 4, kIdBorder = 5 };
+using TimingHook = void (*)(int id, int phase, cudaStream_t s);
+extern TimingHook g_timing_hook;
+inline void timing_mark(int id, int phase, cudaStream_t s) {
+    if (g_timing_hook) g_timing_hook(id, phase, s);
+}
+
 // One launch produces output rows [y_begin, y_end) of `frames` frames of a
 // width x height image.  Input buffer row 0 is image row in_row0 and holds
 // in_rows rows; output buffer row 0 is image row out_row0.  Interior rows

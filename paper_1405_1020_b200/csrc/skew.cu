@@ -625,7 +625,9 @@ cudaError_t launch_nbs(const BandArgs& a, int* counter, void* scratch, int num_s
         const int vec_ok = (reinterpret_cast<std::uintptr_t>(a.in) % 4 == 0) &&
                            ((static_cast<std::size_t>(a.width) * 3) % 4 == 0) &&
                            (a.in_frame_stride % 4 == 0);
+        timing_mark(kIdPrePass, 0, s);
         shear_kernel<<<grid, 256, 0, s>>>(a, S, sg, vec_ok);
+        timing_mark(kIdPrePass, 1, s);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
@@ -640,7 +642,9 @@ cudaError_t launch_nbs(const BandArgs& a, int* counter, void* scratch, int num_s
     e = cudaMemsetAsync(counter, 0, 4 * sizeof(int), s);
     if (e != cudaSuccess) return e;
     const Mul M{16u, 0xFFFFFFF0u, 4u, 1u};
+    timing_mark(kIdSkew, 0, s);
     skew_kernel<NB, SL><<<static_cast<unsigned>(blocks), warps * 32, smem, s>>>(a, S, sg, counter, g, M);
+    timing_mark(kIdSkew, 1, s);
     return cudaGetLastError();
 }
 

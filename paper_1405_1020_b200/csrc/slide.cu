@@ -365,7 +365,9 @@ cudaError_t launch_slide(const BandArgs& a, int* counter, void* scratch, int num
     {
         const dim3 grid(static_cast<unsigned>((a.width + 64 + kTCols - 1) / kTCols),
                         static_cast<unsigned>(tg.Hs / kTRows), static_cast<unsigned>(a.frames));
+        timing_mark(kIdPrePass, 0, s);
         transpose_kernel<<<grid, 256, 0, s>>>(a, T, tg);
+        timing_mark(kIdPrePass, 1, s);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
@@ -380,7 +382,9 @@ cudaError_t launch_slide(const BandArgs& a, int* counter, void* scratch, int num
     if (blocks < 1) blocks = 1;
     e = cudaMemsetAsync(counter, 0, 4 * sizeof(int), s);
     if (e != cudaSuccess) return e;
+    timing_mark(kIdSlide, 0, s);
     slide_kernel<<<static_cast<unsigned>(blocks), warps * 32, smem, s>>>(a, T, tg, counter, g);
+    timing_mark(kIdSlide, 1, s);
     return cudaGetLastError();
 }
 

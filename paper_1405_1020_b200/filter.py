@@ -190,6 +190,19 @@ def kernel_launches() -> int:
     return LIB.opc_kernel_launches()
 
 
+def kernel_timing(enable: bool) -> None:
+    """Start (and clear) or stop live CUDA-event timing of every kernel launch."""
+    _raise(LIB.opc_kernel_timing(1 if enable else 0))
+
+
+def kernel_timing_read(kernel_id: int) -> tuple[float, int]:
+    """(total ms, launches) recorded for one kernel id (_lib.OPC_KID_*)."""
+    ms = ctypes.c_double(0.0)
+    n = ctypes.c_int64(0)
+    _raise(LIB.opc_kernel_timing_read(kernel_id, ctypes.byref(ms), ctypes.byref(n)))
+    return ms.value, n.value
+
+
 def device_count() -> int:
     return LIB.opc_device_count()
 
