@@ -17,8 +17,9 @@
 //    to row y+1; lane t+1 consumes it at step s+1.  The skew turns the vertical
 //    recurrence into a pipeline across the lanes.
 //  * E(x, band top) is built from scratch (2(2r+1) updates per column): at step
-//    s lane t adds row k = (s - t) mod 32 (if k < 2r+1) of column s - k + 2r+1,
-//    which finishes each column exactly one step before lane 0 first reads it.
+//    s lane t < 2r+1 adds row t of column s - t + 2r+1 (one diagonal, one
+//    coalesced load; the pixel it removes is the E update's own load b), which
+//    finishes each column exactly one step before lane 0 first reads it.
 //  * Pixels come from a SHEARED entry plane S[d = x + y][y] written by
 //    shear_kernel (u32 = B | R<<8 | G<<18 | bin<<26): every pixel a warp needs
 //    at step s lies on one of six anti-diagonals, 32 consecutive rows each, so
@@ -225,16 +226,17 @@ template <int SL>
 __device__ __forceinline__ void rmw_sub(unsigned long long* Es, std::uint32_t e, const Mul& M) {
     packed_sub(Es + (e >> 26) * SL, entry_lo(e), entry_r1(e), M.negm16);
 }
-// Masked forms for the branch-free init: mask = all ones or zero, m16 = 16 or
-// 0, nm16 = -16 or 0.
+
+// Masked forms (all lanes execute; lanes with mask 0 add zero): lo & mask,
+// multiplier m16 = 16 & mask or nm16 = -16 & mask.
 template <int SL>
 __device__ __forceinline__ void rmw_add_m(unsigned long long* Es, std::uint32_t e, std::uint32_t mask,
-                                          std::uint32_t m16) {
+                                          std::uint32_t m16, const Mul& M) {
     packed_add(Es + (e >> 26) * SL, entry_lo(e) & mask, entry_r1(e), m16);
 }
 template <int SL>
 __device__ __forceinline__ void rmw_sub_m(unsigned long long* Es, std::uint32_t e, std::uint32_t mask,
-                                          std::uint32_t nm16) {
+                                          std::uint32_t nm16, const Mul& M) {
     packed_sub(Es + (e >> 26) * SL, entry_lo(e) & mask, entry_r1(e), nm16);
 }
 
@@ -343,7 +345,7 @@ __device__ __forceinline__ std::uint32_t winner_rgb(const unsigned long long (&w
 
 
 // E ring.  The init of column c adds its rows k < w2 at steps c - w2 .. c - 1
-// (row k of column s - k + w2 at step s, lane t on row k = (s - t) mod 32), and
+// (lane t adds row t of column s - t + w2 at step s), and
 // lane 31 reads it last at step c + 31: a column lives 32 + w2 steps.  Slots
 // are cleared kBatch at a time (conflict-free) at the end of every step
 // s = -1 mod kBatch: columns s + 1 + w2 .. s + kBatch + w2, whose previous
@@ -376,11 +378,12 @@ __host__ __device__ inline std::size_t per_warp_bytes() {
 
 struct Loads {
     std::uint32_t a, b, c, d;  // E update: entering / leaving rows of the two columns
-    std::uint32_t i1, i2;      // init: one row of column vi (+) and of column vi - w2 (-)
+    std::uint32_t i1;          // init: row t of column s - t + w2 (its leaving pixel is b)
 };
 
 struct Task {
     Mul M;
+    std::uint32_t imask, im16, inm16;  // per lane: t < w2 ? (~0, 16, -16) : 0 (masked init)
     const std::uint32_t* Sf;  // sheared plane of this frame
     std::uint32_t o0;         // element offset of diagonal D0 (ring column 0), ring row 0
     std::uint32_t Hs;         // elements per diagonal
@@ -423,14 +426,11 @@ __device__ __forceinline__ Loads fetch(const Task& T, int s) {
             L.d = ld_off(T.Sf, ob - T.dD, four);   // old row, leaving column
         }
     }
-    const int k = (s - t) & 31;
-    const int vi = s - k + w2;
-    L.i1 = L.i2 = 0;
-    if (!EDGE || (k < w2 && vi >= 0 && vi < T.NV)) {
-        const std::uint32_t oi = ob - t + k;
-        L.i1 = ld_off(T.Sf, oi + T.dI, four);  // init: column vi, row k
-        if (!EDGE || vi >= w2) L.i2 = ld_off(T.Sf, oi, four);  // column vi - w2, row k
-    }
+    // Init (lanes t < w2): row t of column vi = s - t + w2, i.e. diagonal
+    // s + w2, row t; its leaving pixel (column vi - w2 = v, row t) is b.
+    const int vi = s - t + w2;
+    L.i1 = 0;
+    if (!EDGE || (t < w2 && vi >= 0 && vi < T.NV)) L.i1 = ld_off(T.Sf, ob + T.dI, four);
     return L;
 }
 
@@ -442,7 +442,11 @@ __device__ __forceinline__ void prefetch_l2(const Task& T, int s) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 32));
 }
 
-template <int NB, int SL, bool EDGE>
+// SPARSE: lanes t >= w2 skip the init (a branch; small windows, where the
+// active lanes fit one half-warp and the init accesses take half the
+// shared-memory wavefronts); otherwise all lanes run it masked (no divergence;
+// measured 13% faster for r = 15).
+template <int NB, int SL, bool SPARSE, bool EDGE>
 __device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
                                      unsigned long long (&win)[NB], unsigned long long* E,
                                      std::uint32_t* stage, const std::uint32_t* recip) {
@@ -471,21 +475,22 @@ __device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
             rmw_add<SL>(Es, cur.d, T.M);
         }
     }
-    {  // one row of the from-scratch build of E(vi, band top)
-        const int k = (s - t) & 31;
-        const int vi = s - k + w2;
+    {  // one row of the from-scratch build of E(vi, band top): lane t adds row t
+        const int vi = s - t + w2;
         const int islot = static_cast<unsigned>(vi) % SL;
         if (EDGE) {
-            if (k < w2 && vi >= 0 && vi < T.NV) {
+            if (t < w2 && vi >= 0 && vi < T.NV) {
                 rmw_add<SL>(E + islot, cur.i1, T.M);
-                if (vi >= w2) rmw_sub<SL>(E + islot, cur.i2, T.M);
+                if (vi >= w2) rmw_sub<SL>(E + islot, cur.b, T.M);
+            }
+        } else if (SPARSE) {
+            if (t < w2) {  // (a per-lane constant)
+                rmw_add<SL>(E + islot, cur.i1, T.M);
+                rmw_sub<SL>(E + islot, cur.b, T.M);
             }
         } else {
-            // Branch-free: rows k >= w2 contribute zero (their entries are valid
-            // memory, so the bin index stays in range).
-            const std::uint32_t m = k < w2 ? ~0u : 0u;
-            rmw_add_m<SL>(E + islot, cur.i1, m, m & T.M.m16);
-            rmw_sub_m<SL>(E + islot, cur.i2, m, m & T.M.negm16);
+            rmw_add_m<SL>(E + islot, cur.i1, T.imask, T.im16, T.M);
+            rmw_sub_m<SL>(E + islot, cur.b, T.imask, T.inm16, T.M);
         }
     }
     __syncwarp();
@@ -512,7 +517,7 @@ __device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
     __syncwarp();
 }
 
-template <int NB, int SL>
+template <int NB, int SL, bool SPARSE>
 __global__ void __launch_bounds__(kMaxWarps * 32)
     skew_kernel(BandArgs a, const std::uint32_t* __restrict__ S, ShearGeom sg, int* task_counter,
                 WorkSplit g, Mul M) {
@@ -539,6 +544,9 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
     T.dI = T.w2 * T.Hs;
     T.lane = lane;
     T.stride = static_cast<std::size_t>(a.width) * 3;
+    T.imask = lane < T.w2 ? ~0u : 0u;
+    T.im16 = T.imask & M.m16;
+    T.inm16 = T.imask & M.negm16;
 
     long long u = 0, u_end = 0;  // unprocessed units of the current chunk
     int f, kb, x0, x1;
@@ -581,10 +589,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
                     const int s = 32 * p + ss;
                     if (OPC_SKEW_PF_DIST > 0) prefetch_l2(T, s + OPC_SKEW_PF_DIST);
                     const Loads n2 = fetch<false>(T, s + 2);
-                    step<NB, SL, false>(T, s, cur, win, E, stage, recip);
+                    step<NB, SL, SPARSE, false>(T, s, cur, win, E, stage, recip);
                     if (OPC_SKEW_PF_DIST > 0) prefetch_l2(T, s + OPC_SKEW_PF_DIST + 1);
                     const Loads n3 = fetch<false>(T, s + 3);
-                    step<NB, SL, false>(T, s + 1, n1, win, E, stage, recip);
+                    step<NB, SL, SPARSE, false>(T, s + 1, n1, win, E, stage, recip);
                     cur = n2;
                     n1 = n3;
                 }
@@ -593,7 +601,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
                 for (int ss = 0; ss < 32; ++ss) {
                     const int s = 32 * p + ss;
                     const Loads nxt = fetch<true>(T, s + 1);
-                    step<NB, SL, true>(T, s, cur, win, E, stage, recip);
+                    step<NB, SL, SPARSE, true>(T, s, cur, win, E, stage, recip);
                     cur = nxt;
                 }
             }
@@ -601,7 +609,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
     }
 }
 
-template <int NB, int SL>
+template <int NB, int SL, bool SPARSE>
 cudaError_t launch_nbs(const BandArgs& a, int* counter, void* scratch, int num_sms,
                        cudaStream_t s) {
     const std::size_t pw = per_warp_bytes<NB, SL>();
@@ -609,11 +617,11 @@ cudaError_t launch_nbs(const BandArgs& a, int* counter, void* scratch, int num_s
     int warps = kMaxWarps;
     while (warps > 1 && kRecipBytes + warps * pw > limit) --warps;
     const std::size_t smem = kRecipBytes + warps * pw;
-    cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(skew_kernel<NB, SL>),
+    cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(skew_kernel<NB, SL, SPARSE>),
                                   static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = blocks_per_sm(reinterpret_cast<const void*>(skew_kernel<NB, SL>), warps * 32, smem, &per_sm);
+    e = blocks_per_sm(reinterpret_cast<const void*>(skew_kernel<NB, SL, SPARSE>), warps * 32, smem, &per_sm);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
 
@@ -643,7 +651,7 @@ cudaError_t launch_nbs(const BandArgs& a, int* counter, void* scratch, int num_s
     if (e != cudaSuccess) return e;
     const Mul M{16u, 0xFFFFFFF0u, 4u, 1u};
     timing_mark(kIdSkew, 0, s);
-    skew_kernel<NB, SL><<<static_cast<unsigned>(blocks), warps * 32, smem, s>>>(a, S, sg, counter, g, M);
+    skew_kernel<NB, SL, SPARSE><<<static_cast<unsigned>(blocks), warps * 32, smem, s>>>(a, S, sg, counter, g, M);
     timing_mark(kIdSkew, 1, s);
     return cudaGetLastError();
 }
@@ -654,8 +662,12 @@ cudaError_t launch_nb(const BandArgs& a, int* counter, void* scratch, int num_sm
     // The smaller ring when the window allows it (64 >= 16 + w2 + 32) and it
     // buys occupancy: NB = 31 goes from 8 to 11 warps per SM (config 5: -2.4%);
     // for NB = 21 (11 -> 12 warps) it measured 10% slower on config 2.
-    if (NB >= 24 && 2 * a.radius + 1 <= 16) return launch_nbs<NB, 64>(a, counter, scratch, num_sms, s);
-    return launch_nbs<NB, 96>(a, counter, scratch, num_sms, s);
+    const bool small = 2 * a.radius + 1 <= 16;
+    if constexpr (NB >= 24) {
+        if (small) return launch_nbs<NB, 64, true>(a, counter, scratch, num_sms, s);
+    }
+    if (small) return launch_nbs<NB, 96, true>(a, counter, scratch, num_sms, s);
+    return launch_nbs<NB, 96, false>(a, counter, scratch, num_sms, s);
 }
 
 }  // namespace

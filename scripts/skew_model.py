@@ -64,8 +64,7 @@ def model(img: np.ndarray, r: int, L: int, segw: int | None = None) -> np.ndarra
 
             def fetch(s, t):
                 v = s - t
-                k = (s - t) & 31
-                vi = s - k + w2
+                vi = s - t + w2
                 L_ = {}
                 if 0 <= v < NV:
                     L_["a"] = val((D0 + s + w2) * Hs + R0 + t + w2)
@@ -73,10 +72,10 @@ def model(img: np.ndarray, r: int, L: int, segw: int | None = None) -> np.ndarra
                     if v >= w2:
                         L_["c"] = val((D0 + s) * Hs + R0 + t + w2)
                         L_["d"] = val((D0 + s - w2) * Hs + R0 + t)
-                if k < w2 and 0 <= vi < NV:
-                    L_["i1"] = val((D0 + s + w2) * Hs + R0 + k)
+                if t < w2 and 0 <= vi < NV:
+                    L_["i1"] = val((D0 + s + w2) * Hs + R0 + t)  # column vi, row t
                     if vi >= w2:
-                        L_["i2"] = val((D0 + s) * Hs + R0 + k)
+                        L_["i2"] = val((D0 + s) * Hs + R0 + t)  # column vi - w2, row t (= b)
                 return L_
 
             def add(dct, e, sign):
@@ -112,9 +111,8 @@ def model(img: np.ndarray, r: int, L: int, segw: int | None = None) -> np.ndarra
                             if v >= w2:
                                 add(E[slot], cur[t]["c"], -1)
                                 add(E[slot], cur[t]["d"], +1)
-                        k = (s - t) & 31
-                        vi = s - k + w2
-                        if k < w2 and 0 <= vi < NV:
+                        vi = s - t + w2
+                        if t < w2 and 0 <= vi < NV:
                             slot = vi % SLOTS
                             add(E[slot], cur[t]["i1"], +1)
                             if vi >= w2:
