@@ -86,3 +86,22 @@ def test_generate_device_matches_host(gpu, kind, seed, w, h, offset):
     want = opc.generate(kind, w, h, seed=seed).reshape(-1)
     assert np.array_equal(got[offset:offset + want.size], want)
     assert (got[:offset] == 0xAB).all() and (got[offset + want.size:] == 0xAB).all()
+
+
+def test_kernel_timing_records_each_launch(gpu):
+    """opc_kernel_timing: CUDA events around every kernel launch (bench.py's
+    roofline uses the dominant kernel's measured time)."""
+    from paper_1405_1020_b200 import _lib
+    img = opc.generate(opc.Pattern.NOISE, 700, 300, seed=5)
+    p = opc.FilterParams(7, 20)
+    opc.kernel_timing(True)
+    for _ in range(3):
+        opc.apply_cuda(img, p)
+    skew_ms, skew_n = opc.kernel_timing_read(_lib.OPC_KID_SKEW)
+    pre_ms, pre_n = opc.kernel_timing_read(_lib.OPC_KID_PREPASS)
+    bor_ms, bor_n = opc.kernel_timing_read(_lib.OPC_KID_BORDER)
+    opc.kernel_timing(False)
+    assert (skew_n, pre_n, bor_n) == (3, 3, 3)
+    assert skew_ms > 0 and pre_ms > 0 and bor_ms > 0
+    opc.apply_cuda(img, p)  # timing off: nothing recorded
+    assert opc.kernel_timing_read(_lib.OPC_KID_SKEW) == (0.0, 0)
