@@ -105,3 +105,29 @@ def test_kernel_timing_records_each_launch(gpu):
     assert skew_ms > 0 and pre_ms > 0 and bor_ms > 0
     opc.apply_cuda(img, p)  # timing off: nothing recorded
     assert opc.kernel_timing_read(_lib.OPC_KID_SKEW) == (0.0, 0)
+
+
+@pytest.mark.parametrize("y0,y1", [(0, 40), (37, 151), (150, 203), (0, 203)])
+def test_band_writes_exactly_its_rows(gpu, y0, y1):
+    """Canary (proj/tests/test_parallel.cpp:65-103 lifted to the band call): the
+    band's output rows are all written -- identical results over 0x00- and
+    0xFF-filled buffers -- nothing outside them is, and the rows equal the
+    whole-image result."""
+    import ctypes
+    from paper_1405_1020_b200._lib import LIB
+    img = opc.generate(opc.Pattern.NOISE, 97, 203, seed=8)
+    p = opc.FilterParams(6, 20)
+    whole = opc.apply_cuda(img, p)
+    lo, hi = opc.band_input_rows(203, y0, y1, 6)
+    src = np.ascontiguousarray(img[lo:hi])
+    outs = []
+    for fill in (0x00, 0xFF):
+        buf = np.full((y1 - y0 + 2) * 97 * 3, fill, np.uint8)  # one guard row each side
+        c = opc.CudaConfig().to_c()
+        rc = LIB.opc_filter_rgb8_band(src.ctypes.data, buf.ctypes.data + 97 * 3, 97, 203, y0, y1,
+                                      6, 20, 0, ctypes.byref(c))
+        assert rc == 0, LIB.opc_last_error()
+        assert (buf[:97 * 3] == fill).all() and (buf[-97 * 3:] == fill).all()
+        outs.append(buf[97 * 3:-97 * 3].reshape(y1 - y0, 97, 3))
+    assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(outs[0], whole[y0:y1])
