@@ -352,9 +352,12 @@ __device__ __forceinline__ std::uint32_t winner_rgb(const unsigned long long (&w
 // occupants (c - SL) were last read by step s - 1 when SL >= kBatch + w2 + 32.
 //   r <= 7  (w2 <= 16): 64 slots, batches of 16 (used for NB >= 24: config 5 fits 11 warps/SM)
 //   r <= 15 (w2 <= 31): 96 slots, batches of 32
+#ifndef OPC_SKEW_SL_LARGE
+#define OPC_SKEW_SL_LARGE 96  // ring for w2 > 16; 80 (batches of 16, 12 warps/SM) measured 2.6% slower on C4
+#endif
 template <int SL>
 struct Ring {
-    static constexpr int kBatch = SL == 64 ? 16 : 32;
+    static constexpr int kBatch = (SL == 64 || SL == 80) ? 16 : 32;
     static constexpr int kLanes = 32 / kBatch;  // bins cleared per column per store
 };
 #ifndef OPC_SKEW_PF_DIST
@@ -667,7 +670,7 @@ cudaError_t launch_nb(const BandArgs& a, int* counter, void* scratch, int num_sm
         if (small) return launch_nbs<NB, 64, true>(a, counter, scratch, num_sms, s);
     }
     if (small) return launch_nbs<NB, 96, true>(a, counter, scratch, num_sms, s);
-    return launch_nbs<NB, 96, false>(a, counter, scratch, num_sms, s);
+    return launch_nbs<NB, OPC_SKEW_SL_LARGE, false>(a, counter, scratch, num_sms, s);
 }
 
 }  // namespace
