@@ -578,7 +578,9 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
         const int nphases = ((T.NV - 1) >> 5) + 2;
         // steady: every lane past warm-up and every flushed column valid
         const int p_steady_lo = (T.w2 + 62 + 31) >> 5;
-        Loads cur = fetch<true>(T, -32);
+        // The first init row (column 0, lane 0) is added at step -w2: phase -1
+        // starts there.  (Slots the skipped steps would clear are still zero.)
+        Loads cur = fetch<true>(T, -T.w2);
         for (int p = -1; p < nphases; ++p) {
             // (A partial last band runs the steady path too: its rows past
             // y_rows read valid plane rows and are never flushed.)
@@ -601,7 +603,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
                 }
             } else {
 #pragma unroll 1
-                for (int ss = 0; ss < 32; ++ss) {
+                for (int ss = p < 0 ? 32 - T.w2 : 0; ss < 32; ++ss) {
                     const int s = 32 * p + ss;
                     const Loads nxt = fetch<true>(T, s + 1);
                     step<NB, SL, SPARSE, true>(T, s, cur, win, E, stage, recip);
