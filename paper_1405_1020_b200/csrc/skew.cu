@@ -577,7 +577,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
 
         const int nphases = ((T.NV - 1) >> 5) + 2;
         // steady: every lane past warm-up and every flushed column valid
-        const int p_steady_lo = (T.w2 + 62 + 31) >> 5;
+        // From phase p on every step is steady: all lanes past warm-up
+        // (s - 31 >= w2 from s = 32p) and every flushed column valid
+        // (32p - 32 >= w2): 32p >= w2 + 32.
+        const int p_steady_lo = (T.w2 + 32 + 31) >> 5;
         // The first init row (column 0, lane 0) is added at step -w2: phase -1
         // starts there.  (Slots the skipped steps would clear are still zero.)
         Loads cur = fetch<true>(T, -T.w2);
