@@ -174,47 +174,41 @@ struct Mul {
     std::uint32_t m16, negm16, four, one;  // 16, -16, 4, 1
 };
 
-#ifndef OPC_SKEW_WIDE_BINS
-#define OPC_SKEW_WIDE_BINS 0
-#endif
-
-// w += e entirely on the FMA pipe: IMAD.WIDE.U32 adds the low word with its
-// carry into the 64-bit w, IMAD adds the high word (one = 1 at run time).
-__device__ __forceinline__ void wide_add(unsigned long long& w, unsigned long long e,
-                                         std::uint32_t one) {
-    asm("{\n\t.reg .u32 el, eh, wl, wh;\n\t.reg .u64 t;\n\t"
-        "mov.b64 {el, eh}, %1;\n\tmad.wide.u32 t, el, %2, %0;\n\t"
-        "mov.b64 {wl, wh}, t;\n\tmad.lo.u32 wh, eh, %2, wh;\n\tmov.b64 %0, {wl, wh};\n\t}"
-        : "+l"(w) : "l"(e), "r"(one));
-}
-
 __device__ __forceinline__ std::uint32_t entry_lo(std::uint32_t e) { return e & 0x03FC00FFu; }
 __device__ __forceinline__ std::uint32_t entry_r1(std::uint32_t e) {
     return __byte_perm(e, 0x00040000u, 0x7641);  // R + 2^18; x16 = R << 4 | 1 << 22
 }
 
-// p += (r1 * mul) << 32 | lo   (64-bit, carry from the low word)
-__device__ __forceinline__ void packed_add(unsigned long long* p, std::uint32_t lo, std::uint32_t r1,
-                                           std::uint32_t mul) {
+// w + (r1 * mul) << 32 | lo   (64-bit, carry from the low word)
+__device__ __forceinline__ unsigned long long packed_plus(unsigned long long w, std::uint32_t lo,
+                                                          std::uint32_t r1, std::uint32_t mul) {
     std::uint32_t wl, wh;
-    asm("mov.b64 {%0, %1}, %2;" : "=r"(wl), "=r"(wh) : "l"(*p));
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(wl), "=r"(wh) : "l"(w));
     asm("add.cc.u32 %0, %0, %2;\n\tmadc.lo.u32 %1, %3, %4, %1;"
         : "+r"(wl), "+r"(wh) : "r"(lo), "r"(r1), "r"(mul));
     unsigned long long r;
     asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(wl), "r"(wh));
-    *p = r;
+    return r;
 }
-// p -= (r1 * 16) << 32 | lo
-__device__ __forceinline__ void packed_sub(unsigned long long* p, std::uint32_t lo, std::uint32_t r1,
-                                           std::uint32_t negmul) {
+// w - (r1 * 16) << 32 | lo
+__device__ __forceinline__ unsigned long long packed_minus(unsigned long long w, std::uint32_t lo,
+                                                           std::uint32_t r1, std::uint32_t negmul) {
     std::uint32_t wl, wh;
-    asm("mov.b64 {%0, %1}, %2;" : "=r"(wl), "=r"(wh) : "l"(*p));
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(wl), "=r"(wh) : "l"(w));
     // wl - lo with borrow; hi - 16*r1 - borrow == hi + (-16)*r1 - borrow
     asm("sub.cc.u32 %0, %0, %2;\n\tsubc.u32 %1, %1, 0;\n\tmad.lo.u32 %1, %3, %4, %1;"
         : "+r"(wl), "+r"(wh) : "r"(lo), "r"(r1), "r"(negmul));
     unsigned long long r;
     asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(wl), "r"(wh));
-    *p = r;
+    return r;
+}
+__device__ __forceinline__ void packed_add(unsigned long long* p, std::uint32_t lo, std::uint32_t r1,
+                                           std::uint32_t mul) {
+    *p = packed_plus(*p, lo, r1, mul);
+}
+__device__ __forceinline__ void packed_sub(unsigned long long* p, std::uint32_t lo, std::uint32_t r1,
+                                           std::uint32_t negmul) {
+    *p = packed_minus(*p, lo, r1, negmul);
 }
 
 // E[bin(e)][slot] += / -= packed(e).  Es = E + slot, SL slots per bin row.
@@ -360,6 +354,9 @@ struct Ring {
     static constexpr int kBatch = (SL == 64 || SL == 80) ? 16 : 32;
     static constexpr int kLanes = 32 / kBatch;  // bins cleared per column per store
 };
+#ifndef OPC_SKEW_HOIST_INIT
+#define OPC_SKEW_HOIST_INIT 1
+#endif
 #ifndef OPC_SKEW_PF_DIST
 #define OPC_SKEW_PF_DIST 8  // L2 prefetch distance (steps) of the init diagonal; 0 = off
 #endif
@@ -456,6 +453,21 @@ __device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
     const int t = T.lane;
     const int w2 = T.w2;
     const int v = s - t;
+    // Steady steps: the two init targets (slot of column v + w2, never the E
+    // update's slot) are read before the E update chain and written after it,
+    // so the two read-modify-write chains overlap instead of queueing.
+    const int vi = s - t + w2;
+    const int islot = static_cast<unsigned>(vi) % SL;
+    unsigned long long* ip1 = E + islot + (cur.i1 >> 26) * SL;
+    unsigned long long* ip2 = E + islot + (cur.b >> 26) * SL;
+    unsigned long long iold1 = 0, iold2 = 0;
+    // (Only lanes t < w2 touch them: a lane t >= w2 would address the slot of
+    // column s - t + w2 >= s - 31 + w2, which another lane updates in between.)
+    constexpr bool kHoist = !EDGE && SPARSE && OPC_SKEW_HOIST_INIT;  // (r = 15: 1.8% slower)
+    if (kHoist && t < w2) {
+        iold1 = *ip1;
+        iold2 = *ip2;
+    }
     if (!EDGE || (v >= 0 && v < T.NV)) {
         const int slot = static_cast<unsigned>(v) % SL;
         unsigned long long e[NB];
@@ -465,10 +477,7 @@ __device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
             stage[t * kStageStride + (v & 31)] = winner_rgb<NB>(win, recip, T.M.one);
         }
 #pragma unroll
-        for (int b = 0; b < NB; ++b) {
-            if (!EDGE && b < OPC_SKEW_WIDE_BINS) wide_add(win[b], e[b], T.M.one);
-            else win[b] += e[b];
-        }
+        for (int b = 0; b < NB; ++b) win[b] += e[b];
         // Advance E(v) from row t to row t + 1 (lane t + 1 reads it next step).
         unsigned long long* Es = E + slot;
         rmw_add<SL>(Es, cur.a, T.M);
@@ -479,9 +488,17 @@ __device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
         }
     }
     {  // one row of the from-scratch build of E(vi, band top): lane t adds row t
-        const int vi = s - t + w2;
-        const int islot = static_cast<unsigned>(vi) % SL;
-        if (EDGE) {
+        if (kHoist) {
+            const unsigned long long n1 =
+                packed_plus(iold1, entry_lo(cur.i1), entry_r1(cur.i1), T.M.m16);
+            // (both in one bin: one word, the second update applies to n1)
+            const unsigned long long n2 =
+                packed_minus(ip1 == ip2 ? n1 : iold2, entry_lo(cur.b), entry_r1(cur.b), T.M.negm16);
+            if (t < w2) {
+                *ip1 = n1;
+                *ip2 = n2;
+            }
+        } else if (EDGE) {
             if (t < w2 && vi >= 0 && vi < T.NV) {
                 rmw_add<SL>(E + islot, cur.i1, T.M);
                 if (vi >= w2) rmw_sub<SL>(E + islot, cur.b, T.M);

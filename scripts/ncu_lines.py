@@ -1,7 +1,9 @@
 #!/usr/bin/env python3
 """Per-source-line warp-stall samples of one kernel from an ncu --set full report.
 
-usage: python scripts/ncu_lines.py <report.ncu-rep> <object.o> <kernel-regex> <source.cu> [top]
+usage: python scripts/ncu_lines.py <report.ncu-rep> <object.o> <kernel-regex> <source.cu> [top] [ncu-name-regex]
+(kernel-regex matches the mangled name in the object; ncu-name-regex, default the
+same, the demangled name in the report)
 Maps the report's SASS rows (address order) to source lines with nvdisasm -g on
 the cubin extracted from the object (built from the same source with -lineinfo).
 """
@@ -9,6 +11,7 @@ import collections, csv, os, re, subprocess, sys, tempfile
 
 rep, obj, kre, srcf = sys.argv[1:5]
 top = int(sys.argv[5]) if len(sys.argv) > 5 else 25
+nre = sys.argv[6] if len(sys.argv) > 6 else kre
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(obj)], cwd=tmp, capture_output=True)
 cubin = next(f for f in os.listdir(tmp) if f.endswith(".cubin"))
@@ -23,9 +26,12 @@ for l in sass[start + 1:]:
         cur = int(m.group(1))
     elif re.match(r"\s+/\*[0-9a-f]{4,}\*/\s+\S", l):
         lines.append(cur)
-rows = list(csv.reader(subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{kre}",
+rows = list(csv.reader(subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{nre}",
                                        "--print-source", "sass"], capture_output=True, text=True).stdout.splitlines()))
-hdr, data = rows[1], rows[2:]
+# (one block per captured launch: "Kernel Name" row, header row, instruction rows)
+starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"]
+blk = rows[starts[0]:starts[1]] if len(starts) > 1 else rows[starts[0]:]
+hdr, data = blk[1], [r for r in blk[2:] if len(r) == len(blk[1])]
 iss, iex = hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("Instructions Executed")
 if len(data) != len(lines):
     print(f"warning: {len(data)} report rows vs {len(lines)} disassembled instructions")
