@@ -43,4 +43,5 @@ for k, r in enumerate(data):
 tot, totex = sum(agg.values()) or 1, sum(aex.values()) or 1
 src = open(srcf).read().split("\n")
 for ln, v in agg.most_common(top):
-    print(f"line {ln}: samples {v / tot:6.1%} instr {aex[ln] / totex:6.1%}  {src[ln - 1].strip()[:90] if ln else ''}")
+    text = src[ln - 1].strip()[:90] if ln and ln <= len(src) else "(inlined from another file)"
+    print(f"line {ln}: samples {v / tot:6.1%} instr {aex[ln] / totex:6.1%}  {text}")
