@@ -18,7 +18,7 @@
 //    (filter.cpp:41-43) via the exact reciprocal table.
 // Pixels come from a transposed (column-major) entry plane written by the
 // shared pre-pass, so a ring column (32+2r rows) is one contiguous run that
-// cp.async copies 16 bytes at a time, one 32-column phase ahead.
+// cp.async copies 16 bytes at a time, one phase (kPhase columns) ahead.
 #include "kernels.cuh"
 #include "worksplit.cuh"
 
@@ -26,6 +26,18 @@ namespace opc {
 
 namespace {
 
+#ifndef OPC_SLIDE_TRACE
+#define OPC_SLIDE_TRACE 0
+#endif
+#ifndef OPC_SLIDE_UNROLL_SCAN
+#define OPC_SLIDE_UNROLL_SCAN 16
+#endif
+#ifndef OPC_SLIDE_UNROLL_SUMS
+#define OPC_SLIDE_UNROLL_SUMS 16
+#endif
+#ifndef OPC_SLIDE_STEAL
+#define OPC_SLIDE_STEAL 0  // measured no gain on config 3 once rescans were unrolled
+#endif
 #ifndef OPC_SLIDE_GUIDED_K
 #define OPC_SLIDE_GUIDED_K 0  // > 0: guided claims of remaining / (k x resident warps); measured no gain on C3
 #endif
@@ -40,8 +52,22 @@ namespace {
 #endif
 
 constexpr int kWarps = 8;  // upper bound; the launcher fits as many as 227 KB allows
-constexpr int kRingCols = 96;
-constexpr int kStageStride = 33;
+// Ring of entry columns: the window (2r+1) + the phase being slid + the phase
+// being fetched + the leaving column, a compile-time size so the modulo stays
+// cheap; the smaller rings for small radii fit more warps per SM (config 3,
+// r = 10: 88 columns and 16-column output staging give 6 warps instead of 5).
+#ifndef OPC_SLIDE_PHASE
+#define OPC_SLIDE_PHASE 32  // 16 (64-column ring, 7 warps/SM on C3) measured 25% slower:
+                            // a 16-column lead no longer hides the fetch latency on flat runs
+#endif
+constexpr int kPhase = OPC_SLIDE_PHASE;  // columns fetched / slid per phase
+__host__ __device__ constexpr int ring_cols(int r) {
+    return kPhase == 16 ? 64 : r <= 7 ? 80 : r <= 11 ? 88 : 96;  // >= 2r+1 + 2 kPhase + 1
+}
+constexpr int kUnrollScan = OPC_SLIDE_UNROLL_SCAN;
+constexpr int kUnrollSums = OPC_SLIDE_UNROLL_SUMS;
+constexpr int kStageCols = 16;   // output columns staged per flush
+constexpr int kStageStride = 17;
 constexpr int kRecipBytes = 1024 * 4;
 constexpr int kTRows = 32;
 constexpr int kTCols = 128;
@@ -49,7 +75,7 @@ constexpr int kTCols = 128;
 __host__ __device__ inline int ring_rows(int r) { return (32 + 2 * r + 3) & ~3; }  // 16-B rows
 
 __host__ __device__ inline std::size_t per_warp_bytes(int bins, int r) {
-    const std::size_t ring = static_cast<std::size_t>(kRingCols) * ring_rows(r) * 4;
+    const std::size_t ring = static_cast<std::size_t>(ring_cols(r)) * ring_rows(r) * 4;
     const std::size_t cnt = ((static_cast<std::size_t>(bins) * 32 * 2) + 15) & ~std::size_t(15);
     return ring + cnt + 32 * kStageStride * 4;
 }
@@ -123,15 +149,60 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;"); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;"); }
 
+// ---- work stealing between warps ----
+// The slide kernel's step cost depends on the content (a run of columns where
+// rectangle edges make the window winners change costs several times a flat
+// run), so even chunks of equal width leave some warps running long after the
+// rest are idle (config 3 trace: median pass 131 us, slowest 736 us).  Every
+// warp publishes its current pass in a slot: word = seq:24 | prog:20 | lim:20
+// (columns relative to x_lo: the pass runs up to lim, prog = the start of the
+// phase it is in).  A warp that finds the queue empty takes the upper half of
+// the pass with the most columns left by lowering that pass's lim with a CAS
+// on the whole word -- so the victim's published progress is the one the cut
+// was computed from: the victim is inside the published phase and reads lim at
+// its next phase start, so every column from the next phase on can be taken.
+struct StealSlot {
+    unsigned long long word;
+    int x0, f, kb, pad;
+};
+__device__ __forceinline__ unsigned long long steal_word(unsigned seq, int prog, int lim) {
+    return (static_cast<unsigned long long>(seq & 0xFFFFFFu) << 40) |
+           (static_cast<unsigned long long>(prog & 0xFFFFF) << 20) |
+           static_cast<unsigned long long>(lim & 0xFFFFF);
+}
+__device__ __forceinline__ int word_lim(unsigned long long w) { return static_cast<int>(w & 0xFFFFF); }
+__device__ __forceinline__ int word_prog(unsigned long long w) { return static_cast<int>((w >> 20) & 0xFFFFF); }
+__device__ __forceinline__ unsigned word_seq(unsigned long long w) { return static_cast<unsigned>(w >> 40); }
+#ifndef OPC_SLIDE_MIN_STEAL
+#define OPC_SLIDE_MIN_STEAL 64
+#endif
+constexpr int kMinSteal = OPC_SLIDE_MIN_STEAL;  // columns left for a pass to be worth splitting
+
+#if OPC_SLIDE_TRACE
+// Debug trace of the passes (OPC_SLIDE_TRACE builds only): per pass
+// {smid << 48 | kb << 24 | x0, x1, start ns, end ns}.
+__device__ unsigned long long g_trace[1 << 16][4];
+__device__ int g_trace_n;
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
+template <int kRingCols>
 __global__ void __launch_bounds__(kWarps * 32)
     slide_kernel(BandArgs a, const std::uint32_t* __restrict__ T, TGeom tg, int* task_counter,
-                 WorkSplit g) {
+                 WorkSplit g, StealSlot* board) {
     extern __shared__ __align__(16) unsigned char smem[];
     std::uint32_t* recip = reinterpret_cast<std::uint32_t*>(smem);
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int r = a.radius;
     const int w2 = 2 * r + 1;
+    const int kb_ = 16 - (32 - __clz(w2 * w2));  // key bits below the count (>= 6 for r <= 15)
+    const unsigned inc = 1u << kb_, gmask = inc - 1;
+    const int gsize = 1 << kb_;
     const int bins = a.levels + 1;
     const int RR = ring_rows(r);
     unsigned char* wbase = smem + kRecipBytes + warp * per_warp_bytes(bins, r);
@@ -153,7 +224,103 @@ __global__ void __launch_bounds__(kWarps * 32)
 
     long long u = 0, u_end = 0;
     int f, kb, x0, x1;
-    while (next_pass<(OPC_SLIDE_GUIDED_K > 0)>(g, task_counter, lane, u, u_end, f, kb, x0, x1)) {
+    StealSlot* const mine = board + (blockIdx.x * (blockDim.x >> 5) + warp);
+    const int nslots = gridDim.x * (blockDim.x >> 5);
+    unsigned seq = 0;
+    bool queue = true;
+    int tries = 0;
+    for (;;) {
+        bool have = queue && next_pass<(OPC_SLIDE_GUIDED_K > 0)>(g, task_counter, lane, u, u_end, f,
+                                                                 kb, x0, x1);
+        if (!have) {
+            queue = false;
+            if (!OPC_SLIDE_STEAL) break;
+            // Steal: the published pass with the most columns left.
+            int best_rem = 0, best_i = -1;
+#pragma unroll 4
+            for (int i = lane; i < nslots; i += 32) {  // L2 loads, pipelined (not volatile)
+                const unsigned long long w = __ldcg(&board[i].word);
+                const int rem = word_lim(w) - word_prog(w);
+                if (rem > best_rem) {
+                    best_rem = rem;
+                    best_i = i;
+                }
+            }
+            for (int o = 16; o; o >>= 1) {
+                const int r2 = __shfl_xor_sync(FULL, best_rem, o);
+                const int i2 = __shfl_xor_sync(FULL, best_i, o);
+                if (r2 > best_rem || (r2 == best_rem && i2 > best_i)) {
+                    best_rem = r2;
+                    best_i = i2;
+                }
+            }
+            if (best_rem < kMinSteal) break;
+            int ok = 0;
+            if (lane == 0) {
+                StealSlot* v = board + best_i;
+                const unsigned long long w = *reinterpret_cast<volatile unsigned long long*>(&v->word);
+                __threadfence();
+                const int vx0 = *reinterpret_cast<volatile int*>(&v->x0);
+                const int vf = *reinterpret_cast<volatile int*>(&v->f);
+                const int vkb = *reinterpret_cast<volatile int*>(&v->kb);
+                const int P = word_prog(w), L = word_lim(w);
+                // cut: from the phase after the victim's published one, halve
+                // what is left, 32-aligned relative to the victim's pass start
+                int mid = P + kPhase + ((L - P - kPhase) / 2);
+                mid = vx0 + ((mid - vx0 + kPhase - 1) & ~(kPhase - 1));
+                if (mid < L && mid >= P + kPhase &&
+                    atomicCAS(&v->word, w, steal_word(word_seq(w), P, mid)) == w) {
+                    ok = 1;
+                    f = vf;
+                    kb = vkb;
+                    x0 = mid;
+                    x1 = L;
+                }
+            }
+            ok = __shfl_sync(FULL, ok, 0);
+            if (!ok) {  // lost a race: look again (bounded)
+                if (++tries > 256) break;
+                continue;
+            }
+            f = __shfl_sync(FULL, f, 0);
+            kb = __shfl_sync(FULL, kb, 0);
+            x0 = __shfl_sync(FULL, x0, 0);
+            x1 = __shfl_sync(FULL, x1, 0);
+        }
+        // Publish the pass: first an empty range under a new seq (a thief that
+        // read the old fields then fails its CAS), then the fields, then the range.
+        if (lane == 0) {
+            atomicExch(&mine->word, steal_word(++seq, x0, x0));
+            mine->x0 = x0;
+            mine->f = f;
+            mine->kb = kb;
+            __threadfence();
+            atomicExch(&mine->word, steal_word(++seq, x0, x1));
+        }
+        __syncwarp();
+        int pass_cols = x1 - x0;  // lowered when a thief takes the pass's tail
+#if OPC_SLIDE_TRACE
+        const unsigned long long t_start = gtime();
+        struct TraceGuard {
+            int kb, x0, &cols, lane, stolen;
+            unsigned long long t0;
+            __device__ ~TraceGuard() {
+                if (lane == 0) {
+                    unsigned smid;
+                    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+                    const int i = atomicAdd(&g_trace_n, 1);
+                    if (i < (1 << 16)) {
+                        g_trace[i][0] = (static_cast<unsigned long long>(smid) << 48) |
+                                        (static_cast<unsigned long long>(kb) << 24) | x0;
+                        g_trace[i][1] = static_cast<unsigned long long>(x0 + cols) |
+                                        (static_cast<unsigned long long>(stolen) << 30);
+                        g_trace[i][2] = t0;
+                        g_trace[i][3] = gtime();
+                    }
+                }
+            }
+        } trace_guard{kb, x0, pass_cols, lane, !queue, t_start};
+#endif
         const int yb = a.y_lo + 32 * kb;
         const int xs = a.x_lo + x0;
         const int xe = a.x_lo + x1;
@@ -178,30 +345,45 @@ __global__ void __launch_bounds__(kWarps * 32)
         auto ringp = [&](int c) { return ring + (c % kRingCols) * RR + lane; };
 
         // First window: columns [0, w2) plus phase 0's entering columns.
-        load_chunk(0, w2 + 32);
+        load_chunk(0, w2 + kPhase);
         cp_async_commit();
-        load_chunk(w2 + 32, 32);
+        load_chunk(w2 + kPhase, kPhase);
         cp_async_commit();
         cp_async_wait1();
         __syncwarp();
 
-        for (int b = 0; b < bins; ++b) cnt[b * 32 + lane] = 0;
+        // Counts are kept as keys count << kb_ | (G-1 - b mod G), G = 2^kb_ bins,
+        // so within a group of G bins the largest key is the lowest-index
+        // maximum and a rescan is a plain packed max.
+        for (int b = 0; b < bins; ++b) cnt[b * 32 + lane] = static_cast<std::uint16_t>(gmask - (b & gmask));
         for (int c = 0; c < w2; ++c) {
             const std::uint32_t* col = ringp(c);
             for (int k = 0; k < w2; ++k) {
                 const std::uint32_t bn = bin_of(col[k], bm);
-                cnt[bn * 32 + lane] = static_cast<std::uint16_t>(cnt[bn * 32 + lane] + 1);
+                cnt[bn * 32 + lane] = static_cast<std::uint16_t>(cnt[bn * 32 + lane] + inc);
             }
         }
-        // Full scan for the lowest-index maximum, then the winner's sums.
+        // Full scan for the lowest-index maximum (filter.hpp:71-82), all lanes
+        // together: lanes 2k and 2k+1 read the 32-bit words holding both their
+        // counts of one bin, the even lane the even bins, the odd lane the odd
+        // ones, and swap halves at the end of each group -- half the loads and
+        // one packed max per word.  Groups are combined lowest first, strict >.
         auto rescan = [&](int& best, int& bc) {
+            const std::uint32_t* cw = reinterpret_cast<const std::uint32_t*>(cnt) + (lane >> 1);
+            const unsigned sh = (lane & 1) * 16;
             best = 0;
-            bc = cnt[lane];
-            for (int b = 1; b < bins; ++b) {
-                const int c = cnt[b * 32 + lane];
+            bc = -1;
+            for (int g0 = 0; g0 < bins; g0 += gsize) {
+                const int gend = min(bins, g0 + gsize);
+                std::uint32_t m = 0;
+#pragma unroll kUnrollScan
+                for (int b = g0 + (lane & 1); b < gend; b += 2) m = __vmaxu2(m, cw[b * 16]);
+                const std::uint32_t o = __shfl_xor_sync(FULL, m, 1);
+                const std::uint32_t key = max((m >> sh) & 0xFFFFu, (o >> sh) & 0xFFFFu);
+                const int c = static_cast<int>(key >> kb_);
                 if (c > bc) {
                     bc = c;
-                    best = b;
+                    best = g0 + static_cast<int>(gmask - (key & gmask));
                 }
             }
         };
@@ -210,6 +392,7 @@ __global__ void __launch_bounds__(kWarps * 32)
             sr = sg = sb = 0;
             for (int c = x_rel - r; c <= x_rel + r; ++c) {
                 const std::uint32_t* col = ringp(c + r);
+#pragma unroll kUnrollSums
                 for (int k = 0; k < w2; ++k) {
                     const std::uint32_t e = col[k];
                     if (static_cast<int>(bin_of(e, bm)) == best) {
@@ -225,17 +408,34 @@ __global__ void __launch_bounds__(kWarps * 32)
         std::uint32_t sr, sg, sb;
         window_sums(0, best, sr, sg, sb);
 
-        const int n = xe - xs;
-        for (int p = 0; 32 * p < n; ++p) {
+        int n = xe - xs;
+        for (int p = 0; kPhase * p < n; ++p) {
+            if (OPC_SLIDE_STEAL && p > 0) {  // publish progress, learn a lowered end
+                int lim = 0;
+                if (lane == 0) {
+                    unsigned long long w = *reinterpret_cast<volatile unsigned long long*>(&mine->word);
+                    for (;;) {
+                        const unsigned long long nw = steal_word(word_seq(w), x0 + kPhase * p, word_lim(w));
+                        const unsigned long long prev = atomicCAS(&mine->word, w, nw);
+                        if (prev == w) break;
+                        w = prev;
+                    }
+                    lim = word_lim(w);
+                }
+                lim = __shfl_sync(FULL, lim, 0);
+                n = min(n, lim - x0);
+                pass_cols = n;
+                if (kPhase * p >= n) break;
+            }
             if (p > 0) {
                 // Phase p's entering columns were requested a phase ago; request p+1's.
-                load_chunk(w2 + 32 * (p + 1), 32);
+                load_chunk(w2 + kPhase * (p + 1), kPhase);
                 cp_async_commit();
                 cp_async_wait1();
                 __syncwarp();
             }
-            const int xend = min(n, 32 * p + 32);
-            for (int x = 32 * p; x < xend; ++x) {
+            const int xend = min(n, kPhase * p + kPhase);
+            for (int x = kPhase * p; x < xend; ++x) {
                 if (x > 0) {
                     // Slide: add ring column x + 2r (image x + r), remove x - 1 (image x - r - 1).
                     const std::uint32_t* cin = ringp(x + 2 * r);
@@ -256,9 +456,10 @@ __global__ void __launch_bounds__(kWarps * 32)
                             if (ei == eo) continue;
                             const int bi = bin_of(ei, bm), bo = bin_of(eo, bm);
                             if (bi != bo) {
-                                const int ci = cnt[bi * 32 + lane] + 1;
-                                cnt[bi * 32 + lane] = static_cast<std::uint16_t>(ci);
-                                cnt[bo * 32 + lane] = static_cast<std::uint16_t>(cnt[bo * 32 + lane] - 1);
+                                const unsigned ki = cnt[bi * 32 + lane] + inc;
+                                cnt[bi * 32 + lane] = static_cast<std::uint16_t>(ki);
+                                cnt[bo * 32 + lane] = static_cast<std::uint16_t>(cnt[bo * 32 + lane] - inc);
+                                const int ci = static_cast<int>(ki >> kb_);
                                 if (bo == best0) lost = true;
                                 if (ci > cand_c || (ci == cand_c && bi < cand_b)) {
                                     cand_b = bi;
@@ -278,23 +479,30 @@ __global__ void __launch_bounds__(kWarps * 32)
                             }
                         }
                         // Resolve the winner (filter.hpp:71-82).
-                        const int bcf = cnt[best0 * 32 + lane];
-                        bool changed = false;
+                        const int bcf = cnt[best0 * 32 + lane] >> kb_;
+                        bool changed = false, need = false;
                         if (lost && bcf < bc) {
-                            rescan(best, bc);
-                            changed = best != best0;
+                            need = true;
                         } else {
                             bc = bcf;
                             if (cand) {
-                                const int cf = cnt[cand_b * 32 + lane];
+                                const int cf = cnt[cand_b * 32 + lane] >> kb_;
                                 if (cf < cand_c) {
-                                    rescan(best, bc);
-                                    changed = best != best0;
+                                    need = true;
                                 } else if (cf > bc || (cf == bc && cand_b < best)) {
                                     best = cand_b;
                                     bc = cf;
                                     changed = true;
                                 }
+                            }
+                        }
+                        if (__any_sync(FULL, need)) {
+                            int nb, nc;
+                            rescan(nb, nc);
+                            if (need) {
+                                best = nb;
+                                bc = nc;
+                                changed = best != best0;
                             }
                         }
                         if (changed) window_sums(x, best, sr, sg, sb);
@@ -304,19 +512,21 @@ __global__ void __launch_bounds__(kWarps * 32)
                     const std::uint32_t m = recip[bc];
                     const std::uint32_t rgb = __umulhi(sr << 1, m) | (__umulhi(sg << 1, m) << 8) |
                                               (__umulhi(sb << 1, m) << 16);
-                    stage[lane * kStageStride + (x & 31)] = rgb;
+                    stage[lane * kStageStride + (x & (kStageCols - 1))] = rgb;
                 }
-                if ((x & 31) == 31 || x == n - 1) {  // flush the 32-column block
+                if ((x & (kStageCols - 1)) == kStageCols - 1 || x == n - 1) {  // flush the block
                     __syncwarp();
-                    const int xb = x & ~31;
+                    const int xb = x & ~(kStageCols - 1);
                     const int cols = x - xb + 1;
-                    for (int fr = 0; fr < 32; ++fr) {
-                        if (yb + fr >= a.y_hi) break;
-                        if (lane < cols) {
-                            const std::uint32_t rgb = stage[fr * kStageStride + lane];
+                    const int c = lane & (kStageCols - 1);
+                    for (int f0 = 0; f0 < 32; f0 += 32 / kStageCols) {  // 2 rows per store
+                        const int fr = f0 + lane / kStageCols;
+                        if (yb + f0 >= a.y_hi) break;
+                        if (c < cols && yb + fr < a.y_hi) {
+                            const std::uint32_t rgb = stage[fr * kStageStride + c];
                             std::uint8_t* o = out +
                                               static_cast<std::size_t>(yb + fr - a.out_row0) * stride +
-                                              static_cast<std::size_t>(xs + xb + lane) * 3;
+                                              static_cast<std::size_t>(xs + xb + c) * 3;
                             o[0] = static_cast<std::uint8_t>(rgb);
                             o[1] = static_cast<std::uint8_t>(rgb >> 8);
                             o[2] = static_cast<std::uint8_t>(rgb >> 16);
@@ -339,9 +549,12 @@ bool slide_supported(int levels, int radius) {
            kRecipBytes + per_warp_bytes(levels + 1, radius) <= 227 * 1024;
 }
 
+constexpr int kMaxBoardSlots = 148 * 8 * 4;  // resident warps of up to 4 x 148 x 8
+
 std::size_t slide_scratch_bytes(const BandArgs& a) {
     if (a.y_hi <= a.y_lo || a.x_hi <= a.x_lo) return 0;
-    return tgeom(a).frame_elems * a.frames * sizeof(std::uint32_t);
+    return tgeom(a).frame_elems * a.frames * sizeof(std::uint32_t) +
+           kMaxBoardSlots * sizeof(StealSlot);
 }
 
 cudaError_t launch_slide(const BandArgs& a, int* counter, void* scratch, int num_sms,
@@ -353,10 +566,15 @@ cudaError_t launch_slide(const BandArgs& a, int* counter, void* scratch, int num
     int warps = kWarps;
     while (warps > 1 && kRecipBytes + warps * pw > limit) --warps;
     const std::size_t smem = kRecipBytes + warps * pw;
-    cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(slide_kernel), static_cast<int>(smem));
+    const int rc = ring_cols(a.radius);
+    const void* kfn = rc == 64   ? reinterpret_cast<const void*>(slide_kernel<64>)
+                      : rc == 80 ? reinterpret_cast<const void*>(slide_kernel<80>)
+                      : rc == 88 ? reinterpret_cast<const void*>(slide_kernel<88>)
+                                 : reinterpret_cast<const void*>(slide_kernel<96>);
+    cudaError_t e = set_smem_attr(kfn, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = blocks_per_sm(reinterpret_cast<const void*>(slide_kernel), warps * 32, smem, &per_sm);
+    e = blocks_per_sm(kfn, warps * 32, smem, &per_sm);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
 
@@ -380,12 +598,40 @@ cudaError_t launch_slide(const BandArgs& a, int* counter, void* scratch, int num
     long long blocks = (g.nchunks + warps - 1) / warps;
     if (blocks > static_cast<long long>(num_sms) * per_sm) blocks = num_sms * per_sm;
     if (blocks < 1) blocks = 1;
+    StealSlot* board = reinterpret_cast<StealSlot*>(
+        static_cast<unsigned char*>(scratch) + tg.frame_elems * a.frames * sizeof(std::uint32_t));
+    if (blocks * warps > kMaxBoardSlots) return cudaErrorInvalidConfiguration;
+    e = cudaMemsetAsync(board, 0, static_cast<std::size_t>(blocks) * warps * sizeof(StealSlot), s);
+    if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(counter, 0, 4 * sizeof(int), s);
     if (e != cudaSuccess) return e;
     timing_mark(kIdSlide, 0, s);
-    slide_kernel<<<static_cast<unsigned>(blocks), warps * 32, smem, s>>>(a, T, tg, counter, g);
+    const dim3 grid(static_cast<unsigned>(blocks)), block(warps * 32);
+    if (rc == 64) {
+        slide_kernel<64><<<grid, block, smem, s>>>(a, T, tg, counter, g, board);
+    } else if (rc == 80) {
+        slide_kernel<80><<<grid, block, smem, s>>>(a, T, tg, counter, g, board);
+    } else if (rc == 88) {
+        slide_kernel<88><<<grid, block, smem, s>>>(a, T, tg, counter, g, board);
+    } else {
+        slide_kernel<96><<<grid, block, smem, s>>>(a, T, tg, counter, g, board);
+    }
     timing_mark(kIdSlide, 1, s);
     return cudaGetLastError();
 }
 
 }  // namespace opc
+
+#if OPC_SLIDE_TRACE
+extern "C" int opc_debug_slide_trace(unsigned long long* out, int max) {
+    int n = 0;
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(&n, opc::g_trace_n, sizeof(int));
+    n = n < max ? n : max;
+    if (n > (1 << 16)) n = 1 << 16;
+    cudaMemcpyFromSymbol(out, opc::g_trace, static_cast<std::size_t>(n) * 32);
+    const int zero = 0;
+    cudaMemcpyToSymbol(opc::g_trace_n, &zero, sizeof(int));
+    return n;
+}
+#endif
