@@ -423,8 +423,8 @@ def main() -> None:
         "kernel_ms": round(kernel_ms, 4),
         "kernel_launches": kernel_n,
         "step_share": {"kernel": round(kernel_total_ms / step_total_ms, 4),
-                       "pre_pass": round(pre_ms / step_total_ms, 4),
-                       "border": round(border_ms / step_total_ms, 4)},
+                       "pre_pass_and_border": round(pre_ms / step_total_ms, 4),
+                       "border_alone": round(border_ms / step_total_ms, 4)},
         "frac_of_step": round(ops_px * interior * args.steps / (step_total_ms / 1e3) / peak_ops, 4),
         "hbm": {"achieved_gbs": round(alg_bytes * args.steps / (step_total_ms / 1e3) / 1e9, 1),
                 "peak_gbs": hbm_gbs,

@@ -353,9 +353,12 @@ int plan(int levels, int radius, int forced, long long interior_px) {
 }
 
 // Runs the filter on device buffers already holding the band input.
-int run_device(const opc::BandArgs& a, int border, int kernel, DevCtx* ctx, cudaStream_t s) {
+int run_device(const opc::BandArgs& band, int border, int kernel, DevCtx* ctx, cudaStream_t s) {
     // (a frame too large for the skew family's 32-bit plane offsets takes the direct family)
     cudaError_t e = cudaSuccess;
+    opc::BandArgs a = band;
+    a.border = opc::make_border_job(a, border);
+    const bool interior = a.y_hi > a.y_lo && a.x_hi > a.x_lo;
     if (kernel == OPC_KERNEL_SKEW && !opc::skew_fits(a)) kernel = OPC_KERNEL_DIRECT;
     if (kernel == OPC_KERNEL_SKEW) {
         // Rotate over 16 task counters (16 bytes each: chunk index + 64-bit
@@ -375,12 +378,18 @@ int run_device(const opc::BandArgs& a, int border, int kernel, DevCtx* ctx, cuda
         e = opc::launch_direct(a, s);
         if (e != cudaSuccess) return cuda_error(e, "direct kernel launch");
     }
-    if (a.y_hi > a.y_lo && a.x_hi > a.x_lo) {
-        g_launches.fetch_add(kernel == OPC_KERNEL_DIRECT ? 1 : 2);  // + the pre-pass
+    // The border job rides on the first kernel of the family (direct tile,
+    // shear or transpose pre-pass); a band without interior launches it alone,
+    // and so does the generic direct kernel.
+    if (interior) {
+        const bool own_border = kernel == OPC_KERNEL_DIRECT && !opc::direct_fuses_border(a);
+        g_launches.fetch_add((kernel == OPC_KERNEL_DIRECT ? 1 : 2) +
+                             (own_border && a.border.nblocks > 0 ? 1 : 0));
+    } else {
+        e = opc::launch_border(a, s);
+        if (e != cudaSuccess) return cuda_error(e, "border kernel launch");
+        if (a.border.nblocks > 0) g_launches.fetch_add(1);
     }
-    e = opc::launch_border(a, border, s);
-    if (e != cudaSuccess) return cuda_error(e, "border kernel launch");
-    if (a.radius > 0) g_launches.fetch_add(1);
     return OPC_OK;
 }
 

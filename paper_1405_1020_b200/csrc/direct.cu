@@ -12,6 +12,7 @@
 // (r > 15, or L+1 > 32 at r > 15) and the kernel the tests force to cross-check
 // the fast families.
 #include "kernels.cuh"
+#include "border.cuh"
 
 namespace opc {
 
@@ -88,6 +89,12 @@ __global__ void __launch_bounds__(kTileW * kTileH)
     direct_tile_kernel(BandArgs a) {
     __shared__ std::uint32_t tile[(kTileH + 2 * kTileMaxR) * (kTileW + 2 * kTileMaxR)];
     extern __shared__ std::uint32_t counts[];  // [bins][256]
+    const int main_rows = (a.y_hi - a.y_lo + kTileH - 1) / kTileH;
+    if (static_cast<int>(blockIdx.y) >= main_rows) {  // appended border blocks
+        const int b = (blockIdx.y - main_rows) * gridDim.x + blockIdx.x;
+        if (b < a.border.nblocks) border_block(a, b, blockIdx.z, threadIdx.y * kTileW + threadIdx.x);
+        return;
+    }
     const int r = a.radius;
     const int tw = kTileW + 2 * r, th = kTileH + 2 * r;
     const int x0 = a.x_lo + blockIdx.x * kTileW;  // first output column of the tile
@@ -141,38 +148,9 @@ __global__ void __launch_bounds__(kTileW * kTileH)
     o[2] = static_cast<std::uint8_t>(sb / best_count);
 }
 
-// Border pixels of the output band (filter.cpp:54 / parallel.cpp:113):
-// CopyInput copies the input bytes, ZeroFill writes zeros.  The flat byte
-// index space is [full border rows][left+right strips of interior rows].
-__global__ void border_kernel(BandArgs a, int policy, long long full_bytes, long long strip_bytes,
-                              int top_rows, int first_full_top, int first_full_bottom) {
-    const long long per_frame = full_bytes + strip_bytes;
-    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int frame = blockIdx.y;
-    if (i >= per_frame) return;
-    const long long row_bytes = static_cast<long long>(a.width) * 3;
-    int y;
-    long long col_byte;
-    if (i < full_bytes) {
-        const long long row = i / row_bytes;
-        col_byte = i % row_bytes;
-        y = row < top_rows ? first_full_top + static_cast<int>(row)
-                           : first_full_bottom + static_cast<int>(row - top_rows);
-    } else {
-        const long long j = i - full_bytes;
-        const long long side = static_cast<long long>(a.radius) * 3;
-        const long long per_row = 2 * side;
-        y = a.y_lo + static_cast<int>(j / per_row);
-        const long long k = j % per_row;
-        col_byte = k < side ? k : row_bytes - per_row + k;
-    }
-    std::uint8_t v = 0;
-    if (policy == 0) {
-        v = a.in[a.in_frame_stride * frame + static_cast<std::size_t>(y - a.in_row0) * row_bytes +
-                 col_byte];
-    }
-    a.out[a.out_frame_stride * frame + static_cast<std::size_t>(y - a.out_row0) * row_bytes +
-          col_byte] = v;
+// Standalone border launch: all blocks on the border job.
+__global__ void __launch_bounds__(kBorderThreads) border_kernel(BandArgs a) {
+    border_block(a, blockIdx.x, blockIdx.y, threadIdx.x);
 }
 
 }  // namespace
@@ -195,14 +173,19 @@ std::uint32_t bin_multiplier(int levels) {
     return 0;
 }
 
+bool direct_fuses_border(const BandArgs& a) {
+    return a.radius <= kTileMaxR && a.levels + 1 <= kTileMaxBins && a.levels <= 255;
+}
+
 cudaError_t launch_direct(const BandArgs& a, cudaStream_t s) {
     if (a.y_hi <= a.y_lo || a.x_hi <= a.x_lo || a.frames <= 0) return cudaSuccess;
-    if (a.radius <= kTileMaxR && a.levels + 1 <= kTileMaxBins && a.levels <= 255) {
+    if (direct_fuses_border(a)) {
         const std::size_t smem = static_cast<std::size_t>(a.levels + 1) * kTileW * kTileH * 4;
         cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(direct_tile_kernel), static_cast<int>(smem));
         if (e != cudaSuccess) return e;
-        const dim3 grid(static_cast<unsigned>((a.x_hi - a.x_lo + kTileW - 1) / kTileW),
-                        static_cast<unsigned>((a.y_hi - a.y_lo + kTileH - 1) / kTileH),
+        const unsigned gx = static_cast<unsigned>((a.x_hi - a.x_lo + kTileW - 1) / kTileW);
+        const dim3 grid(gx, static_cast<unsigned>((a.y_hi - a.y_lo + kTileH - 1) / kTileH) +
+                                border_grid_rows(a, gx),
                         static_cast<unsigned>(a.frames));
         timing_mark(kIdDirect, 0, s);
         direct_tile_kernel<<<grid, dim3(kTileW, kTileH), smem, s>>>(a);
@@ -219,28 +202,36 @@ cudaError_t launch_direct(const BandArgs& a, cudaStream_t s) {
     timing_mark(kIdDirect, 0, s);
     direct_kernel<<<grid, kDirectThreads, smem, s>>>(a, pixels);
     timing_mark(kIdDirect, 1, s);
-    return cudaGetLastError();
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return launch_border(a, s);  // 64-thread blocks: the border job runs on its own
 }
 
-cudaError_t launch_border(const BandArgs& a, int policy, cudaStream_t s) {
+BorderJob make_border_job(const BandArgs& a, int policy) {
+    BorderJob j{};
+    j.policy = policy;
     // Full border rows inside this band's output rows.
     const int out_lo = a.y_begin, out_hi = a.y_end;
-    const int top_lo = out_lo, top_hi = out_hi < a.radius ? out_hi : a.radius;
-    const int top_rows = top_hi > top_lo ? top_hi - top_lo : 0;
-    const int bot_lo = out_lo > a.height - a.radius ? out_lo : a.height - a.radius;
-    const int bot_rows = out_hi > bot_lo ? out_hi - bot_lo : 0;
-    const long long row_bytes = static_cast<long long>(a.width) * 3;
-    const long long full_bytes = static_cast<long long>(top_rows + bot_rows) * row_bytes;
-    const int mid_rows = a.y_hi > a.y_lo ? a.y_hi - a.y_lo : 0;
-    const long long strip_bytes = static_cast<long long>(mid_rows) * 2 * a.radius * 3;
-    const long long per_frame = full_bytes + strip_bytes;
-    if (per_frame <= 0 || a.frames <= 0) return cudaSuccess;
-    const int threads = 256;
-    const dim3 grid(static_cast<unsigned>((per_frame + threads - 1) / threads),
-                    static_cast<unsigned>(a.frames));
+    j.top_lo = out_lo;
+    const int top_hi = out_hi < a.radius ? out_hi : a.radius;
+    j.top_rows = top_hi > j.top_lo ? top_hi - j.top_lo : 0;
+    j.bot_lo = out_lo > a.height - a.radius ? out_lo : a.height - a.radius;
+    j.bot_rows = out_hi > j.bot_lo ? out_hi - j.bot_lo : 0;
+    const long long full_bytes = static_cast<long long>(j.top_rows + j.bot_rows) * a.width * 3;
+    const int mid_rows = a.y_hi > a.y_lo && a.radius > 0 ? a.y_hi - a.y_lo : 0;
+    if (full_bytes <= 0 && mid_rows <= 0) return j;
+    long long nfull = (full_bytes + 16 * kBorderThreads - 1) / (16 * kBorderThreads);
+    if (nfull > 1184) nfull = 1184;
+    j.nfull = static_cast<int>(nfull);
+    j.nblocks = j.nfull + (mid_rows + kBorderThreads / 32 - 1) / (kBorderThreads / 32);
+    return j;
+}
+
+cudaError_t launch_border(const BandArgs& a, cudaStream_t s) {
+    if (a.border.nblocks <= 0 || a.frames <= 0) return cudaSuccess;
+    const dim3 grid(static_cast<unsigned>(a.border.nblocks), static_cast<unsigned>(a.frames));
     timing_mark(kIdBorder, 0, s);
-    border_kernel<<<grid, threads, 0, s>>>(a, policy, full_bytes, strip_bytes, top_rows, top_lo,
-                                           bot_lo);
+    border_kernel<<<grid, kBorderThreads, 0, s>>>(a);
     timing_mark(kIdBorder, 1, s);
     return cudaGetLastError();
 }

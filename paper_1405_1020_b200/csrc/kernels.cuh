@@ -63,6 +63,18 @@ inline void timing_mark(int id, int phase, cudaStream_t s) {
 // [y_lo, y_hi) (= [y_begin, y_end) clipped to [r, H-r)) and columns
 // [x_lo, x_hi) are computed by the filter kernels; the border pixels of rows
 // [y_begin, y_end) are written by the border kernel.
+// The border pixels of a launch's output rows, written by extra blocks of the
+// launch's first kernel (pre-pass or direct), or by border_kernel when the
+// band has no interior.  Blocks [0, nfull) copy the full border rows, the
+// rest one interior row's left and right r-pixel strips per warp.
+struct BorderJob {
+    int policy;  // 0 CopyInput, 1 ZeroFill
+    int top_lo, top_rows, bot_lo, bot_rows;
+    int nfull;    // blocks on the full rows
+    int nblocks;  // nfull + strip blocks; 0 = nothing to write
+};
+constexpr int kBorderThreads = 256;
+
 struct BandArgs {
     const std::uint8_t* in;
     std::uint8_t* out;
@@ -80,6 +92,7 @@ struct BandArgs {
     int radius;
     int levels;
     std::uint32_t bin_mul;  // bin = umulhi(r+g+b, bin_mul) == (r+g+b)*L/765
+    BorderJob border;       // fused into the first kernel of the launch
 };
 
 // Exact magic multiplier for floor(s * L / 765), s in [0, 765], L in [1, 256];
@@ -88,7 +101,10 @@ std::uint32_t bin_multiplier(int levels);
 
 // ---- kernel families (each returns cudaError_t of the launch) ----
 cudaError_t launch_direct(const BandArgs& a, cudaStream_t s);
-cudaError_t launch_border(const BandArgs& a, int border_policy, cudaStream_t s);
+bool direct_fuses_border(const BandArgs& a);  // tile kernel: border blocks appended
+BorderJob make_border_job(const BandArgs& a, int border_policy);
+// Standalone border launch (a band without interior rows): a.border's blocks.
+cudaError_t launch_border(const BandArgs& a, cudaStream_t s);
 
 // Skew family: L + 1 <= 32, radius <= 15.  `task_counter` is a device int
 // (zeroed by the launcher on the stream).

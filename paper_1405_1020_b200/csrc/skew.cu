@@ -35,6 +35,7 @@
 //  * Output: a 32x32 staging tile; each step one row completes a 32-pixel
 //    block, written as one coalesced 96-byte run.
 #include "kernels.cuh"
+#include "border.cuh"
 #include "worksplit.cuh"
 
 namespace opc {
@@ -96,6 +97,11 @@ __device__ __forceinline__ std::uint32_t entry_from_brg(std::uint32_t t, std::ui
 __global__ void __launch_bounds__(256)
     shear_kernel(BandArgs a, std::uint32_t* S, ShearGeom g, int vec_ok) {
     __shared__ __align__(16) std::uint32_t tile[kShearRows * kShearStride];
+    if (static_cast<int>(blockIdx.y) >= g.Hs / kShearRows) {  // appended border blocks
+        const int b = (blockIdx.y - g.Hs / kShearRows) * gridDim.x + blockIdx.x;
+        if (b < a.border.nblocks) border_block(a, b, blockIdx.z, threadIdx.x);
+        return;
+    }
     const int x0 = blockIdx.x * kShearCols;
     const int y0 = g.y_base + blockIdx.y * kShearRows;
     const int frame = blockIdx.z;
@@ -672,8 +678,9 @@ cudaError_t launch_nbs(const BandArgs& a, int* counter, void* scratch, int num_s
     const ShearGeom sg = shear_geom(a);
     std::uint32_t* S = static_cast<std::uint32_t*>(scratch);
     {
-        const dim3 grid(static_cast<unsigned>((a.width + kShearPad + kShearCols - 1) / kShearCols),
-                        static_cast<unsigned>(sg.Hs / kShearRows), static_cast<unsigned>(a.frames));
+        const unsigned gx = static_cast<unsigned>((a.width + kShearPad + kShearCols - 1) / kShearCols);
+        const dim3 grid(gx, static_cast<unsigned>(sg.Hs / kShearRows) + border_grid_rows(a, gx),
+                        static_cast<unsigned>(a.frames));
         const int vec_ok = (reinterpret_cast<std::uintptr_t>(a.in) % 4 == 0) &&
                            ((static_cast<std::size_t>(a.width) * 3) % 4 == 0) &&
                            (a.in_frame_stride % 4 == 0);

@@ -20,6 +20,7 @@
 // shared pre-pass, so a ring column (32+2r rows) is one contiguous run that
 // cp.async copies 16 bytes at a time, one phase (kPhase columns) ahead.
 #include "kernels.cuh"
+#include "border.cuh"
 #include "worksplit.cuh"
 
 namespace opc {
@@ -100,6 +101,11 @@ __host__ inline TGeom tgeom(const BandArgs& a) {
 // column's 32 rows are one 128-byte store.
 __global__ void __launch_bounds__(256) transpose_kernel(BandArgs a, std::uint32_t* T, TGeom g) {
     __shared__ std::uint32_t tile[kTRows * (kTCols + 1)];
+    if (static_cast<int>(blockIdx.y) >= g.Hs / kTRows) {  // appended border blocks
+        const int b = (blockIdx.y - g.Hs / kTRows) * gridDim.x + blockIdx.x;
+        if (b < a.border.nblocks) border_block(a, b, blockIdx.z, threadIdx.x);
+        return;
+    }
     const int x0 = blockIdx.x * kTCols;
     const int y0 = g.y_base + blockIdx.y * kTRows;
     const int frame = blockIdx.z;
@@ -581,8 +587,9 @@ cudaError_t launch_slide(const BandArgs& a, int* counter, void* scratch, int num
     const TGeom tg = tgeom(a);
     std::uint32_t* T = static_cast<std::uint32_t*>(scratch);
     {
-        const dim3 grid(static_cast<unsigned>((a.width + 64 + kTCols - 1) / kTCols),
-                        static_cast<unsigned>(tg.Hs / kTRows), static_cast<unsigned>(a.frames));
+        const unsigned gx = static_cast<unsigned>((a.width + 64 + kTCols - 1) / kTCols);
+        const dim3 grid(gx, static_cast<unsigned>(tg.Hs / kTRows) + border_grid_rows(a, gx),
+                        static_cast<unsigned>(a.frames));
         timing_mark(kIdPrePass, 0, s);
         transpose_kernel<<<grid, 256, 0, s>>>(a, T, tg);
         timing_mark(kIdPrePass, 1, s);

@@ -27,6 +27,7 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--kernel", type=int, default=0)
     ap.add_argument("--frames", type=int, default=0, help="limit frames of a batch config")
+    ap.add_argument("--kt", action="store_true", help="also print per-kernel times (event hook)")
     args = ap.parse_args()
     cfg = opc.CONFIGS[args.config]
     frames = cfg.frames if args.frames <= 0 else min(cfg.frames, args.frames)
@@ -39,6 +40,8 @@ def main() -> None:
     c = opc.CudaConfig(device=0, stream=s.cuda_stream, kernel=args.kernel,
                        allow_levels_256=cfg.levels == 256)
     p = opc.FilterParams(cfg.radius, cfg.levels)
+    if args.kt:
+        opc.kernel_timing(True)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with torch.cuda.stream(s):
         ev[0].record(s)
@@ -47,6 +50,13 @@ def main() -> None:
                                   p, c, frames=frames)
             ev[i + 1].record(s)
     s.synchronize()
+    if args.kt:
+        from paper_1405_1020_b200 import _lib
+        for name in ("DIRECT", "SKEW", "SLIDE", "PREPASS", "BORDER"):
+            t, n = opc.kernel_timing_read(getattr(_lib, "OPC_KID_" + name))
+            if n:
+                print(f"  {name.lower()}: {t / n * 1e3:.1f} us x {n}")
+        opc.kernel_timing(False)
     ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
     mp = frames * cfg.width * cfg.height / 1e6
     print(f"{args.config} kernel={args.kernel} frames={frames} ms/step={ms} "

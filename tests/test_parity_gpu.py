@@ -260,4 +260,30 @@ def test_device_pointer_path_with_torch_stream(gpu):
 def test_launch_counter_advances(gpu):
     before = gpu.kernel_launches()
     run(gpu, np.zeros((40, 40, 3), np.uint8), 3, 20)
-    assert gpu.kernel_launches() >= before + 2  # filter kernel + border kernel
+    assert gpu.kernel_launches() >= before + 1  # direct tile kernel (border blocks fused)
+
+
+@pytest.mark.parametrize("kernel", [AUTO, DIRECT, SKEW, SLIDE])
+@pytest.mark.parametrize("r", [3, 6])
+@pytest.mark.parametrize("in_off,out_off", [(0, 0), (1, 3), (5, 2), (16, 7)])
+def test_device_pointers_at_unaligned_offsets(gpu, kernel, r, in_off, out_off):
+    """The fused border job copies 16 bytes per store: unaligned and mutually
+    misaligned device pointers take its head / byte-assembling paths.  Bytes
+    around the output stay untouched."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(in_off * 31 + out_off)
+    w, h, L = 203, 77, 20
+    img = rng.integers(0, 256, (h, w, 3), dtype=np.uint8)
+    n = img.size
+    for b in (0, 1):
+        want = oracle_lib.oracle_filter(img, r, L, b)
+        dev_in = torch.zeros(n + 64, dtype=torch.uint8, device="cuda")
+        dev_in[in_off:in_off + n] = torch.from_numpy(img.reshape(-1)).cuda()
+        dev_out = torch.full((n + 64,), 0xCD, dtype=torch.uint8, device="cuda")
+        cfg = gpu.CudaConfig(device=0, kernel=kernel)
+        gpu.apply_cuda_device(dev_in.data_ptr() + in_off, dev_out.data_ptr() + out_off, w, h,
+                              gpu.FilterParams(r, L, gpu.BorderPolicy(b)), cfg)
+        torch.cuda.synchronize()
+        got = dev_out.cpu().numpy()
+        assert np.array_equal(got[out_off:out_off + n].reshape(h, w, 3), want), (b, kernel)
+        assert (got[:out_off] == 0xCD).all() and (got[out_off + n:] == 0xCD).all()
