@@ -16,7 +16,7 @@ LIB_PATH = Path(os.environ.get("OILPAINT_B200_LIB",
 OPC_OK, OPC_EINVAL, OPC_ECUDA, OPC_ENOMEM = 0, 1, 2, 3
 OPC_FLAG_DEVICE_POINTERS = 0x1
 OPC_FLAG_ALLOW_LEVELS_256 = 0x2
-OPC_KERNEL_AUTO, OPC_KERNEL_DIRECT, OPC_KERNEL_SKEW, OPC_KERNEL_SLIDE = 0, 1, 2, 3
+OPC_KERNEL_AUTO, OPC_KERNEL_DIRECT, OPC_KERNEL_SKEW, OPC_KERNEL_SLIDE, OPC_KERNEL_COLUMN = 0, 1, 2, 3, 4
 
 # Every symbol include/oilpaint_b200.h and include/oilpaint_b200_patterns.h declare.
 EXPORTS = (
@@ -28,7 +28,7 @@ EXPORTS = (
 )
 
 
-OPC_KID_DIRECT, OPC_KID_SKEW, OPC_KID_SLIDE, OPC_KID_PREPASS, OPC_KID_BORDER = 1, 2, 3, 4, 5
+OPC_KID_DIRECT, OPC_KID_SKEW, OPC_KID_SLIDE, OPC_KID_PREPASS, OPC_KID_BORDER, OPC_KID_COLUMN = 1, 2, 3, 4, 5, 6
 
 
 class opc_config(ctypes.Structure):

@@ -341,6 +341,9 @@ int ensure(void** p, std::size_t* cap, std::size_t need) {
 int plan(int levels, int radius, int forced, long long interior_px) {
     if (forced == OPC_KERNEL_DIRECT) return OPC_KERNEL_DIRECT;
     if (forced == OPC_KERNEL_SKEW) return opc::skew_supported(levels, radius) ? OPC_KERNEL_SKEW : -1;
+    if (forced == OPC_KERNEL_COLUMN) {
+        return opc::column_supported(levels, radius) ? OPC_KERNEL_COLUMN : -1;
+    }
     if (forced == OPC_KERNEL_SLIDE) {
         return opc::slide_supported(levels, radius) ? OPC_KERNEL_SLIDE : -1;
     }
@@ -374,6 +377,9 @@ int run_device(const opc::BandArgs& band, int border, int kernel, DevCtx* ctx, c
         if (rc != OPC_OK) return rc;
         e = opc::launch_slide(a, counter, ctx->d_scratch, ctx->num_sms, s);
         if (e != cudaSuccess) return cuda_error(e, "slide kernel launch");
+    } else if (kernel == OPC_KERNEL_COLUMN) {
+        e = opc::launch_column(a, ctx->num_sms, s);
+        if (e != cudaSuccess) return cuda_error(e, "column kernel launch");
     } else {
         e = opc::launch_direct(a, s);
         if (e != cudaSuccess) return cuda_error(e, "direct kernel launch");
@@ -383,7 +389,7 @@ int run_device(const opc::BandArgs& band, int border, int kernel, DevCtx* ctx, c
     // and so does the generic direct kernel.
     if (interior) {
         const bool own_border = kernel == OPC_KERNEL_DIRECT && !opc::direct_fuses_border(a);
-        g_launches.fetch_add((kernel == OPC_KERNEL_DIRECT ? 1 : 2) +
+        g_launches.fetch_add((kernel == OPC_KERNEL_DIRECT || kernel == OPC_KERNEL_COLUMN ? 1 : 2) +
                              (own_border && a.border.nblocks > 0 ? 1 : 0));
     } else {
         e = opc::launch_border(a, s);
