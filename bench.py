@@ -352,8 +352,9 @@ def main() -> None:
     barrier()
     launches = opc.kernel_launches() - launches0
     step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
-    family = opc.plan_kernel(W, H, r, L)  # kernel ids 1-3 = OPC_KERNEL_DIRECT/SKEW/SLIDE
-    kernel_total_ms, kernel_n = opc.kernel_timing_read(family)
+    family = opc.plan_kernel(W, H, r, L)  # OPC_KERNEL_DIRECT/SKEW/SLIDE/COLUMN = 1-4
+    kid = {4: _lib.OPC_KID_COLUMN}.get(family, family)  # timing ids: 1-3 as the families, 6 column
+    kernel_total_ms, kernel_n = opc.kernel_timing_read(kid)
     pre_ms, _ = opc.kernel_timing_read(_lib.OPC_KID_PREPASS)
     border_ms, _ = opc.kernel_timing_read(_lib.OPC_KID_BORDER)
     opc.kernel_timing(False)
@@ -419,7 +420,7 @@ def main() -> None:
         "model": f"colhist {ops_px} lane-ops per interior pixel (SURVEY 8d, B={L + 1}); "
                  f"{num_sms} SMs x 4 x 32 x {sm_mhz:.0f} MHz ({peaks_kind} sm_max_mhz)",
         "algorithmic_ops_per_launch": ops_px * interior * args.steps // max(1, kernel_n),
-        "kernel": {1: "direct", 2: "skew", 3: "slide"}.get(family, str(family)),
+        "kernel": {1: "direct", 2: "skew", 3: "slide", 4: "column"}.get(family, str(family)),
         "kernel_ms": round(kernel_ms, 4),
         "kernel_launches": kernel_n,
         "step_share": {"kernel": round(kernel_total_ms / step_total_ms, 4),

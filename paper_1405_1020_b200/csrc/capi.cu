@@ -347,6 +347,15 @@ int plan(int levels, int radius, int forced, long long interior_px) {
     if (forced == OPC_KERNEL_SLIDE) {
         return opc::slide_supported(levels, radius) ? OPC_KERNEL_SLIDE : -1;
     }
+    // Small images: the column family, while its per-pixel cost (~ 2r+1
+    // updates per pixel) stays below the skew family's fill-bound launch
+    // (scripts/size_sweep.py on one B200, noise, L = 20: column wins up to
+    // interior * (2r+1) ~ 50M, e.g. 1920x1080 r <= 7, 2560x1600 r <= 5,
+    // 4096^2 r <= 2; the skew family beyond).
+    if (forced == OPC_KERNEL_AUTO && opc::column_supported(levels, radius) &&
+        interior_px * (2 * radius + 1) <= 50ll * 1000 * 1000) {
+        return OPC_KERNEL_COLUMN;
+    }
     if (forced == OPC_KERNEL_AUTO && radius <= 3 && interior_px <= (4ll << 20)) {
         return OPC_KERNEL_DIRECT;
     }

@@ -94,17 +94,21 @@ def test_kernel_timing_records_each_launch(gpu):
     from paper_1405_1020_b200 import _lib
     img = opc.generate(opc.Pattern.NOISE, 700, 300, seed=5)
     p = opc.FilterParams(7, 20)
+    skew = opc.CudaConfig(kernel=_lib.OPC_KERNEL_SKEW)
     opc.kernel_timing(True)
     for _ in range(3):
-        opc.apply_cuda(img, p)
+        opc.apply_cuda(img, p, skew)
+    opc.apply_cuda(img, p)  # automatic choice for this size: the column family
     skew_ms, skew_n = opc.kernel_timing_read(_lib.OPC_KID_SKEW)
     pre_ms, pre_n = opc.kernel_timing_read(_lib.OPC_KID_PREPASS)
     bor_ms, bor_n = opc.kernel_timing_read(_lib.OPC_KID_BORDER)
+    col_ms, col_n = opc.kernel_timing_read(_lib.OPC_KID_COLUMN)
     opc.kernel_timing(False)
-    # the border job rides on the shear pre-pass: no border launch of its own
-    assert (skew_n, pre_n, bor_n) == (3, 3, 0)
-    assert skew_ms > 0 and pre_ms > 0 and bor_ms == 0
-    opc.apply_cuda(img, p)  # timing off: nothing recorded
+    # the border job rides on the shear pre-pass / the column kernel: no
+    # border launch of its own
+    assert (skew_n, pre_n, bor_n, col_n) == (3, 3, 0, 1)
+    assert skew_ms > 0 and pre_ms > 0 and bor_ms == 0 and col_ms > 0
+    opc.apply_cuda(img, p, skew)  # timing off: nothing recorded
     assert opc.kernel_timing_read(_lib.OPC_KID_SKEW) == (0.0, 0)
 
 
