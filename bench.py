@@ -282,9 +282,18 @@ def main() -> None:
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # One process per GPU over NCCL.  OPC_BENCH_BACKEND=gloo with more ranks
+    # than GPUs is a plumbing check only (ranks share devices; not a number
+    # to report): the rank -> device map wraps around.
+    backend = os.environ.get("OPC_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     W, H, F = cfg.width, cfg.height, cfg.frames
     r, L = cfg.radius, cfg.levels
@@ -359,7 +368,8 @@ def main() -> None:
     border_ms, _ = opc.kernel_timing_read(_lib.OPC_KID_BORDER)
     opc.kernel_timing(False)
     total_ms = ev[0].elapsed_time(ev[args.steps])
-    t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{local}")
+    red_dev = f"cuda:{local}" if backend == "nccl" else "cpu"
+    t = torch.tensor([total_ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
@@ -389,7 +399,7 @@ def main() -> None:
     for _ in range(args.e2e_steps):
         step_e2e()
     e2e_s = time.perf_counter() - t0
-    te = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = job_pixels * args.e2e_steps / float(te.item()) / 1e6
