@@ -77,16 +77,18 @@ __host__ inline ShearGeom shear_geom(const BandArgs& a) {
 // layout is chosen so that the packed 64-bit contribution (count 1, R, G, B)
 // costs two ALU ops: lo = e & 0x03FC00FF (B | G << 18) and the byte permute
 // R + 2^18, whose x16 is the hi word R << 4 | 1 << 22.
+// With `key` (r <= 7, the KEY layout below) the entry is B | R << 8 | G << 16 |
+// bin << 24 instead.
 __device__ __forceinline__ std::uint32_t make_entry(std::uint32_t r, std::uint32_t g,
-                                                    std::uint32_t b, std::uint32_t bin_mul) {
+                                                    std::uint32_t b, std::uint32_t bin_mul, int key) {
     const std::uint32_t bin = __umulhi(r + g + b, bin_mul);  // filter.hpp:31-35
-    return b | (r << 8) | (g << 18) | (bin << 26);
+    return key ? b | (r << 8) | (g << 16) | (bin << 24) : b | (r << 8) | (g << 18) | (bin << 26);
 }
 
 // Entry from t = B | R << 8 | G << 16 (byte 3 ignored).
-__device__ __forceinline__ std::uint32_t entry_from_brg(std::uint32_t t, std::uint32_t bin_mul) {
+__device__ __forceinline__ std::uint32_t entry_from_brg(std::uint32_t t, std::uint32_t bin_mul, int key) {
     const std::uint32_t bin = __umulhi(__dp4a(t, 0x00010101u, 0u), bin_mul);
-    return (t & 0xFFFFu) | ((t & 0x00FF0000u) << 2) | (bin << 26);
+    return key ? (t & 0xFFFFFFu) | (bin << 24) : (t & 0xFFFFu) | ((t & 0x00FF0000u) << 2) | (bin << 26);
 }
 
 // Sheared entry plane.  Block: 32 rows x 128 columns staged through shared
@@ -95,7 +97,7 @@ __device__ __forceinline__ std::uint32_t entry_from_brg(std::uint32_t t, std::ui
 // global memory and splits them with byte permutes; row stride 132 words keeps
 // both the 16-byte tile stores and the diagonal reads conflict-free.
 __global__ void __launch_bounds__(256)
-    shear_kernel(BandArgs a, std::uint32_t* S, ShearGeom g, int vec_ok) {
+    shear_kernel(BandArgs a, std::uint32_t* S, ShearGeom g, int vec_ok, int key) {
     __shared__ __align__(16) std::uint32_t tile[kShearRows * kShearStride];
     if (static_cast<int>(blockIdx.y) >= g.Hs / kShearRows) {  // appended border blocks
         const int b = (blockIdx.y - g.Hs / kShearRows) * gridDim.x + blockIdx.x;
@@ -124,10 +126,10 @@ __global__ void __launch_bounds__(256)
         for (int k = 0; k < kShearRows / 8; ++k) {
             // bytes R0 G0 B0 R1 | G1 B1 R2 G2 | B2 R3 G3 B3
             uint4 e;
-            e.x = entry_from_brg(__byte_perm(w[k][0], w[k][1], 0x0102), a.bin_mul);
-            e.y = entry_from_brg(__byte_perm(w[k][0], w[k][1], 0x0435), a.bin_mul);
-            e.z = entry_from_brg(__byte_perm(w[k][1], w[k][2], 0x0324), a.bin_mul);
-            e.w = entry_from_brg(__byte_perm(w[k][2], w[k][2], 0x0213), a.bin_mul);
+            e.x = entry_from_brg(__byte_perm(w[k][0], w[k][1], 0x0102), a.bin_mul, key);
+            e.y = entry_from_brg(__byte_perm(w[k][0], w[k][1], 0x0435), a.bin_mul, key);
+            e.z = entry_from_brg(__byte_perm(w[k][1], w[k][2], 0x0324), a.bin_mul, key);
+            e.w = entry_from_brg(__byte_perm(w[k][2], w[k][2], 0x0213), a.bin_mul, key);
             *reinterpret_cast<uint4*>(&tile[(warp + 8 * k) * kShearStride + 4 * lane]) = e;
         }
     } else {
@@ -143,7 +145,7 @@ __global__ void __launch_bounds__(256)
                 if (x < a.width && y < in_hi) {
                     const std::uint8_t* p = in + static_cast<std::size_t>(y - a.in_row0) * stride +
                                             static_cast<std::size_t>(x) * 3;
-                    e = make_entry(p[0], p[1], p[2], a.bin_mul);
+                    e = make_entry(p[0], p[1], p[2], a.bin_mul, key);
                 }
                 tile[row * kShearStride + c] = e;
             }
@@ -180,10 +182,23 @@ struct Mul {
     std::uint32_t m16, negm16, four, one;  // 16, -16, 4, 1
 };
 
-__device__ __forceinline__ std::uint32_t entry_lo(std::uint32_t e) { return e & 0x03FC00FFu; }
-__device__ __forceinline__ std::uint32_t entry_r1(std::uint32_t e) {
-    return __byte_perm(e, 0x00040000u, 0x7641);  // R + 2^18; x16 = R << 4 | 1 << 22
+// Packed histogram words.  Default layout (any r <= 15):
+//   hi = count << 22 | sumR << 4 | sumG >> 14      lo = sumG << 18 | sumB
+// KEY layout (r <= 7: count <= 225, sums < 2^16), the multiplier M.m16 = 1:
+//   hi = count << 24 | (31 - bin) << 16 | sumR      lo = sumG << 16 | sumB
+// where the window words start at (31 - bin) << 48 (E words carry no key), so
+// the largest hi word is the largest count at the lowest bin.
+template <bool KEY = false>
+__device__ __forceinline__ std::uint32_t entry_lo(std::uint32_t e) {
+    return KEY ? __byte_perm(e, 0u, 0x4240) : e & 0x03FC00FFu;  // KEY: B | G << 16
 }
+template <bool KEY = false>
+__device__ __forceinline__ std::uint32_t entry_r1(std::uint32_t e) {
+    // default: R + 2^18 (x16 = R << 4 | 1 << 22); KEY: R | 1 << 24 (x1)
+    return KEY ? __byte_perm(e, 0x01000000u, 0x7541) : __byte_perm(e, 0x00040000u, 0x7641);
+}
+template <bool KEY = false>
+__device__ __forceinline__ std::uint32_t entry_bin(std::uint32_t e) { return KEY ? e >> 24 : e >> 26; }
 
 // w + (r1 * mul) << 32 | lo   (64-bit, carry from the low word)
 __device__ __forceinline__ unsigned long long packed_plus(unsigned long long w, std::uint32_t lo,
@@ -218,26 +233,26 @@ __device__ __forceinline__ void packed_sub(unsigned long long* p, std::uint32_t 
 }
 
 // E[bin(e)][slot] += / -= packed(e).  Es = E + slot, SL slots per bin row.
-template <int SL>
+template <int SL, bool KEY = false>
 __device__ __forceinline__ void rmw_add(unsigned long long* Es, std::uint32_t e, const Mul& M) {
-    packed_add(Es + (e >> 26) * SL, entry_lo(e), entry_r1(e), M.m16);
+    packed_add(Es + entry_bin<KEY>(e) * SL, entry_lo<KEY>(e), entry_r1<KEY>(e), M.m16);
 }
-template <int SL>
+template <int SL, bool KEY = false>
 __device__ __forceinline__ void rmw_sub(unsigned long long* Es, std::uint32_t e, const Mul& M) {
-    packed_sub(Es + (e >> 26) * SL, entry_lo(e), entry_r1(e), M.negm16);
+    packed_sub(Es + entry_bin<KEY>(e) * SL, entry_lo<KEY>(e), entry_r1<KEY>(e), M.negm16);
 }
 
 // Masked forms (all lanes execute; lanes with mask 0 add zero): lo & mask,
 // multiplier m16 = 16 & mask or nm16 = -16 & mask.
-template <int SL>
+template <int SL, bool KEY = false>
 __device__ __forceinline__ void rmw_add_m(unsigned long long* Es, std::uint32_t e, std::uint32_t mask,
                                           std::uint32_t m16, const Mul& M) {
-    packed_add(Es + (e >> 26) * SL, entry_lo(e) & mask, entry_r1(e), m16);
+    packed_add(Es + entry_bin<KEY>(e) * SL, entry_lo<KEY>(e) & mask, entry_r1<KEY>(e), m16);
 }
-template <int SL>
+template <int SL, bool KEY = false>
 __device__ __forceinline__ void rmw_sub_m(unsigned long long* Es, std::uint32_t e, std::uint32_t mask,
                                           std::uint32_t nm16, const Mul& M) {
-    packed_sub(Es + (e >> 26) * SL, entry_lo(e) & mask, entry_r1(e), nm16);
+    packed_sub(Es + entry_bin<KEY>(e) * SL, entry_lo<KEY>(e) & mask, entry_r1<KEY>(e), nm16);
 }
 
 // Lowest-index bin with the largest count (filter.hpp:71-82) and its truncated
@@ -263,6 +278,41 @@ __device__ __forceinline__ void pick_if_ge(std::uint32_t& lo, std::uint32_t& hi,
         "@p mad.lo.u32 %0, %2, %5, 0;\n\t@p mad.lo.u32 %1, %3, %5, 0;\n\t}"
         : "+r"(lo), "+r"(hi)
         : "r"(bl), "r"(bh), "r"(T), "r"(one));
+}
+
+// KEY layout: the largest hi word (a max tree) is the winner's hi word; its
+// (31 - bin) field selects the lo word through a 5-level multiplexer.
+template <int NB>
+__device__ __forceinline__ std::uint32_t winner_rgb_key(const unsigned long long (&w)[NB],
+                                                        const std::uint32_t* recip) {
+    std::uint32_t mx[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) mx[b] = static_cast<std::uint32_t>(w[b] >> 32);
+#pragma unroll
+    for (int step = 1; step < NB; step *= 3) {
+#pragma unroll
+        for (int i = 0; i + step < NB; i += 3 * step) {
+            mx[i] = max(mx[i], mx[i + step]);
+            if (i + 2 * step < NB) mx[i] = max(mx[i], mx[i + 2 * step]);
+        }
+    }
+    const std::uint32_t hi = mx[0];
+    const std::uint32_t best = 31u - ((hi >> 16) & 31u);
+    std::uint32_t v[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) v[b] = static_cast<std::uint32_t>(w[b]);
+#pragma unroll
+    for (int k = 0; (1 << k) < NB; ++k) {
+        const bool bit = (best >> k) & 1u;
+#pragma unroll
+        for (int i = 0; i + (1 << k) < NB; i += 2 << k) v[i] = bit ? v[i + (1 << k)] : v[i];
+    }
+    const std::uint32_t lo = v[0];
+    const std::uint32_t m = recip[hi >> 24];
+    const std::uint32_t qr = __umulhi((hi & 0xFFFFu) << 1, m);
+    const std::uint32_t qg = __umulhi((lo >> 16) << 1, m);
+    const std::uint32_t qb = __umulhi((lo & 0xFFFFu) << 1, m);
+    return qr | (qg << 8) | (qb << 16);
 }
 
 template <int NB>
@@ -375,6 +425,9 @@ struct Ring {
 #ifndef OPC_SKEW_MIN_CHUNK
 #define OPC_SKEW_MIN_CHUNK 128
 #endif
+#ifndef OPC_SKEW_KEY
+#define OPC_SKEW_KEY 1  // KEY histogram layout for r <= 7 (the SPARSE launches)
+#endif
 #ifndef OPC_SKEW_MAX_WARPS
 #define OPC_SKEW_MAX_WARPS 12
 #endif
@@ -459,6 +512,7 @@ template <int NB, int SL, bool SPARSE, bool EDGE>
 __device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
                                      unsigned long long (&win)[NB], unsigned long long* E,
                                      std::uint32_t* stage, const std::uint32_t* recip) {
+    constexpr bool KEY = SPARSE && OPC_SKEW_KEY;
     const int t = T.lane;
     const int w2 = T.w2;
     const int v = s - t;
@@ -467,8 +521,8 @@ __device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
     // so the two read-modify-write chains overlap instead of queueing.
     const int vi = s - t + w2;
     const int islot = static_cast<unsigned>(vi) % SL;
-    unsigned long long* ip1 = E + islot + (cur.i1 >> 26) * SL;
-    unsigned long long* ip2 = E + islot + (cur.b >> 26) * SL;
+    unsigned long long* ip1 = E + islot + entry_bin<KEY>(cur.i1) * SL;
+    unsigned long long* ip2 = E + islot + entry_bin<KEY>(cur.b) * SL;
     unsigned long long iold1 = 0, iold2 = 0;
     // (Only lanes t < w2 touch them: a lane t >= w2 would address the slot of
     // column s - t + w2 >= s - 31 + w2, which another lane updates in between.)
@@ -483,43 +537,44 @@ __device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
 #pragma unroll
         for (int b = 0; b < NB; ++b) e[b] = E[b * SL + slot];
         if (!EDGE || (v >= w2 && t < T.y_rows)) {
-            stage[t * kStageStride + (v & 31)] = winner_rgb<NB>(win, recip, T.M.one);
+            stage[t * kStageStride + (v & 31)] =
+                KEY ? winner_rgb_key<NB>(win, recip) : winner_rgb<NB>(win, recip, T.M.one);
         }
 #pragma unroll
         for (int b = 0; b < NB; ++b) win[b] += e[b];
         // Advance E(v) from row t to row t + 1 (lane t + 1 reads it next step).
         unsigned long long* Es = E + slot;
-        rmw_add<SL>(Es, cur.a, T.M);
-        rmw_sub<SL>(Es, cur.b, T.M);
+        rmw_add<SL, KEY>(Es, cur.a, T.M);
+        rmw_sub<SL, KEY>(Es, cur.b, T.M);
         if (!EDGE || v >= w2) {
-            rmw_sub<SL>(Es, cur.c, T.M);
-            rmw_add<SL>(Es, cur.d, T.M);
+            rmw_sub<SL, KEY>(Es, cur.c, T.M);
+            rmw_add<SL, KEY>(Es, cur.d, T.M);
         }
     }
     {  // one row of the from-scratch build of E(vi, band top): lane t adds row t
         if (kHoist) {
             const unsigned long long n1 =
-                packed_plus(iold1, entry_lo(cur.i1), entry_r1(cur.i1), T.M.m16);
+                packed_plus(iold1, entry_lo<KEY>(cur.i1), entry_r1<KEY>(cur.i1), T.M.m16);
             // (both in one bin: one word, the second update applies to n1)
             const unsigned long long n2 =
-                packed_minus(ip1 == ip2 ? n1 : iold2, entry_lo(cur.b), entry_r1(cur.b), T.M.negm16);
+                packed_minus(ip1 == ip2 ? n1 : iold2, entry_lo<KEY>(cur.b), entry_r1<KEY>(cur.b), T.M.negm16);
             if (t < w2) {
                 *ip1 = n1;
                 *ip2 = n2;
             }
         } else if (EDGE) {
             if (t < w2 && vi >= 0 && vi < T.NV) {
-                rmw_add<SL>(E + islot, cur.i1, T.M);
-                if (vi >= w2) rmw_sub<SL>(E + islot, cur.b, T.M);
+                rmw_add<SL, KEY>(E + islot, cur.i1, T.M);
+                if (vi >= w2) rmw_sub<SL, KEY>(E + islot, cur.b, T.M);
             }
         } else if (SPARSE) {
             if (t < w2) {  // (a per-lane constant)
-                rmw_add<SL>(E + islot, cur.i1, T.M);
-                rmw_sub<SL>(E + islot, cur.b, T.M);
+                rmw_add<SL, KEY>(E + islot, cur.i1, T.M);
+                rmw_sub<SL, KEY>(E + islot, cur.b, T.M);
             }
         } else {
-            rmw_add_m<SL>(E + islot, cur.i1, T.imask, T.im16, T.M);
-            rmw_sub_m<SL>(E + islot, cur.b, T.imask, T.inm16, T.M);
+            rmw_add_m<SL, KEY>(E + islot, cur.i1, T.imask, T.im16, T.M);
+            rmw_sub_m<SL, KEY>(E + islot, cur.b, T.imask, T.inm16, T.M);
         }
     }
     __syncwarp();
@@ -597,7 +652,9 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
 
         unsigned long long win[NB];
 #pragma unroll
-        for (int b = 0; b < NB; ++b) win[b] = 0ull;
+        for (int b = 0; b < NB; ++b) {
+            win[b] = (SPARSE && OPC_SKEW_KEY) ? static_cast<unsigned long long>(31 - b) << 48 : 0ull;
+        }
         for (int i = lane; i < NB * SL; i += 32) E[i] = 0ull;
         __syncwarp();
 
@@ -685,7 +742,7 @@ cudaError_t launch_nbs(const BandArgs& a, int* counter, void* scratch, int num_s
                            ((static_cast<std::size_t>(a.width) * 3) % 4 == 0) &&
                            (a.in_frame_stride % 4 == 0);
         timing_mark(kIdPrePass, 0, s);
-        shear_kernel<<<grid, 256, 0, s>>>(a, S, sg, vec_ok);
+        shear_kernel<<<grid, 256, 0, s>>>(a, S, sg, vec_ok, (SPARSE && OPC_SKEW_KEY) ? 1 : 0);
         timing_mark(kIdPrePass, 1, s);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -700,7 +757,7 @@ cudaError_t launch_nbs(const BandArgs& a, int* counter, void* scratch, int num_s
 
     e = cudaMemsetAsync(counter, 0, 4 * sizeof(int), s);
     if (e != cudaSuccess) return e;
-    const Mul M{16u, 0xFFFFFFF0u, 4u, 1u};
+    const Mul M = (SPARSE && OPC_SKEW_KEY) ? Mul{1u, 0xFFFFFFFFu, 4u, 1u} : Mul{16u, 0xFFFFFFF0u, 4u, 1u};
     timing_mark(kIdSkew, 0, s);
     skew_kernel<NB, SL, SPARSE><<<static_cast<unsigned>(blocks), warps * 32, smem, s>>>(a, S, sg, counter, g, M);
     timing_mark(kIdSkew, 1, s);
