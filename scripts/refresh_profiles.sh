@@ -8,6 +8,8 @@ cp gpurun_out/launches.csv profiles/r01_c4_bench_launches.csv
 cp gpurun_out/timing.log profiles/r01_configs_timing.log
 for k in skew shear; do python scripts/ncu_summary.py gpurun_out/prof_c4.ncu-rep profiles/r01_c4_${k}_ncu $k > /dev/null; done
 for k in slide transpose; do python scripts/ncu_summary.py gpurun_out/prof_c3.ncu-rep profiles/r01_c3_${k}_ncu $k > /dev/null; done
+python scripts/ncu_summary.py gpurun_out/prof_c5.ncu-rep profiles/r01_c5_skew_ncu skew > /dev/null
+python scripts/ncu_summary.py gpurun_out/prof_c2.ncu-rep profiles/r01_c2_column_ncu column > /dev/null
 python - <<'PY'
 import json
 d = json.load(open('profiles/r01_c4_skew_ncu.json'))
