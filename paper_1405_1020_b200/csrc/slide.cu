@@ -23,6 +23,10 @@
 #include "border.cuh"
 #include "worksplit.cuh"
 
+#ifndef OPC_SLIDE_COOP_SUMS
+#define OPC_SLIDE_COOP_SUMS 1
+#endif
+
 namespace opc {
 
 namespace {
@@ -511,7 +515,38 @@ __global__ void __launch_bounds__(kWarps * 32)
                                 changed = best != best0;
                             }
                         }
+#if OPC_SLIDE_COOP_SUMS
+                        // Winner changed: the new winner's window sums, one lane's
+                        // window at a time with lane c < 2r+1 summing its column c
+                        // (2r+1 loads per lane instead of (2r+1)^2 on one lane
+                        // while the others wait).
+                        for (unsigned todo = __ballot_sync(FULL, changed); todo; todo &= todo - 1) {
+                            const int j = __ffs(todo) - 1;
+                            const int bj = __shfl_sync(FULL, best, j);
+                            std::uint32_t cr = 0, cg = 0, cbb = 0;
+                            if (lane < w2) {
+                                const std::uint32_t* col = ring + ((x + lane) % kRingCols) * RR + j;
+                                for (int k = 0; k < w2; ++k) {
+                                    const std::uint32_t e = col[k];
+                                    if (static_cast<int>(bin_of(e, bm)) == bj) {
+                                        cr += e & 0xFFu;
+                                        cg += (e >> 8) & 0xFFu;
+                                        cbb += (e >> 16) & 0xFFu;
+                                    }
+                                }
+                            }
+                            cr = __reduce_add_sync(FULL, cr);
+                            cg = __reduce_add_sync(FULL, cg);
+                            cbb = __reduce_add_sync(FULL, cbb);
+                            if (lane == j) {
+                                sr = cr;
+                                sg = cg;
+                                sb = cbb;
+                            }
+                        }
+#else
                         if (changed) window_sums(x, best, sr, sg, sb);
+#endif
                     }
                 }
                 if (row_ok) {
