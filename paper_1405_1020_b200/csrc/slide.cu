@@ -365,12 +365,33 @@ __global__ void __launch_bounds__(kWarps * 32)
         // Counts are kept as keys count << kb_ | (G-1 - b mod G), G = 2^kb_ bins,
         // so within a group of G bins the largest key is the lowest-index
         // maximum and a rescan is a plain packed max.
-        for (int b = 0; b < bins; ++b) cnt[b * 32 + lane] = static_cast<std::uint16_t>(gmask - (b & gmask));
-        for (int c = 0; c < w2; ++c) {
-            const std::uint32_t* col = ringp(c);
-            for (int k = 0; k < w2; ++k) {
-                const std::uint32_t bn = bin_of(col[k], bm);
-                cnt[bn * 32 + lane] = static_cast<std::uint16_t>(cnt[bn * 32 + lane] + inc);
+        // (16-byte stores: one bin row is 64 bytes, 4 lanes per row)
+        for (int q = lane; q < bins * 4; q += 32) {
+            const std::uint32_t v = gmask - ((q >> 2) & gmask);
+            const std::uint32_t v2 = v | (v << 16);
+            reinterpret_cast<uint4*>(cnt)[q] = make_uint4(v2, v2, v2, v2);
+        }
+        __syncwarp();
+        // Fast path: the first windows of all lanes lie in ring columns
+        // [0, 2r] x rows [0, 32 + 2r); when that block is one colour (flat
+        // content, config 3) every lane's window is (2r+1)^2 copies of it.
+        const std::uint32_t e0 = ring[0];
+        bool uni = true;
+        for (int i = lane; i < w2 * (32 + 2 * r); i += 32) {
+            const int c = i / (32 + 2 * r), k = i - c * (32 + 2 * r);
+            uni &= ring[c * RR + k] == e0;  // ring columns 0..2r: no wrap
+        }
+        const bool flat0 = __all_sync(FULL, uni);
+        if (flat0) {
+            const int b0 = static_cast<int>(bin_of(e0, bm));
+            cnt[b0 * 32 + lane] = static_cast<std::uint16_t>(cnt[b0 * 32 + lane] + w2 * w2 * inc);
+        } else {
+            for (int c = 0; c < w2; ++c) {
+                const std::uint32_t* col = ringp(c);
+                for (int k = 0; k < w2; ++k) {
+                    const std::uint32_t bn = bin_of(col[k], bm);
+                    cnt[bn * 32 + lane] = static_cast<std::uint16_t>(cnt[bn * 32 + lane] + inc);
+                }
             }
         }
         // Full scan for the lowest-index maximum (filter.hpp:71-82), all lanes
@@ -414,9 +435,18 @@ __global__ void __launch_bounds__(kWarps * 32)
             }
         };
         int best, bc;
-        rescan(best, bc);
         std::uint32_t sr, sg, sb;
-        window_sums(0, best, sr, sg, sb);
+        if (flat0) {
+            const std::uint32_t n0 = static_cast<std::uint32_t>(w2 * w2);
+            best = static_cast<int>(bin_of(e0, bm));
+            bc = w2 * w2;
+            sr = n0 * (e0 & 0xFFu);
+            sg = n0 * ((e0 >> 8) & 0xFFu);
+            sb = n0 * ((e0 >> 16) & 0xFFu);
+        } else {
+            rescan(best, bc);
+            window_sums(0, best, sr, sg, sb);
+        }
 
         int n = xe - xs;
         for (int p = 0; kPhase * p < n; ++p) {
