@@ -413,6 +413,9 @@ struct Ring {
 #ifndef OPC_SKEW_LOOKAHEAD
 #define OPC_SKEW_LOOKAHEAD 3  // steps between a step's global loads and their use (NB <= 21)
 #endif
+#ifndef OPC_SKEW_LOOK3_MAXNB
+#define OPC_SKEW_LOOK3_MAXNB 21  // bins up to which loads run 3 steps ahead (registers)
+#endif
 #ifndef OPC_SKEW_HOIST_INIT
 #define OPC_SKEW_HOIST_INIT 1
 #endif
@@ -676,7 +679,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
                 // steps ahead (the init column's) is pulled into L2 now.
                 // Global loads run kLook steps ahead of their use (3 for NB <= 21:
                 // 1% faster on C4; 2 for more bins, where the registers run out).
-                constexpr int kLook = NB <= 21 ? OPC_SKEW_LOOKAHEAD : 2;
+                constexpr int kLook = NB <= OPC_SKEW_LOOK3_MAXNB ? OPC_SKEW_LOOKAHEAD : 2;
                 Loads n1 = fetch<false>(T, 32 * p + 1);
                 Loads n2{};
                 if constexpr (kLook >= 3) n2 = fetch<false>(T, 32 * p + 2);
