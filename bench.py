@@ -60,6 +60,17 @@ def colhist_ops_per_px(bins: int) -> int:
     return 7 * 2 + 8 * bins + 3 * bins + 12
 
 
+def best_fit_model(radius: int, bins: int) -> tuple[str, int]:
+    """The cheapest of SURVEY.md 8(d)'s per-pixel op models (the highest,
+    i.e. most conservative, roof): direct 7n^2 + 4B + 12, slide (Huang)
+    7*2n + 3B + 12, colhist 7*2 + 11B + 12, n = 2r + 1."""
+    n = 2 * radius + 1
+    models = {"direct": 7 * n * n + 4 * bins + 12, "slide": 7 * 2 * n + 3 * bins + 12,
+              "colhist": colhist_ops_per_px(bins)}
+    name = min(models, key=models.get)
+    return name, models[name]
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons, sampled every 20 ms from before the
     warm-up to after the timed region; summary() keeps the samples whose
@@ -247,13 +258,30 @@ def reference_arm(args, cfg) -> None:
 METRIC = "output megapixels/sec at radius r, levels L (1/2/4/8 B200) and % of roofline"
 
 
-def workload_config(cfg, n: int) -> dict:
+def rank0_in_bytes(cfg, n: int) -> int:
+    """Input bytes of rank 0 of an n-GPU run (its row band plus halos, or its frames)."""
+    W, H, F = cfg.width, cfg.height, cfg.frames
+    if F == 1:
+        from paper_1405_1020_b200 import band_input_rows
+        lo, hi = band_input_rows(H, 0, H // n, cfg.radius)
+        return (hi - lo) * W * 3
+    return (F // n) * H * W * 3
+
+
+def workload_config(cfg, n: int, in_bytes: int | None = None) -> dict:
     return {"workload": f"{cfg.name}: {cfg.description}", "width": cfg.width,
             "height": cfg.height, "frames": cfg.frames, "radius": cfg.radius,
             "levels": cfg.levels, "border": "CopyInput", "partition":
             ("frames" if cfg.frames > 1 else "row bands with r-row halos") + f" over {n} GPU(s)",
-            "l2": "input 805 MB > 126 MB L2 (no flush needed)" if cfg.name == "c4" else
-                  "inputs re-read each step; L2 not flushed (small config)"}
+            "l2": l2_note(rank0_in_bytes(cfg, n) if in_bytes is None else in_bytes)}
+
+
+def l2_note(in_bytes: int) -> str:
+    """Per-rank input bytes vs the L2 (main() flushes below 2 x 126 MiB)."""
+    mb = in_bytes / 2**20
+    if mb >= 2 * 126:
+        return f"input {mb:.0f} MiB per GPU > 126 MB L2 (no flush needed)"
+    return f"input {mb:.1f} MiB per GPU < 2 x 126 MB L2: L2 flushed between timed steps (512 MiB memset, untimed)"
 
 
 def main() -> None:
@@ -341,7 +369,14 @@ def main() -> None:
         step_device()
     stream.synchronize()
 
+    # Inputs smaller than twice the 126 MB L2 (configs 1-3): the L2 is flushed
+    # between timed steps (a 512 MB memset on the stream, outside the steps'
+    # event pairs), so every step reads its input from HBM.
+    flush = None
+    if host_in.numel() < 2 * 126 * 2**20:
+        flush = torch.empty(512 * 2**20, dtype=torch.uint8, device=f"cuda:{local}")
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    ev_end = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     launches0 = opc.kernel_launches()
     barrier()
     torch.cuda.synchronize()
@@ -351,23 +386,33 @@ def main() -> None:
     with ClockSampler(local) as clocks:
         clocks.mark_start()
         with torch.cuda.stream(stream):
-            ev[0].record(stream)
-            for i in range(args.steps):
-                step_device()
-                ev[i + 1].record(stream)
+            if flush is None:
+                ev[0].record(stream)
+                for i in range(args.steps):
+                    step_device()
+                    ev[i + 1].record(stream)
+            else:
+                for i in range(args.steps):
+                    flush.zero_()
+                    ev[i].record(stream)
+                    step_device()
+                    ev_end[i].record(stream)
         stream.synchronize()
         clocks.mark_end()
     torch.cuda.synchronize()
     barrier()
     launches = opc.kernel_launches() - launches0
-    step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    if flush is None:
+        step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    else:
+        step_ms = [ev[i].elapsed_time(ev_end[i]) for i in range(args.steps)]
     family = opc.plan_kernel(W, H, r, L)  # OPC_KERNEL_DIRECT/SKEW/SLIDE/COLUMN = 1-4
     kid = {4: _lib.OPC_KID_COLUMN}.get(family, family)  # timing ids: 1-3 as the families, 6 column
     kernel_total_ms, kernel_n = opc.kernel_timing_read(kid)
     pre_ms, _ = opc.kernel_timing_read(_lib.OPC_KID_PREPASS)
     border_ms, _ = opc.kernel_timing_read(_lib.OPC_KID_BORDER)
     opc.kernel_timing(False)
-    total_ms = ev[0].elapsed_time(ev[args.steps])
+    total_ms = ev[0].elapsed_time(ev[args.steps]) if flush is None else sum(step_ms)
     red_dev = f"cuda:{local}" if backend == "nccl" else "cpu"
     t = torch.tensor([total_ms], dtype=torch.float64, device=red_dev)
     if world > 1:
@@ -411,7 +456,7 @@ def main() -> None:
     sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
     num_sms = torch.cuda.get_device_properties(local).multi_processor_count
     peak_ops = num_sms * 4 * 32 * sm_mhz * 1e6
-    ops_px = colhist_ops_per_px(L + 1)
+    model_name, ops_px = best_fit_model(r, L + 1)
     # achieved = algorithmic lane-ops of the timed steps / time inside the
     # dominant kernel (its launches, CUDA events on the launch stream)
     kernel_ms = kernel_total_ms / max(1, kernel_n)
@@ -427,7 +472,7 @@ def main() -> None:
         "bound": "issue", "achieved": round(achieved_ops / 1e12, 3),
         "peak": round(peak_ops / 1e12, 3), "unit": "Tlane-op/s",
         "frac": round(achieved_ops / peak_ops, 4), "traffic": traffic,
-        "model": f"colhist {ops_px} lane-ops per interior pixel (SURVEY 8d, B={L + 1}); "
+        "model": f"{model_name} {ops_px} lane-ops per interior pixel (SURVEY 8d best fit, B={L + 1}); "
                  f"{num_sms} SMs x 4 x 32 x {sm_mhz:.0f} MHz ({peaks_kind} sm_max_mhz)",
         "algorithmic_ops_per_launch": ops_px * interior * args.steps // max(1, kernel_n),
         "kernel": {1: "direct", 2: "skew", 3: "slide", 4: "column"}.get(family, str(family)),
