@@ -124,11 +124,27 @@ __global__ void __launch_bounds__(kColThreads)
         if (ty0 < rows_per_pass) {
             const int x = min(x0 - r + tx, a.width - 1);
             const std::uint8_t* p = in + static_cast<std::size_t>(x) * 3;
-            for (int ty = ty0; ty < tht; ty += rows_per_pass) {
-                const int y = min(y0 - r + ty, in_last);
-                const std::uint8_t* q = p + static_cast<std::size_t>(y - a.in_row0) * stride;
-                const std::uint32_t R = q[0], G = q[1], B = q[2];
-                tile[ty * tw + tx] = B | (R << 8) | (G << 16) | (__umulhi(R + G + B, a.bin_mul) << 24);
+            // kLoadBatch rows' loads in flight before the first store: the
+            // launch is one round of blocks, so this phase is pure latency
+            constexpr int kLoadBatch = 8;
+            for (int ty = ty0; ty < tht; ty += kLoadBatch * rows_per_pass) {
+                std::uint32_t R[kLoadBatch], G[kLoadBatch], B[kLoadBatch];
+#pragma unroll
+                for (int j = 0; j < kLoadBatch; ++j) {
+                    const int y = min(y0 - r + min(ty + j * rows_per_pass, tht - 1), in_last);
+                    const std::uint8_t* q = p + static_cast<std::size_t>(y - a.in_row0) * stride;
+                    R[j] = q[0];
+                    G[j] = q[1];
+                    B[j] = q[2];
+                }
+#pragma unroll
+                for (int j = 0; j < kLoadBatch; ++j) {
+                    const int yy = ty + j * rows_per_pass;
+                    if (yy < tht) {
+                        tile[yy * tw + tx] = B[j] | (R[j] << 8) | (G[j] << 16) |
+                                             (__umulhi(R[j] + G[j] + B[j], a.bin_mul) << 24);
+                    }
+                }
             }
         }
     }
