@@ -33,8 +33,11 @@ int opc_generate(int32_t kind, uint64_t seed, int32_t width, int32_t height, int
 
 /* The same bytes written into DEVICE memory `d_out` (3*width*height bytes) on
  * `stream` (NULL: the library's stream of `device`; device < 0: current), for
- * kinds 0-3.  Asynchronous.  Returns 0, 1 (invalid argument or a kind without a
- * device generator) or 2 (CUDA error); opc_last_error() has the message. */
+ * every kind; OPC_PATTERN_VIDEO takes the frame folded into the seed (seed +
+ * frame, as opc_generate does internally).  Asynchronous, except that the first
+ * call of kinds 10/12 on a device copies the sine / Gaussian tables and waits
+ * for them.  Returns 0, 1 (invalid argument) or 2 (CUDA error);
+ * opc_last_error() has the message. */
 int opc_generate_device(int32_t kind, uint64_t seed, int32_t width, int32_t height,
                         uint8_t* d_out, int32_t device, void* stream);
 

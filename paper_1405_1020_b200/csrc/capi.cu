@@ -866,7 +866,7 @@ int opc_generate_device(int32_t kind, uint64_t seed, int32_t width, int32_t heig
     rc = opc::launch_generate(kind, seed, width, height, d_out, s, &e);
     if (rc == -1) {
         return set_error(OPC_EINVAL, "pattern kind " + std::to_string(kind) +
-                                         " has no device generator (kinds 0-3 do)");
+                                         " has no device generator");
     }
     if (rc != 0) return set_error(OPC_EINVAL, "invalid pattern spec");
     if (e != cudaSuccess) return cuda_error(e, "generator launch");

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "../../include/oilpaint_b200_patterns.h"
+#include "gen_spec.h"
 
 namespace {
 
@@ -110,36 +111,14 @@ const std::vector<std::int32_t>& gauss_table() {
     return t;
 }
 
-struct Wave {
-    std::uint32_t px, py, ph;  // phase increments in 2^-32 turns
-    std::int32_t amp;          // weight, sum over the 4 waves ~ 2^14
-};
-
 // Config 2 / 5 field: per channel, 4 sinusoids with 0.5-4 cycles across the
 // frame in x and y, random phase, amplitude in [0.5, 1).
 void smooth_field(std::uint64_t seed, int w, int h, bool gaussian, std::uint8_t* out,
                   int threads) {
-    Stream rng{seed};
-    Wave waves[3][4];
-    for (int c = 0; c < 3; ++c) {
-        double amp[4], sum = 0;
-        for (int k = 0; k < 4; ++k) {
-            amp[k] = 0.5 + 0.5 * rng.unit();
-            const double fx = (0.5 + 3.5 * rng.unit()) / w;
-            const double fy = (0.5 + 3.5 * rng.unit()) / h;
-            const double ph = rng.unit();
-            waves[c][k].px = static_cast<std::uint32_t>(std::llround(fx * 4294967296.0));
-            waves[c][k].py = static_cast<std::uint32_t>(std::llround(fy * 4294967296.0));
-            waves[c][k].ph = static_cast<std::uint32_t>(std::llround(ph * 4294967296.0) & 0xFFFFFFFFll);
-            sum += amp[k];
-        }
-        for (int k = 0; k < 4; ++k) {
-            waves[c][k].amp = static_cast<std::int32_t>(std::lround(amp[k] / sum * 16384.0));
-        }
-    }
-    const std::uint64_t noise_seed = rng.next();
-    const std::vector<std::int32_t>& sine = sine_table();
-    const std::vector<std::int32_t>* gauss = gaussian ? &gauss_table() : nullptr;
+    opc::SmoothSpec sp;
+    opc::smooth_spec(seed, w, h, &sp);
+    const std::int32_t* sine = opc::sine_table_data();
+    const std::int32_t* gauss = gaussian ? opc::gauss_table_data() : nullptr;
     parallel_rows(h, threads, [&](int y0, int y1) {
         for (int y = y0; y < y1; ++y) {
             for (int x = 0; x < w; ++x) {
@@ -147,15 +126,15 @@ void smooth_field(std::uint64_t seed, int w, int h, bool gaussian, std::uint8_t*
                 for (int c = 0; c < 3; ++c) {
                     std::int64_t s = 0;
                     for (int k = 0; k < 4; ++k) {
-                        const Wave& wv = waves[c][k];
+                        const opc::GenWave& wv = sp.waves[4 * c + k];
                         const std::uint32_t phase = wv.px * static_cast<std::uint32_t>(x) +
                                                     wv.py * static_cast<std::uint32_t>(y) + wv.ph;
                         s += static_cast<std::int64_t>(wv.amp) * sine[phase >> 20];
                     }
                     int v = 128 + static_cast<int>((s * 255) >> 30);
-                    const std::uint64_t word = stream_word(noise_seed, pix * 3 + c);
+                    const std::uint64_t word = stream_word(sp.noise_seed, pix * 3 + c);
                     if (gauss) {
-                        v += ((*gauss)[word & 0xFFFFu] + 128) >> 8;
+                        v += (gauss[word & 0xFFFFu] + 128) >> 8;
                     } else {
                         v += static_cast<int>(word % 17) - 8;
                     }
@@ -169,41 +148,22 @@ void smooth_field(std::uint64_t seed, int w, int h, bool gaussian, std::uint8_t*
 // Config 3: background colour plus 64 axis-aligned rectangles with random
 // inclusive corners and colours, painted in order (later on top).
 void rects(std::uint64_t seed, int w, int h, std::uint8_t* out, int threads) {
-    Stream rng{seed};
-    const std::uint64_t bg = rng.next();
-    struct Rect {
-        int x0, x1, y0, y1;
-        std::uint8_t r, g, b;
-    };
-    std::vector<Rect> rs(64);
-    for (Rect& q : rs) {
-        int xa = static_cast<int>(rng.next() % static_cast<std::uint64_t>(w));
-        int xb = static_cast<int>(rng.next() % static_cast<std::uint64_t>(w));
-        int ya = static_cast<int>(rng.next() % static_cast<std::uint64_t>(h));
-        int yb = static_cast<int>(rng.next() % static_cast<std::uint64_t>(h));
-        const std::uint64_t col = rng.next();
-        q.x0 = std::min(xa, xb);
-        q.x1 = std::max(xa, xb);
-        q.y0 = std::min(ya, yb);
-        q.y1 = std::max(ya, yb);
-        q.r = static_cast<std::uint8_t>(col);
-        q.g = static_cast<std::uint8_t>(col >> 8);
-        q.b = static_cast<std::uint8_t>(col >> 16);
-    }
+    opc::RectsSpec sp;
+    opc::rects_spec(seed, w, h, &sp);
     parallel_rows(h, threads, [&](int y0, int y1) {
         for (int y = y0; y < y1; ++y) {
             std::uint8_t* row = out + static_cast<std::size_t>(y) * w * 3;
             for (int x = 0; x < w; ++x) {
-                row[3 * x] = static_cast<std::uint8_t>(bg);
-                row[3 * x + 1] = static_cast<std::uint8_t>(bg >> 8);
-                row[3 * x + 2] = static_cast<std::uint8_t>(bg >> 16);
+                row[3 * x] = static_cast<std::uint8_t>(sp.bg);
+                row[3 * x + 1] = static_cast<std::uint8_t>(sp.bg >> 8);
+                row[3 * x + 2] = static_cast<std::uint8_t>(sp.bg >> 16);
             }
-            for (const Rect& q : rs) {
+            for (const opc::GenRect& q : sp.rects) {
                 if (y < q.y0 || y > q.y1) continue;
                 for (int x = q.x0; x <= q.x1; ++x) {
-                    row[3 * x] = q.r;
-                    row[3 * x + 1] = q.g;
-                    row[3 * x + 2] = q.b;
+                    row[3 * x] = static_cast<std::uint8_t>(q.rgb);
+                    row[3 * x + 1] = static_cast<std::uint8_t>(q.rgb >> 8);
+                    row[3 * x + 2] = static_cast<std::uint8_t>(q.rgb >> 16);
                 }
             }
         }
@@ -211,6 +171,52 @@ void rects(std::uint64_t seed, int w, int h, std::uint8_t* out, int threads) {
 }
 
 }  // namespace
+
+namespace opc {
+
+void smooth_spec(std::uint64_t seed, int w, int h, SmoothSpec* out) {
+    Stream rng{seed};
+    for (int c = 0; c < 3; ++c) {
+        double amp[4], sum = 0;
+        for (int k = 0; k < 4; ++k) {
+            amp[k] = 0.5 + 0.5 * rng.unit();
+            const double fx = (0.5 + 3.5 * rng.unit()) / w;
+            const double fy = (0.5 + 3.5 * rng.unit()) / h;
+            const double ph = rng.unit();
+            GenWave& wv = out->waves[4 * c + k];
+            wv.px = static_cast<std::uint32_t>(std::llround(fx * 4294967296.0));
+            wv.py = static_cast<std::uint32_t>(std::llround(fy * 4294967296.0));
+            wv.ph = static_cast<std::uint32_t>(std::llround(ph * 4294967296.0) & 0xFFFFFFFFll);
+            sum += amp[k];
+        }
+        for (int k = 0; k < 4; ++k) {
+            out->waves[4 * c + k].amp = static_cast<std::int32_t>(std::lround(amp[k] / sum * 16384.0));
+        }
+    }
+    out->noise_seed = rng.next();
+}
+
+void rects_spec(std::uint64_t seed, int w, int h, RectsSpec* out) {
+    Stream rng{seed};
+    out->bg = static_cast<std::uint32_t>(rng.next() & 0xFFFFFFu);
+    for (GenRect& q : out->rects) {
+        const int xa = static_cast<int>(rng.next() % static_cast<std::uint64_t>(w));
+        const int xb = static_cast<int>(rng.next() % static_cast<std::uint64_t>(w));
+        const int ya = static_cast<int>(rng.next() % static_cast<std::uint64_t>(h));
+        const int yb = static_cast<int>(rng.next() % static_cast<std::uint64_t>(h));
+        const std::uint64_t col = rng.next();
+        q.x0 = std::min(xa, xb);
+        q.x1 = std::max(xa, xb);
+        q.y0 = std::min(ya, yb);
+        q.y1 = std::max(ya, yb);
+        q.rgb = static_cast<std::uint32_t>(col & 0xFFFFFFu);
+    }
+}
+
+const std::int32_t* sine_table_data() { return sine_table().data(); }
+const std::int32_t* gauss_table_data() { return gauss_table().data(); }
+
+}  // namespace opc
 
 extern "C" int opc_generate(int32_t kind, uint64_t seed, int32_t w, int32_t h, int32_t frame,
                             uint8_t* out, int32_t threads) {

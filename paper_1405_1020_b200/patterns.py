@@ -37,9 +37,11 @@ def generate(kind: Pattern, width: int, height: int, seed: int = 0, frame: int =
 
 
 def generate_device(kind: Pattern, width: int, height: int, d_out: int, seed: int = 0,
-                    device: int = -1, stream: int | None = None) -> None:
-    """Write the pattern into device memory at address `d_out` (kinds NOISE,
-    GRADIENT, UNIFORM, CHECKER; asynchronous on `stream`)."""
+                    device: int = -1, stream: int | None = None, frame: int = 0) -> None:
+    """Write the pattern into device memory at address `d_out` (every kind, the
+    same bytes as generate(); asynchronous on `stream`)."""
+    if int(kind) == 12:  # VIDEO: frame f is the field seeded seed + f
+        seed = seed + frame
     rc = LIB.opc_generate_device(int(kind), seed & 0xFFFFFFFFFFFFFFFF, width, height, d_out,
                                  device, stream or None)
     if rc != 0:

@@ -72,20 +72,41 @@ def test_pipelined_host_path_large_image(gpu):
 @pytest.mark.gpu
 @pytest.mark.parametrize("kind,seed", [(opc.Pattern.NOISE, 4), (opc.Pattern.NOISE, 42),
                                        (opc.Pattern.GRADIENT, 0), (opc.Pattern.UNIFORM, 0x123456),
-                                       (opc.Pattern.CHECKER, 5)])
+                                       (opc.Pattern.CHECKER, 5), (opc.Pattern.SMOOTH, 2),
+                                       (opc.Pattern.RECTS, 3), (opc.Pattern.VIDEO, 5)])
 @pytest.mark.parametrize("w,h,offset", [(1, 1, 0), (333, 97, 0), (257, 3, 5), (1024, 64, 3)])
 def test_generate_device_matches_host(gpu, kind, seed, w, h, offset):
     """On-device generation writes the host generator's bytes,
-    also at unaligned destinations."""
+    also at unaligned destinations (VIDEO: frame 3 of the batch)."""
     import torch
+    frame = 3 if kind == opc.Pattern.VIDEO else 0
     buf = torch.full((w * h * 3 + offset + 8,), 0xAB, dtype=torch.uint8, device="cuda")
     opc.generate_device(kind, w, h, buf.data_ptr() + offset, seed=seed, device=0,
-                        stream=torch.cuda.current_stream().cuda_stream or None)
+                        stream=torch.cuda.current_stream().cuda_stream or None, frame=frame)
     torch.cuda.synchronize()
     got = buf.cpu().numpy()
-    want = opc.generate(kind, w, h, seed=seed).reshape(-1)
+    want = opc.generate(kind, w, h, seed=seed, frame=frame).reshape(-1)
     assert np.array_equal(got[offset:offset + want.size], want)
     assert (got[:offset] == 0xAB).all() and (got[offset + want.size:] == 0xAB).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["c2", "c3", "c5"])
+def test_generate_device_full_config_inputs(gpu, name):
+    """Full-size config inputs generated on the device hash to the committed
+    input digests (tests/golden/config_digests.json)."""
+    import hashlib
+    import json
+    import torch
+    cfg = opc.CONFIGS[name]
+    d = json.loads((Path(__file__).resolve().parent / "golden" / "config_digests.json").read_text())
+    frames = [0, cfg.frames - 1] if cfg.frames > 1 else [0]
+    buf = torch.empty(cfg.width * cfg.height * 3, dtype=torch.uint8, device="cuda")
+    for f in frames:
+        opc.generate_device(cfg.pattern, cfg.width, cfg.height, buf.data_ptr(), seed=cfg.seed,
+                            device=0, frame=f)
+        torch.cuda.synchronize()
+        assert hashlib.sha256(buf.cpu().numpy().tobytes()).hexdigest() == d[name]["inputs"][f], (name, f)
 
 
 def test_kernel_timing_records_each_launch(gpu):
