@@ -26,8 +26,8 @@ def test_best_fit_models_match_survey_table(bench):
     assert bench.best_fit_model(15, 21) == ("colhist", 257)  # C4
     assert bench.best_fit_model(7, 31) == ("slide", 315)     # C5
     assert bench.colhist_ops_per_px(21) == 257
-    # many bins, tiny window: the direct scan is the cheapest model
-    assert bench.best_fit_model(0, 257) == ("direct", 7 + 4 * 257 + 12)
+    # radius 0 with very few bins: the direct scan is the cheapest model
+    assert bench.best_fit_model(0, 2) == ("direct", 7 + 4 * 2 + 12)
 
 
 def test_l2_rule_and_rank_bytes(bench):
