@@ -23,6 +23,9 @@
 #include "border.cuh"
 #include "worksplit.cuh"
 
+#ifndef OPC_SLIDE_BRANCHFREE
+#define OPC_SLIDE_BRANCHFREE 1
+#endif
 #ifndef OPC_SLIDE_COOP_SUMS
 #define OPC_SLIDE_COOP_SUMS 1
 #endif
@@ -491,6 +494,31 @@ __global__ void __launch_bounds__(kWarps * 32)
                         const int best0 = best;
                         bool lost = false, cand = false;
                         int cand_b = 0, cand_c = 0;
+#if OPC_SLIDE_BRANCHFREE
+                        // Branch-free form: every row pays two count updates (of
+                        // zero when the pixel does not change bin), so lanes whose
+                        // changes sit at different rows do not diverge.
+                        for (int k = 0; k < w2; ++k) {
+                            const std::uint32_t ei = cin[k], eo = cout[k];
+                            const int bi = bin_of(ei, bm), bo = bin_of(eo, bm);
+                            const bool mv = bi != bo;
+                            const unsigned d = mv ? inc : 0u;
+                            const unsigned ki = cnt[bi * 32 + lane] + d;
+                            cnt[bi * 32 + lane] = static_cast<std::uint16_t>(ki);
+                            cnt[bo * 32 + lane] = static_cast<std::uint16_t>(cnt[bo * 32 + lane] - d);
+                            const int ci = static_cast<int>(ki >> kb_);
+                            lost |= mv && bo == best0;
+                            const bool better = mv && (ci > cand_c || (ci == cand_c && bi < cand_b));
+                            cand_b = better ? bi : cand_b;
+                            cand_c = better ? ci : cand_c;
+                            cand |= better;
+                            const std::uint32_t mi = bi == best0 ? 0xFFFFFFFFu : 0u;
+                            const std::uint32_t mo = bo == best0 ? 0xFFFFFFFFu : 0u;
+                            sr += (ei & mi & 0xFFu) - (eo & mo & 0xFFu);
+                            sg += ((ei & mi) >> 8 & 0xFFu) - ((eo & mo) >> 8 & 0xFFu);
+                            sb += ((ei & mi) >> 16 & 0xFFu) - ((eo & mo) >> 16 & 0xFFu);
+                        }
+#else
                         for (int k = 0; k < w2; ++k) {
                             const std::uint32_t ei = cin[k], eo = cout[k];
                             if (ei == eo) continue;
@@ -518,6 +546,7 @@ __global__ void __launch_bounds__(kWarps * 32)
                                 sb -= (eo >> 16) & 0xFFu;
                             }
                         }
+#endif
                         // Resolve the winner (filter.hpp:71-82).
                         const int bcf = cnt[best0 * 32 + lane] >> kb_;
                         bool changed = false, need = false;
