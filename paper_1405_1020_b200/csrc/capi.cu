@@ -366,6 +366,20 @@ int plan(int levels, int radius, int forced, long long interior_px) {
 
 // Runs the filter on device buffers already holding the band input.
 int run_device(const opc::BandArgs& band, int border, int kernel, DevCtx* ctx, cudaStream_t s) {
+    // Frames ride on gridDim.z (<= 65535) in the per-frame kernels: larger
+    // batches run as consecutive launches of at most that many frames.
+    constexpr int kMaxFrames = 65535;
+    if (band.frames > kMaxFrames) {
+        for (int f0 = 0; f0 < band.frames; f0 += kMaxFrames) {
+            opc::BandArgs b = band;
+            b.frames = std::min(kMaxFrames, band.frames - f0);
+            b.in = band.in + band.in_frame_stride * static_cast<std::size_t>(f0);
+            b.out = band.out + band.out_frame_stride * static_cast<std::size_t>(f0);
+            const int rc = run_device(b, border, kernel, ctx, s);
+            if (rc != OPC_OK) return rc;
+        }
+        return OPC_OK;
+    }
     // (a frame too large for the skew family's 32-bit plane offsets takes the direct family)
     cudaError_t e = cudaSuccess;
     opc::BandArgs a = band;

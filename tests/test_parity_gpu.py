@@ -263,6 +263,26 @@ def test_batch_equals_per_frame(gpu):
         assert np.array_equal(out[f], oracle_lib.oracle_filter(frames[f], 7, 30))
 
 
+def test_batch_beyond_grid_z_limit(gpu):
+    """More frames than gridDim.z allows (65535): consecutive launches."""
+    rng = np.random.default_rng(77)
+    n = 65535 + 1200
+    frames = rng.integers(0, 256, (n, 4, 5, 3), dtype=np.uint8)
+    torch = pytest.importorskip("torch")
+    dev_in = torch.from_numpy(frames).cuda()
+    for k in (AUTO, SKEW, DIRECT):
+        got = gpu.apply_cuda_batch(frames, gpu.FilterParams(1, 20), gpu.CudaConfig(kernel=k))
+        dev_out = torch.empty_like(dev_in)
+        gpu.apply_cuda_device(dev_in.data_ptr(), dev_out.data_ptr(), 5, 4, gpu.FilterParams(1, 20),
+                              gpu.CudaConfig(device=0, kernel=k), frames=n)
+        torch.cuda.synchronize()
+        dgot = dev_out.cpu().numpy()
+        for i in (0, 1, 65534, 65535, 65536, n - 1):
+            want = oracle_lib.oracle_filter(frames[i], 1, 20)
+            assert np.array_equal(got[i], want), (k, i)
+            assert np.array_equal(dgot[i], want), (k, i, "device")
+
+
 def test_device_pointer_path_with_torch_stream(gpu):
     torch = pytest.importorskip("torch")
     rng = np.random.default_rng(14)
