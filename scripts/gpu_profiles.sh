@@ -16,4 +16,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"col
 timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu --e2e-steps 1 > gpurun_out/plain_b.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 5 --warmup 3 --no-cpu --e2e-steps 1 > gpurun_out/ncu_launch.log 2>&1
 for c in c1 c2 c3 c5; do timeout 900 python bench.py --config $c --steps 20 --warmup 3 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; done
+for c in c1 c2 c3 c5; do timeout 900 python bench.py --impl reference --config $c --steps 3 --warmup 1 > gpurun_out/bench_ref_$c.json 2> gpurun_out/bench_ref_$c.err; done
 echo done > gpurun_out/profiles.done

@@ -11,6 +11,7 @@ for k in slide transpose; do python scripts/ncu_summary.py gpurun_out/prof_c3.nc
 python scripts/ncu_summary.py gpurun_out/prof_c5.ncu-rep profiles/r01_c5_skew_ncu skew > /dev/null
 python scripts/ncu_summary.py gpurun_out/prof_c2.ncu-rep profiles/r01_c2_column_ncu column > /dev/null
 for c in c1 c2 c3 c5; do [ -s gpurun_out/bench_$c.json ] && cp gpurun_out/bench_$c.json profiles/r01_bench_$c.json; done
+for c in c1 c2 c3 c5; do [ -s gpurun_out/bench_ref_$c.json ] && cp gpurun_out/bench_ref_$c.json profiles/r01_bench_reference_$c.json; done
 python - <<'PY'
 import json
 d = json.load(open('profiles/r01_c4_skew_ncu.json'))
