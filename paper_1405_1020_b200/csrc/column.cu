@@ -10,9 +10,9 @@
 //  * the tile's input pixels (plus the r-pixel halo) are loaded once into
 //    shared memory as entries B | R << 8 | G << 16 | bin << 24
 //    (bin = (R+G+B)*L/765, filter.hpp:31-35);
-//  * the thread's window histogram lives in shared memory as packed 64-bit
-//    words, hi = count << 22 | (31 - bin) << 16 | sumR, lo = sumG << 16 | sumB
-//    (r <= 7: sums < 2^16), in a [bin][thread] layout (a warp's dynamic-bin
+//  * the thread's window histogram lives in shared memory as two 32-bit words
+//    per bin, hi = count << 22 | (31 - bin) << 16 | sumR, lo = sumG << 16 | sumB
+//    (r <= 7: sums < 2^16), in [bin][thread] arrays (a warp's dynamic-bin
 //    accesses hit 32 consecutive words: conflict-free);
 //  * the first window is built with (2r+1)^2 updates, every next row with
 //    2(2r+1): the leaving row's pixels subtracted, the entering row's added
@@ -62,32 +62,19 @@ __host__ inline std::size_t col_smem_bytes(const ColGeom& g, int bins, int r) {
     return hist + tile + 16 + ((recip + 15) & ~std::size_t(15));
 }
 
-// Histogram word of one bin (r <= 7: window totals count <= 225, channel sums
-// <= 225 * 255 < 2^16):
+// Histogram words of one bin (r <= 7: window totals count <= 225, channel sums
+// <= 225 * 255 < 2^16), two independent 32-bit words:
 //   hi = count << 22 | (31 - bin) << 16 | sumR      lo = sumG << 16 | sumB
 // The constant (31 - bin) field makes the largest hi word the largest count at
 // the lowest bin, so the argmax is a plain max.  Adds and subtracts are modular
-// 64-bit arithmetic: exact whenever the window totals fit their fields.
+// 32-bit arithmetic, exact whenever the window totals fit their fields (no
+// carry ever needs to cross from lo to hi).  Separate [bin][thread] arrays of
+// 32-bit words: the argmax reads of the hi words are conflict-free (as the
+// high halves of 64-bit words, lanes t and t+16 shared a bank).
 // Tile entry of one pixel: B | R << 8 | G << 16 | bin << 24.
-__device__ __forceinline__ unsigned long long col_plus(unsigned long long w, std::uint32_t e) {
-    std::uint32_t wl, wh;
-    asm("mov.b64 {%0, %1}, %2;" : "=r"(wl), "=r"(wh) : "l"(w));
-    const std::uint32_t lo = __byte_perm(e, 0u, 0x4240);           // B | G << 16
-    const std::uint32_t hi = __byte_perm(e, 0x00400000u, 0x7641);  // R | 1 << 22
-    asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, %3;" : "+r"(wl), "+r"(wh) : "r"(lo), "r"(hi));
-    unsigned long long r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(wl), "r"(wh));
-    return r;
-}
-__device__ __forceinline__ unsigned long long col_minus(unsigned long long w, std::uint32_t e) {
-    std::uint32_t wl, wh;
-    asm("mov.b64 {%0, %1}, %2;" : "=r"(wl), "=r"(wh) : "l"(w));
-    const std::uint32_t lo = __byte_perm(e, 0u, 0x4240);
-    const std::uint32_t hi = __byte_perm(e, 0x00400000u, 0x7641);
-    asm("sub.cc.u32 %0, %0, %2;\n\tsubc.u32 %1, %1, %3;" : "+r"(wl), "+r"(wh) : "r"(lo), "r"(hi));
-    unsigned long long r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(wl), "r"(wh));
-    return r;
+__device__ __forceinline__ std::uint32_t col_lo(std::uint32_t e) { return __byte_perm(e, 0u, 0x4240); }  // B | G << 16
+__device__ __forceinline__ std::uint32_t col_hi(std::uint32_t e) {
+    return __byte_perm(e, 0x00400000u, 0x7641);  // R | 1 << 22
 }
 
 template <int NB>
@@ -106,7 +93,8 @@ __global__ void __launch_bounds__(kColThreads)
     const int r = a.radius;
     const int w2 = 2 * r + 1;
     const int tw = g.twc + 2 * r, tht = trows + 2 * r;
-    unsigned long long* hist = reinterpret_cast<unsigned long long*>(smem);  // [NB][256]
+    std::uint32_t* hist_hi = reinterpret_cast<std::uint32_t*>(smem);  // [NB][256]
+    std::uint32_t* hist_lo = hist_hi + NB * kColThreads;               // [NB][256]
     std::uint32_t* tile = reinterpret_cast<std::uint32_t*>(smem + std::size_t(NB) * kColThreads * 8);
     std::uint32_t* recip = tile + tw * tht;
     recip = reinterpret_cast<std::uint32_t*>((reinterpret_cast<std::uintptr_t>(recip) + 15) & ~std::uintptr_t(15));
@@ -153,7 +141,10 @@ __global__ void __launch_bounds__(kColThreads)
         recip[i] = i ? 0x80000000u / static_cast<std::uint32_t>(i) + 1u : 0u;
     }
 #pragma unroll
-    for (int b = 0; b < NB; ++b) hist[b * kColThreads + tid] = static_cast<unsigned long long>(31 - b) << 48;
+    for (int b = 0; b < NB; ++b) {
+        hist_hi[b * kColThreads + tid] = static_cast<std::uint32_t>(31 - b) << 16;
+        hist_lo[b * kColThreads + tid] = 0u;
+    }
     __syncthreads();
 
     const int cx = tid % g.twc, gy = tid / g.twc;
@@ -161,15 +152,17 @@ __global__ void __launch_bounds__(kColThreads)
     const int ybeg = y0 + gy * g.th;
     if (x >= a.x_hi || ybeg >= a.y_hi) return;
     const int yend = min(ybeg + g.th, a.y_hi);
-    unsigned long long* h = hist + tid;
+    std::uint32_t* hh = hist_hi + tid;
+    std::uint32_t* hl = hist_lo + tid;
     const std::uint32_t* col = tile + (gy * g.th) * tw + cx;  // window top-left of row ybeg
 
     for (int dy = 0; dy < w2; ++dy) {
         const std::uint32_t* row = col + dy * tw;
         for (int dx = 0; dx < w2; ++dx) {
             const std::uint32_t e = row[dx];
-            unsigned long long* p = h + (e >> 24) * kColThreads;
-            *p = col_plus(*p, e);
+            const int b = static_cast<int>(e >> 24) * kColThreads;
+            hh[b] += col_hi(e);
+            hl[b] += col_lo(e);
         }
     }
     std::uint8_t* o = a.out + a.out_frame_stride * frame +
@@ -179,7 +172,7 @@ __global__ void __launch_bounds__(kColThreads)
         // argmax (filter.hpp:71-82): the largest hi word
         std::uint32_t hw[NB];
 #pragma unroll
-        for (int b = 0; b < NB; ++b) hw[b] = static_cast<std::uint32_t>(h[b * kColThreads] >> 32);
+        for (int b = 0; b < NB; ++b) hw[b] = hh[b * kColThreads];
 #pragma unroll
         for (int step = 1; step < NB; step *= 3) {
 #pragma unroll
@@ -190,7 +183,7 @@ __global__ void __launch_bounds__(kColThreads)
         }
         const std::uint32_t hi32 = hw[0];
         const int best = 31 - static_cast<int>((hi32 >> 16) & 31u);
-        const std::uint32_t lo32 = static_cast<std::uint32_t>(h[best * kColThreads]);
+        const std::uint32_t lo32 = hl[best * kColThreads];
         const std::uint32_t m = recip[hi32 >> 22];  // filter.cpp:41-43
         o[0] = static_cast<std::uint8_t>(__umulhi((hi32 & 0xFFFFu) << 1, m));
         o[1] = static_cast<std::uint8_t>(__umulhi((lo32 >> 16) << 1, m));
@@ -202,10 +195,12 @@ __global__ void __launch_bounds__(kColThreads)
         const std::uint32_t* enter = col + w2 * tw;
         for (int dx = 0; dx < w2; ++dx) {
             const std::uint32_t el = leave[dx], ee = enter[dx];
-            unsigned long long* pl = h + (el >> 24) * kColThreads;
-            *pl = col_minus(*pl, el);
-            unsigned long long* pe = h + (ee >> 24) * kColThreads;
-            *pe = col_plus(*pe, ee);
+            const int bl = static_cast<int>(el >> 24) * kColThreads;
+            hh[bl] -= col_hi(el);
+            hl[bl] -= col_lo(el);
+            const int be = static_cast<int>(ee >> 24) * kColThreads;
+            hh[be] += col_hi(ee);
+            hl[be] += col_lo(ee);
         }
         col += tw;
     }
