@@ -256,19 +256,10 @@ __device__ __forceinline__ void rmw_sub_m(unsigned long long* Es, std::uint32_t 
 }
 
 // Lowest-index bin with the largest count (filter.hpp:71-82) and its truncated
-// channel averages (filter.cpp:41-43), packed R | G << 8 | B << 16.  Static
-// tournament: hi_b > (hi_a | 0x3FFFFF) <=> count_b > count_a; ties keep the
-// left (lower-bin) operand.  (Moving part of the first level onto the FMA pipe
-// with IMAD-based selects was measured slower: profiles/r01_notes.md.)
-#ifndef OPC_ARGMAX_SCAN
-#define OPC_ARGMAX_SCAN 1
-#endif
-#ifndef OPC_ARGMAX_SEL_BINS
-#define OPC_ARGMAX_SEL_BINS 0
-#endif
-#ifndef OPC_ARGMAX_GROUPS
-#define OPC_ARGMAX_GROUPS 1  // 3, 4, 7 measured slower (more instructions)
-#endif
+// channel averages (filter.cpp:41-43), packed R | G << 8 | B << 16.
+// (A static tournament, FMA-pipe selects in its first level, and 3/4/7
+// parallel scan groups were measured slower than the max-scan below:
+// profiles/r01_notes.md.)
 
 // Conditional copy on the FMA pipe: if (p) d = a * one (one = 1 at run time,
 // so ptxas cannot turn the predicated IMAD into an ALU select).
@@ -318,13 +309,12 @@ __device__ __forceinline__ std::uint32_t winner_rgb_key(const unsigned long long
 template <int NB>
 __device__ __forceinline__ std::uint32_t winner_rgb(const unsigned long long (&w)[NB],
                                                     const std::uint32_t* recip, std::uint32_t one) {
-#if OPC_ARGMAX_SCAN
     // Max-scan: the largest hi word carries the largest count c* (its low 22
     // bits are sums, irrelevant to the count).  T = c* << 22; then a scan from
     // the top bin down keeps the last (= lowest-index) bin with hi >= T, i.e.
-    // count == c*.  The max is an ALU min/max tree; the conditional copies are
-    // predicated IMADs on the FMA pipe, which has the spare issue slots.
-    // Balanced max tree (short dependency chains: few warps per scheduler).
+    // count == c*.  The max is an ALU min/max tree (balanced: short dependency
+    // chains); the conditional copies are predicated IMADs on the FMA pipe,
+    // which has the spare issue slots.
     std::uint32_t mx[NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b) mx[b] = static_cast<std::uint32_t>(w[b] >> 32);
@@ -337,51 +327,12 @@ __device__ __forceinline__ std::uint32_t winner_rgb(const unsigned long long (&w
         }
     }
     const std::uint32_t T = mx[0] & 0xFFC00000u;
-    // G independent scans over groups of bins, then the groups merged the
-    // same way (a group without a hit keeps its top bin, whose hi < T).
-    constexpr int G = OPC_ARGMAX_GROUPS;
-    constexpr int GS = (NB + G - 1) / G;
-    std::uint32_t glo[G], ghi[G];
+    std::uint32_t lo = static_cast<std::uint32_t>(w[NB - 1]);
+    std::uint32_t hi = static_cast<std::uint32_t>(w[NB - 1] >> 32);
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-        const int b0 = g * GS, b1 = min(NB, b0 + GS) - 1;
-        if (b0 > b1) continue;
-        glo[g] = static_cast<std::uint32_t>(w[b1]);
-        ghi[g] = static_cast<std::uint32_t>(w[b1] >> 32);
-#pragma unroll
-        for (int b = b1 - 1; b >= b0; --b) {
-            const std::uint32_t bl = static_cast<std::uint32_t>(w[b]);
-            const std::uint32_t bh = static_cast<std::uint32_t>(w[b] >> 32);
-            if (b < OPC_ARGMAX_SEL_BINS) {
-                const bool p = bh >= T;
-                glo[g] = p ? bl : glo[g];
-                ghi[g] = p ? bh : ghi[g];
-            } else {
-                pick_if_ge(glo[g], ghi[g], bl, bh, T, one);
-            }
-        }
+    for (int b = NB - 2; b >= 0; --b) {
+        pick_if_ge(lo, hi, static_cast<std::uint32_t>(w[b]), static_cast<std::uint32_t>(w[b] >> 32), T, one);
     }
-    int last = G - 1;
-    while (last * GS >= NB) --last;
-    std::uint32_t lo = glo[last], hi = ghi[last];
-#pragma unroll
-    for (int g = last - 1; g >= 0; --g) pick_if_ge(lo, hi, glo[g], ghi[g], T, one);
-#else
-    unsigned long long t[NB];
-#pragma unroll
-    for (int b = 0; b < NB; ++b) t[b] = w[b];
-#pragma unroll
-    for (int step = 1; step < NB; step <<= 1) {
-#pragma unroll
-        for (int i = 0; i + step < NB; i += 2 * step) {
-            const std::uint32_t ah = static_cast<std::uint32_t>(t[i] >> 32);
-            const std::uint32_t bh = static_cast<std::uint32_t>(t[i + step] >> 32);
-            t[i] = bh > (ah | 0x3FFFFFu) ? t[i + step] : t[i];
-        }
-    }
-    const std::uint32_t lo = static_cast<std::uint32_t>(t[0]);
-    const std::uint32_t hi = static_cast<std::uint32_t>(t[0] >> 32);
-#endif
     const std::uint32_t count = hi >> 22;
     const std::uint32_t m = recip[count];
     const std::uint32_t sr = (hi >> 4) & 0x3FFFFu;

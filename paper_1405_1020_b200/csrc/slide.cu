@@ -23,12 +23,6 @@
 #include "border.cuh"
 #include "worksplit.cuh"
 
-#ifndef OPC_SLIDE_BRANCHFREE
-#define OPC_SLIDE_BRANCHFREE 1
-#endif
-#ifndef OPC_SLIDE_COOP_SUMS
-#define OPC_SLIDE_COOP_SUMS 1
-#endif
 
 namespace opc {
 
@@ -494,7 +488,6 @@ __global__ void __launch_bounds__(kWarps * 32)
                         const int best0 = best;
                         bool lost = false, cand = false;
                         int cand_b = 0, cand_c = 0;
-#if OPC_SLIDE_BRANCHFREE
                         // Branch-free form: every row pays two count updates (of
                         // zero when the pixel does not change bin), so lanes whose
                         // changes sit at different rows do not diverge.
@@ -518,35 +511,6 @@ __global__ void __launch_bounds__(kWarps * 32)
                             sg += ((ei & mi) >> 8 & 0xFFu) - ((eo & mo) >> 8 & 0xFFu);
                             sb += ((ei & mi) >> 16 & 0xFFu) - ((eo & mo) >> 16 & 0xFFu);
                         }
-#else
-                        for (int k = 0; k < w2; ++k) {
-                            const std::uint32_t ei = cin[k], eo = cout[k];
-                            if (ei == eo) continue;
-                            const int bi = bin_of(ei, bm), bo = bin_of(eo, bm);
-                            if (bi != bo) {
-                                const unsigned ki = cnt[bi * 32 + lane] + inc;
-                                cnt[bi * 32 + lane] = static_cast<std::uint16_t>(ki);
-                                cnt[bo * 32 + lane] = static_cast<std::uint16_t>(cnt[bo * 32 + lane] - inc);
-                                const int ci = static_cast<int>(ki >> kb_);
-                                if (bo == best0) lost = true;
-                                if (ci > cand_c || (ci == cand_c && bi < cand_b)) {
-                                    cand_b = bi;
-                                    cand_c = ci;
-                                    cand = true;
-                                }
-                            }
-                            if (bi == best0) {
-                                sr += ei & 0xFFu;
-                                sg += (ei >> 8) & 0xFFu;
-                                sb += (ei >> 16) & 0xFFu;
-                            }
-                            if (bo == best0) {
-                                sr -= eo & 0xFFu;
-                                sg -= (eo >> 8) & 0xFFu;
-                                sb -= (eo >> 16) & 0xFFu;
-                            }
-                        }
-#endif
                         // Resolve the winner (filter.hpp:71-82).
                         const int bcf = cnt[best0 * 32 + lane] >> kb_;
                         bool changed = false, need = false;
@@ -574,7 +538,6 @@ __global__ void __launch_bounds__(kWarps * 32)
                                 changed = best != best0;
                             }
                         }
-#if OPC_SLIDE_COOP_SUMS
                         // Winner changed: the new winner's window sums, one lane's
                         // window at a time with lane c < 2r+1 summing its column c
                         // (2r+1 loads per lane instead of (2r+1)^2 on one lane
@@ -603,9 +566,6 @@ __global__ void __launch_bounds__(kWarps * 32)
                                 sb = cbb;
                             }
                         }
-#else
-                        if (changed) window_sums(x, best, sr, sg, sb);
-#endif
                     }
                 }
                 if (row_ok) {
