@@ -37,9 +37,6 @@ namespace {
 #ifndef OPC_SLIDE_UNROLL_SUMS
 #define OPC_SLIDE_UNROLL_SUMS 16
 #endif
-#ifndef OPC_SLIDE_STEAL
-#define OPC_SLIDE_STEAL 0  // measured no gain on config 3 once rescans were unrolled
-#endif
 #ifndef OPC_SLIDE_GUIDED_K
 #define OPC_SLIDE_GUIDED_K 0  // > 0: guided claims of remaining / (k x resident warps); measured no gain on C3
 #endif
@@ -156,34 +153,6 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;"); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;"); }
 
-// ---- work stealing between warps ----
-// The slide kernel's step cost depends on the content (a run of columns where
-// rectangle edges make the window winners change costs several times a flat
-// run), so even chunks of equal width leave some warps running long after the
-// rest are idle (config 3 trace: median pass 131 us, slowest 736 us).  Every
-// warp publishes its current pass in a slot: word = seq:24 | prog:20 | lim:20
-// (columns relative to x_lo: the pass runs up to lim, prog = the start of the
-// phase it is in).  A warp that finds the queue empty takes the upper half of
-// the pass with the most columns left by lowering that pass's lim with a CAS
-// on the whole word -- so the victim's published progress is the one the cut
-// was computed from: the victim is inside the published phase and reads lim at
-// its next phase start, so every column from the next phase on can be taken.
-struct StealSlot {
-    unsigned long long word;
-    int x0, f, kb, pad;
-};
-__device__ __forceinline__ unsigned long long steal_word(unsigned seq, int prog, int lim) {
-    return (static_cast<unsigned long long>(seq & 0xFFFFFFu) << 40) |
-           (static_cast<unsigned long long>(prog & 0xFFFFF) << 20) |
-           static_cast<unsigned long long>(lim & 0xFFFFF);
-}
-__device__ __forceinline__ int word_lim(unsigned long long w) { return static_cast<int>(w & 0xFFFFF); }
-__device__ __forceinline__ int word_prog(unsigned long long w) { return static_cast<int>((w >> 20) & 0xFFFFF); }
-__device__ __forceinline__ unsigned word_seq(unsigned long long w) { return static_cast<unsigned>(w >> 40); }
-#ifndef OPC_SLIDE_MIN_STEAL
-#define OPC_SLIDE_MIN_STEAL 64
-#endif
-constexpr int kMinSteal = OPC_SLIDE_MIN_STEAL;  // columns left for a pass to be worth splitting
 
 #if OPC_SLIDE_TRACE
 // Debug trace of the passes (OPC_SLIDE_TRACE builds only): per pass
@@ -200,7 +169,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 template <int kRingCols>
 __global__ void __launch_bounds__(kWarps * 32)
     slide_kernel(BandArgs a, const std::uint32_t* __restrict__ T, TGeom tg, int* task_counter,
-                 WorkSplit g, StealSlot* board) {
+                 WorkSplit g) {
     extern __shared__ __align__(16) unsigned char smem[];
     std::uint32_t* recip = reinterpret_cast<std::uint32_t*>(smem);
     const int lane = threadIdx.x & 31;
@@ -231,82 +200,9 @@ __global__ void __launch_bounds__(kWarps * 32)
 
     long long u = 0, u_end = 0;
     int f, kb, x0, x1;
-    StealSlot* const mine = board + (blockIdx.x * (blockDim.x >> 5) + warp);
-    const int nslots = gridDim.x * (blockDim.x >> 5);
-    unsigned seq = 0;
-    bool queue = true;
-    int tries = 0;
-    for (;;) {
-        bool have = queue && next_pass<(OPC_SLIDE_GUIDED_K > 0)>(g, task_counter, lane, u, u_end, f,
-                                                                 kb, x0, x1);
-        if (!have) {
-            queue = false;
-            if (!OPC_SLIDE_STEAL) break;
-            // Steal: the published pass with the most columns left.
-            int best_rem = 0, best_i = -1;
-#pragma unroll 4
-            for (int i = lane; i < nslots; i += 32) {  // L2 loads, pipelined (not volatile)
-                const unsigned long long w = __ldcg(&board[i].word);
-                const int rem = word_lim(w) - word_prog(w);
-                if (rem > best_rem) {
-                    best_rem = rem;
-                    best_i = i;
-                }
-            }
-            for (int o = 16; o; o >>= 1) {
-                const int r2 = __shfl_xor_sync(FULL, best_rem, o);
-                const int i2 = __shfl_xor_sync(FULL, best_i, o);
-                if (r2 > best_rem || (r2 == best_rem && i2 > best_i)) {
-                    best_rem = r2;
-                    best_i = i2;
-                }
-            }
-            if (best_rem < kMinSteal) break;
-            int ok = 0;
-            if (lane == 0) {
-                StealSlot* v = board + best_i;
-                const unsigned long long w = *reinterpret_cast<volatile unsigned long long*>(&v->word);
-                __threadfence();
-                const int vx0 = *reinterpret_cast<volatile int*>(&v->x0);
-                const int vf = *reinterpret_cast<volatile int*>(&v->f);
-                const int vkb = *reinterpret_cast<volatile int*>(&v->kb);
-                const int P = word_prog(w), L = word_lim(w);
-                // cut: from the phase after the victim's published one, halve
-                // what is left, 32-aligned relative to the victim's pass start
-                int mid = P + kPhase + ((L - P - kPhase) / 2);
-                mid = vx0 + ((mid - vx0 + kPhase - 1) & ~(kPhase - 1));
-                if (mid < L && mid >= P + kPhase &&
-                    atomicCAS(&v->word, w, steal_word(word_seq(w), P, mid)) == w) {
-                    ok = 1;
-                    f = vf;
-                    kb = vkb;
-                    x0 = mid;
-                    x1 = L;
-                }
-            }
-            ok = __shfl_sync(FULL, ok, 0);
-            if (!ok) {  // lost a race: look again (bounded)
-                if (++tries > 256) break;
-                continue;
-            }
-            f = __shfl_sync(FULL, f, 0);
-            kb = __shfl_sync(FULL, kb, 0);
-            x0 = __shfl_sync(FULL, x0, 0);
-            x1 = __shfl_sync(FULL, x1, 0);
-        }
-        // Publish the pass: first an empty range under a new seq (a thief that
-        // read the old fields then fails its CAS), then the fields, then the range.
-        if (lane == 0) {
-            atomicExch(&mine->word, steal_word(++seq, x0, x0));
-            mine->x0 = x0;
-            mine->f = f;
-            mine->kb = kb;
-            __threadfence();
-            atomicExch(&mine->word, steal_word(++seq, x0, x1));
-        }
-        __syncwarp();
-        int pass_cols = x1 - x0;  // lowered when a thief takes the pass's tail
+    while (next_pass<(OPC_SLIDE_GUIDED_K > 0)>(g, task_counter, lane, u, u_end, f, kb, x0, x1)) {
 #if OPC_SLIDE_TRACE
+        int pass_cols = x1 - x0;
         const unsigned long long t_start = gtime();
         struct TraceGuard {
             int kb, x0, &cols, lane, stolen;
@@ -326,7 +222,7 @@ __global__ void __launch_bounds__(kWarps * 32)
                     }
                 }
             }
-        } trace_guard{kb, x0, pass_cols, lane, !queue, t_start};
+        } trace_guard{kb, x0, pass_cols, lane, 0, t_start};
 #endif
         const int yb = a.y_lo + 32 * kb;
         const int xs = a.x_lo + x0;
@@ -447,23 +343,6 @@ __global__ void __launch_bounds__(kWarps * 32)
 
         int n = xe - xs;
         for (int p = 0; kPhase * p < n; ++p) {
-            if (OPC_SLIDE_STEAL && p > 0) {  // publish progress, learn a lowered end
-                int lim = 0;
-                if (lane == 0) {
-                    unsigned long long w = *reinterpret_cast<volatile unsigned long long*>(&mine->word);
-                    for (;;) {
-                        const unsigned long long nw = steal_word(word_seq(w), x0 + kPhase * p, word_lim(w));
-                        const unsigned long long prev = atomicCAS(&mine->word, w, nw);
-                        if (prev == w) break;
-                        w = prev;
-                    }
-                    lim = word_lim(w);
-                }
-                lim = __shfl_sync(FULL, lim, 0);
-                n = min(n, lim - x0);
-                pass_cols = n;
-                if (kPhase * p >= n) break;
-            }
             if (p > 0) {
                 // Phase p's entering columns were requested a phase ago; request p+1's.
                 load_chunk(w2 + kPhase * (p + 1), kPhase);
@@ -609,12 +488,9 @@ bool slide_supported(int levels, int radius) {
            kRecipBytes + per_warp_bytes(levels + 1, radius) <= 227 * 1024;
 }
 
-constexpr int kMaxBoardSlots = 148 * 8 * 4;  // resident warps of up to 4 x 148 x 8
-
 std::size_t slide_scratch_bytes(const BandArgs& a) {
     if (a.y_hi <= a.y_lo || a.x_hi <= a.x_lo) return 0;
-    return tgeom(a).frame_elems * a.frames * sizeof(std::uint32_t) +
-           kMaxBoardSlots * sizeof(StealSlot);
+    return tgeom(a).frame_elems * a.frames * sizeof(std::uint32_t);
 }
 
 cudaError_t launch_slide(const BandArgs& a, int* counter, void* scratch, int num_sms,
@@ -659,23 +535,18 @@ cudaError_t launch_slide(const BandArgs& a, int* counter, void* scratch, int num
     long long blocks = (g.nchunks + warps - 1) / warps;
     if (blocks > static_cast<long long>(num_sms) * per_sm) blocks = num_sms * per_sm;
     if (blocks < 1) blocks = 1;
-    StealSlot* board = reinterpret_cast<StealSlot*>(
-        static_cast<unsigned char*>(scratch) + tg.frame_elems * a.frames * sizeof(std::uint32_t));
-    if (blocks * warps > kMaxBoardSlots) return cudaErrorInvalidConfiguration;
-    e = cudaMemsetAsync(board, 0, static_cast<std::size_t>(blocks) * warps * sizeof(StealSlot), s);
-    if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(counter, 0, 4 * sizeof(int), s);
     if (e != cudaSuccess) return e;
     timing_mark(kIdSlide, 0, s);
     const dim3 grid(static_cast<unsigned>(blocks)), block(warps * 32);
     if (rc == 64) {
-        slide_kernel<64><<<grid, block, smem, s>>>(a, T, tg, counter, g, board);
+        slide_kernel<64><<<grid, block, smem, s>>>(a, T, tg, counter, g);
     } else if (rc == 80) {
-        slide_kernel<80><<<grid, block, smem, s>>>(a, T, tg, counter, g, board);
+        slide_kernel<80><<<grid, block, smem, s>>>(a, T, tg, counter, g);
     } else if (rc == 88) {
-        slide_kernel<88><<<grid, block, smem, s>>>(a, T, tg, counter, g, board);
+        slide_kernel<88><<<grid, block, smem, s>>>(a, T, tg, counter, g);
     } else {
-        slide_kernel<96><<<grid, block, smem, s>>>(a, T, tg, counter, g, board);
+        slide_kernel<96><<<grid, block, smem, s>>>(a, T, tg, counter, g);
     }
     timing_mark(kIdSlide, 1, s);
     return cudaGetLastError();
