@@ -473,7 +473,10 @@ def main() -> None:
         "peak": round(peak_ops / 1e12, 3), "unit": "Tlane-op/s",
         "frac": round(achieved_ops / peak_ops, 4), "traffic": traffic,
         "model": f"{model_name} {ops_px} lane-ops per interior pixel (SURVEY 8d best fit, B={L + 1}); "
-                 f"{num_sms} SMs x 4 x 32 x {sm_mhz:.0f} MHz ({peaks_kind} sm_max_mhz)",
+                 f"{num_sms} SMs x 4 x 32 x {sm_mhz:.0f} MHz ({peaks_kind} sm_max_mhz)"
+                 + ("; the slide kernel skips the updates of flat steps (no pixel of the "
+                    "entering column differs from the leaving one), which the model counts, so "
+                    "frac > 1 is possible on flat content" if family == 3 else ""),
         "algorithmic_ops_per_launch": ops_px * interior * args.steps // max(1, kernel_n),
         "kernel": {1: "direct", 2: "skew", 3: "slide", 4: "column"}.get(family, str(family)),
         "kernel_ms": round(kernel_ms, 4),
