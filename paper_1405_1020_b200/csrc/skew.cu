@@ -97,7 +97,7 @@ __device__ __forceinline__ std::uint32_t entry_from_brg(std::uint32_t t, std::ui
 // global memory and splits them with byte permutes; row stride 132 words keeps
 // both the 16-byte tile stores and the diagonal reads conflict-free.
 __global__ void __launch_bounds__(256)
-    shear_kernel(BandArgs a, std::uint32_t* S, ShearGeom g, int vec_ok, int key) {
+    shear_kernel(BandArgs a, std::uint32_t* S, ShearGeom g, int vec_ok, int key, std::uint32_t* bmask) {
     __shared__ __align__(16) std::uint32_t tile[kShearRows * kShearStride];
     if (static_cast<int>(blockIdx.y) >= g.Hs / kShearRows) {  // appended border blocks
         const int b = (blockIdx.y - g.Hs / kShearRows) * gridDim.x + blockIdx.x;
@@ -152,6 +152,27 @@ __global__ void __launch_bounds__(256)
         }
     }
     __syncthreads();
+    if (bmask) {
+        // Bin masks of the tile's four 32-column blocks (bit b: some pixel of
+        // the block has bin b), for the skew kernel's per-phase bin groups:
+        // warp w covers block w / 2, rows (w & 1) * 16 .. + 15.
+        __shared__ std::uint32_t wm[8];
+        const int j = warp >> 1;
+        std::uint32_t m = 0;
+#pragma unroll
+        for (int rr = 0; rr < 16; ++rr) {
+            const std::uint32_t e = tile[((warp & 1) * 16 + rr) * kShearStride + 32 * j + lane];
+            m |= 1u << (key ? e >> 24 : e >> 26);
+        }
+        m = __reduce_or_sync(0xFFFFFFFFu, m);
+        if (lane == 0) wm[warp] = m;
+        __syncthreads();
+        if (threadIdx.x < kShearCols / 32) {
+            const std::size_t nbx = static_cast<std::size_t>(gridDim.x) * (kShearCols / 32);
+            bmask[(static_cast<std::size_t>(frame) * (g.Hs / kShearRows) + blockIdx.y) * nbx +
+                  blockIdx.x * (kShearCols / 32) + threadIdx.x] = wm[2 * threadIdx.x] | wm[2 * threadIdx.x + 1];
+        }
+    }
     // Element (x, y) -> (x + yo) * Hs + yo with yo = y - y_base; for row lane of
     // the tile and diagonal dd = c + lane that is base + dd * Hs.  The grid
     // covers exactly Hs rows, so only the column range needs a check.
@@ -414,7 +435,14 @@ struct Task {
     int NV, X0, w2, lane;
     int y_rows;               // valid rows in the band (<= 32)
     std::size_t stride;
+    std::uint32_t gm;         // bin groups (8 bins each) the current phase touches (GROUPED steps)
 };
+#ifndef OPC_SKEW_GROUPS
+#define OPC_SKEW_GROUPS 1  // KEY launches with NB >= 24: skip the E rows of bin groups a phase never sees
+#endif
+#ifndef OPC_SKEW_GROUP_BINS
+#define OPC_SKEW_GROUP_BINS 8  // bins per group (4, 8 or 16)
+#endif
 
 // 32-bit element offset from a 64-bit base: one IMAD.WIDE (FMA pipe; the
 // runtime multiplier four = 4 keeps ptxas from turning it into ALU LEAs).
@@ -493,15 +521,34 @@ __device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
     }
     if (!EDGE || (v >= 0 && v < T.NV)) {
         const int slot = static_cast<unsigned>(v) % SL;
-        unsigned long long e[NB];
+        // GROUPED: E rows of bin groups the phase's pixels never reach are
+        // zero for every column of the phase: neither read nor added (the
+        // winner first, then each active group's rows loaded and added).
+        constexpr bool GROUPED = KEY && NB >= 24 && OPC_SKEW_GROUPS && !EDGE;
+        if constexpr (GROUPED) {
+            stage[t * kStageStride + (v & 31)] = winner_rgb_key<NB>(win, recip);
+            constexpr int GS = OPC_SKEW_GROUP_BINS;
 #pragma unroll
-        for (int b = 0; b < NB; ++b) e[b] = E[b * SL + slot];
-        if (!EDGE || (v >= w2 && t < T.y_rows)) {
-            stage[t * kStageStride + (v & 31)] =
-                KEY ? winner_rgb_key<NB>(win, recip) : winner_rgb<NB>(win, recip, T.M.one);
+            for (int g8 = 0; g8 < (NB + GS - 1) / GS; ++g8) {
+                if ((T.gm >> g8) & 1u) {
+                    unsigned long long e[GS];
+#pragma unroll
+                    for (int b = GS * g8; b < NB && b < GS * g8 + GS; ++b) e[b - GS * g8] = E[b * SL + slot];
+#pragma unroll
+                    for (int b = GS * g8; b < NB && b < GS * g8 + GS; ++b) win[b] += e[b - GS * g8];
+                }
+            }
+        } else {
+            unsigned long long e[NB];
+#pragma unroll
+            for (int b = 0; b < NB; ++b) e[b] = E[b * SL + slot];
+            if (!EDGE || (v >= w2 && t < T.y_rows)) {
+                stage[t * kStageStride + (v & 31)] =
+                    KEY ? winner_rgb_key<NB>(win, recip) : winner_rgb<NB>(win, recip, T.M.one);
+            }
+#pragma unroll
+            for (int b = 0; b < NB; ++b) win[b] += e[b];
         }
-#pragma unroll
-        for (int b = 0; b < NB; ++b) win[b] += e[b];
         // Advance E(v) from row t to row t + 1 (lane t + 1 reads it next step).
         unsigned long long* Es = E + slot;
         rmw_add<SL, KEY>(Es, cur.a, T.M);
@@ -561,10 +608,40 @@ __device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
     __syncwarp();
 }
 
+// Bin groups (8 bins each) the pixels of a steady phase can contribute to:
+// the lanes' E columns v in [s0 - 31, s0 + 31] hold column histograms of image
+// columns [xs - r + v - w2, xs - r + v], rows [yb - r, yb + 31 + r]; the OR of
+// the shear pre-pass's 32 x 32 block bin masks over that region.
+__device__ __forceinline__ std::uint32_t phase_groups(const BandArgs& a, const ShearGeom& sg,
+                                                      const std::uint32_t* bmask, int f, int yb, int xs,
+                                                      int s0, int w2, int lane) {
+    const int r = a.radius;
+    const int nty = sg.Hs / kShearRows;
+    const int nbx = (a.width + kShearPad + kShearCols - 1) / kShearCols * (kShearCols / 32);
+    const int ty0 = (yb - r - sg.y_base) >> 5;
+    const int ty1 = min(nty - 1, (yb + 31 + r - sg.y_base) >> 5);
+    const int c0 = max(0, xs - r + s0 - 31 - w2);
+    const int c1 = min(a.width + kShearPad - 1, xs - r + s0 + 31);
+    const int bx0 = c0 >> 5, bx1 = max(bx0, c1 >> 5);
+    const int nx = bx1 - bx0 + 1;
+    std::uint32_t m = 0;
+    if (lane < (ty1 - ty0 + 1) * nx) {
+        const int ty = ty0 + lane / nx, bx = bx0 + lane % nx;
+        m = bmask[(static_cast<std::size_t>(f) * nty + ty) * nbx + bx];
+    }
+    m = __reduce_or_sync(0xFFFFFFFFu, m);
+    constexpr int GS = OPC_SKEW_GROUP_BINS;
+    constexpr std::uint32_t gmask = (1u << GS) - 1u;
+    std::uint32_t gm = 0;
+#pragma unroll
+    for (int g8 = 0; g8 < 32 / GS; ++g8) gm |= ((m >> (GS * g8)) & gmask) ? 1u << g8 : 0u;
+    return gm;
+}
+
 template <int NB, int SL, bool SPARSE>
 __global__ void __launch_bounds__(kMaxWarps * 32)
     skew_kernel(BandArgs a, const std::uint32_t* __restrict__ S, ShearGeom sg, int* task_counter,
-                WorkSplit g, Mul M) {
+                WorkSplit g, Mul M, const std::uint32_t* __restrict__ bmask) {
     extern __shared__ __align__(16) unsigned char smem[];
     std::uint32_t* recip = reinterpret_cast<std::uint32_t*>(smem);
     const int lane = threadIdx.x & 31;
@@ -632,6 +709,9 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
             // y_rows read valid plane rows and are never flushed.)
             const bool steady = p >= p_steady_lo && 32 * p + 31 < T.NV;
             if (steady) {
+                if constexpr (SPARSE && OPC_SKEW_KEY && NB >= 24 && OPC_SKEW_GROUPS) {
+                    T.gm = phase_groups(a, sg, bmask, f, yb, xs, 32 * p, T.w2, lane);
+                }
                 // Loads run two steps ahead; the diagonal first touched eight
                 // steps ahead (the init column's) is pulled into L2 now.
                 // Global loads run kLook steps ahead of their use (3 for NB <= 21:
@@ -694,6 +774,11 @@ cudaError_t launch_nbs(const BandArgs& a, int* counter, void* scratch, int num_s
 
     const ShearGeom sg = shear_geom(a);
     std::uint32_t* S = static_cast<std::uint32_t*>(scratch);
+    // block bin-mask table (GROUPED launches), after the plane
+    std::uint32_t* bmask = nullptr;
+    if constexpr (SPARSE && OPC_SKEW_KEY && NB >= 24 && OPC_SKEW_GROUPS) {
+        bmask = S + sg.frame_elems * a.frames;
+    }
     {
         const unsigned gx = static_cast<unsigned>((a.width + kShearPad + kShearCols - 1) / kShearCols);
         const dim3 grid(gx, static_cast<unsigned>(sg.Hs / kShearRows) + border_grid_rows(a, gx),
@@ -702,7 +787,7 @@ cudaError_t launch_nbs(const BandArgs& a, int* counter, void* scratch, int num_s
                            ((static_cast<std::size_t>(a.width) * 3) % 4 == 0) &&
                            (a.in_frame_stride % 4 == 0);
         timing_mark(kIdPrePass, 0, s);
-        shear_kernel<<<grid, 256, 0, s>>>(a, S, sg, vec_ok, (SPARSE && OPC_SKEW_KEY) ? 1 : 0);
+        shear_kernel<<<grid, 256, 0, s>>>(a, S, sg, vec_ok, (SPARSE && OPC_SKEW_KEY) ? 1 : 0, bmask);
         timing_mark(kIdPrePass, 1, s);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -726,7 +811,8 @@ cudaError_t launch_nbs(const BandArgs& a, int* counter, void* scratch, int num_s
     if (e != cudaSuccess) return e;
     const Mul M = (SPARSE && OPC_SKEW_KEY) ? Mul{1u, 0xFFFFFFFFu, 4u, 1u} : Mul{16u, 0xFFFFFFF0u, 4u, 1u};
     timing_mark(kIdSkew, 0, s);
-    skew_kernel<NB, SL, SPARSE><<<static_cast<unsigned>(blocks), warps * 32, smem, s>>>(a, S, sg, counter, g, M);
+    skew_kernel<NB, SL, SPARSE><<<static_cast<unsigned>(blocks), warps * 32, smem, s>>>(a, S, sg, counter, g, M,
+                                                                                      bmask);
     timing_mark(kIdSkew, 1, s);
     return cudaGetLastError();
 }
@@ -758,7 +844,11 @@ bool skew_supported(int levels, int radius) {
 
 std::size_t skew_scratch_bytes(const BandArgs& a) {
     if (a.y_hi <= a.y_lo || a.x_hi <= a.x_lo) return 0;
-    return shear_geom(a).frame_elems * a.frames * sizeof(std::uint32_t);
+    const ShearGeom sg = shear_geom(a);
+    const std::size_t nbx = static_cast<std::size_t>(a.width + kShearPad + kShearCols - 1) / kShearCols *
+                            (kShearCols / 32);
+    const std::size_t table = static_cast<std::size_t>(a.frames) * (sg.Hs / kShearRows) * nbx;  // bin masks
+    return (sg.frame_elems * a.frames + table) * sizeof(std::uint32_t);
 }
 
 cudaError_t launch_skew(const BandArgs& a, int* task_counter, void* scratch, int num_sms,
