@@ -167,6 +167,37 @@ def test_skew_tie_heavy_content(gpu, content):
             assert np.array_equal(run(gpu, img, r, L, 0, COLUMN), want), (content, r, L)
 
 
+@pytest.mark.parametrize("L", [23, 30, 31])
+def test_skew_bin_groups_on_smooth_batches(gpu, L):
+    """KEY launches with >= 24 bins skip the bin groups a phase never sees
+    (block bin masks from the shear pre-pass): smooth ramps whose bin range
+    drifts across the frame and between frames, odd sizes, partial bands."""
+    rng = np.random.default_rng(L)
+    for (w, h, f) in ((333, 97, 3), (130, 517, 2), (1000, 40, 2)):
+        yy, xx = np.mgrid[0:h, 0:w]
+        frames = []
+        for k in range(f):
+            base = (xx * (2 + k) + yy * (3 - k)) % 256
+            img = np.stack([base, (base + 40 * k) % 256, (255 - base)], axis=-1)
+            img = np.clip(img + rng.integers(-6, 7, img.shape), 0, 255).astype(np.uint8)
+            frames.append(img)
+        batch = np.stack(frames)
+        torch = pytest.importorskip("torch")
+        dev_in = torch.from_numpy(batch).cuda()
+        dev_out = torch.empty_like(dev_in)
+        for r in (3, 7):
+            got = gpu.apply_cuda_batch(batch, gpu.FilterParams(r, L), gpu.CudaConfig(kernel=SKEW))
+            # one launch over all frames (the per-frame bin-mask tables)
+            gpu.apply_cuda_device(dev_in.data_ptr(), dev_out.data_ptr(), w, h, gpu.FilterParams(r, L),
+                                  gpu.CudaConfig(device=0, kernel=SKEW), frames=f)
+            torch.cuda.synchronize()
+            dgot = dev_out.cpu().numpy()
+            for k in range(f):
+                want = oracle_lib.oracle_filter(batch[k], r, L, 0, threads=4)
+                assert np.array_equal(got[k], want), (w, h, k, r, L)
+                assert np.array_equal(dgot[k], want), (w, h, k, r, L, "device batch")
+
+
 def test_large_radius_and_l256(gpu):
     rng = np.random.default_rng(9)
     for r, L in ((16, 20), (20, 5), (31, 255), (12, 256), (3, 256)):
