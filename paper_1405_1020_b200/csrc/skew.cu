@@ -160,9 +160,14 @@ __global__ void __launch_bounds__(256)
         const int j = warp >> 1;
         std::uint32_t m = 0;
 #pragma unroll
+        // (pixels of the pad columns and of rows past the input are not in
+        // any output window: left out)
+        const bool col_ok = x0 + 32 * j + lane < a.width;
+#pragma unroll
         for (int rr = 0; rr < 16; ++rr) {
-            const std::uint32_t e = tile[((warp & 1) * 16 + rr) * kShearStride + 32 * j + lane];
-            m |= 1u << (key ? e >> 24 : e >> 26);
+            const int row = (warp & 1) * 16 + rr;
+            const std::uint32_t e = tile[row * kShearStride + 32 * j + lane];
+            if (col_ok && y0 + row < in_hi) m |= 1u << (key ? e >> 24 : e >> 26);
         }
         m = __reduce_or_sync(0xFFFFFFFFu, m);
         if (lane == 0) wm[warp] = m;
@@ -296,7 +301,7 @@ __device__ __forceinline__ void pick_if_ge(std::uint32_t& lo, std::uint32_t& hi,
 // (31 - bin) field selects the lo word through a 5-level multiplexer.
 template <int NB>
 __device__ __forceinline__ std::uint32_t winner_rgb_key(const unsigned long long (&w)[NB],
-                                                        const std::uint32_t* recip) {
+                                                        const std::uint32_t* recip, int base = 0) {
     std::uint32_t mx[NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b) mx[b] = static_cast<std::uint32_t>(w[b] >> 32);
@@ -309,7 +314,7 @@ __device__ __forceinline__ std::uint32_t winner_rgb_key(const unsigned long long
         }
     }
     const std::uint32_t hi = mx[0];
-    const std::uint32_t best = 31u - ((hi >> 16) & 31u);
+    const std::uint32_t best = 31u - ((hi >> 16) & 31u) - static_cast<std::uint32_t>(base);
     std::uint32_t v[NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b) v[b] = static_cast<std::uint32_t>(w[b]);
@@ -436,7 +441,11 @@ struct Task {
     int y_rows;               // valid rows in the band (<= 32)
     std::size_t stride;
     std::uint32_t gm;         // bin groups (8 bins each) the current phase touches (GROUPED steps)
+    int base;                 // windowed passes: bin of win[0]
 };
+#ifndef OPC_SKEW_WINDOW
+#define OPC_SKEW_WINDOW 16  // KEY launches with NB >= 24: window of bins kept per pass when every phase fits (0 = off)
+#endif
 #ifndef OPC_SKEW_GROUPS
 #define OPC_SKEW_GROUPS 1  // KEY launches with NB >= 24: skip the E rows of bin groups a phase never sees
 #endif
@@ -496,9 +505,9 @@ __device__ __forceinline__ void prefetch_l2(const Task& T, int s) {
 // active lanes fit one half-warp and the init accesses take half the
 // shared-memory wavefronts); otherwise all lanes run it masked (no divergence;
 // measured 13% faster for r = 15).
-template <int NB, int SL, bool SPARSE, bool EDGE>
+template <int NB, int SL, bool SPARSE, bool EDGE, int NW = NB>
 __device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
-                                     unsigned long long (&win)[NB], unsigned long long* E,
+                                     unsigned long long (&win)[NW], unsigned long long* E,
                                      std::uint32_t* stage, const std::uint32_t* recip) {
     constexpr bool KEY = SPARSE && OPC_SKEW_KEY;
     const int t = T.lane;
@@ -524,8 +533,19 @@ __device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
         // GROUPED: E rows of bin groups the phase's pixels never reach are
         // zero for every column of the phase: neither read nor added (the
         // winner first, then each active group's rows loaded and added).
-        constexpr bool GROUPED = KEY && NB >= 24 && OPC_SKEW_GROUPS && !EDGE;
-        if constexpr (GROUPED) {
+        constexpr bool WIN = NW < NB;  // windowed pass: win[k] is bin T.base + k
+        constexpr bool GROUPED = KEY && NB >= 24 && OPC_SKEW_GROUPS && !EDGE && !WIN;
+        if constexpr (WIN) {
+            unsigned long long e[NW];
+            const unsigned long long* Eb = E + T.base * SL + slot;
+#pragma unroll
+            for (int k = 0; k < NW; ++k) e[k] = Eb[k * SL];
+            if (!EDGE || (v >= w2 && t < T.y_rows)) {
+                stage[t * kStageStride + (v & 31)] = winner_rgb_key<NW>(win, recip, T.base);
+            }
+#pragma unroll
+            for (int k = 0; k < NW; ++k) win[k] += e[k];
+        } else if constexpr (GROUPED) {
             stage[t * kStageStride + (v & 31)] = winner_rgb_key<NB>(win, recip);
             constexpr int GS = OPC_SKEW_GROUP_BINS;
 #pragma unroll
@@ -612,16 +632,17 @@ __device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
 // the lanes' E columns v in [s0 - 31, s0 + 31] hold column histograms of image
 // columns [xs - r + v - w2, xs - r + v], rows [yb - r, yb + 31 + r]; the OR of
 // the shear pre-pass's 32 x 32 block bin masks over that region.
-__device__ __forceinline__ std::uint32_t phase_groups(const BandArgs& a, const ShearGeom& sg,
-                                                      const std::uint32_t* bmask, int f, int yb, int xs,
-                                                      int s0, int w2, int lane) {
+__device__ __forceinline__ std::uint32_t phase_bins(const BandArgs& a, const ShearGeom& sg,
+                                                    const std::uint32_t* bmask, int f, int yb, int xs,
+                                                    int s0, int w2, int lane) {
     const int r = a.radius;
     const int nty = sg.Hs / kShearRows;
     const int nbx = (a.width + kShearPad + kShearCols - 1) / kShearCols * (kShearCols / 32);
     const int ty0 = (yb - r - sg.y_base) >> 5;
     const int ty1 = min(nty - 1, (yb + 31 + r - sg.y_base) >> 5);
     const int c0 = max(0, xs - r + s0 - 31 - w2);
-    const int c1 = min(a.width + kShearPad - 1, xs - r + s0 + 31);
+    const int c1 = min(a.width - 1, xs - r + s0 + 31);
+    if (c1 < c0) return 0u;  // no image column in the phase yet
     const int bx0 = c0 >> 5, bx1 = max(bx0, c1 >> 5);
     const int nx = bx1 - bx0 + 1;
     std::uint32_t m = 0;
@@ -629,13 +650,122 @@ __device__ __forceinline__ std::uint32_t phase_groups(const BandArgs& a, const S
         const int ty = ty0 + lane / nx, bx = bx0 + lane % nx;
         m = bmask[(static_cast<std::size_t>(f) * nty + ty) * nbx + bx];
     }
-    m = __reduce_or_sync(0xFFFFFFFFu, m);
+    return __reduce_or_sync(0xFFFFFFFFu, m);
+}
+__device__ __forceinline__ std::uint32_t phase_groups(const BandArgs& a, const ShearGeom& sg,
+                                                      const std::uint32_t* bmask, int f, int yb, int xs,
+                                                      int s0, int w2, int lane) {
+    const std::uint32_t m = phase_bins(a, sg, bmask, f, yb, xs, s0, w2, lane);
     constexpr int GS = OPC_SKEW_GROUP_BINS;
     constexpr std::uint32_t gmask = (1u << GS) - 1u;
     std::uint32_t gm = 0;
 #pragma unroll
     for (int g8 = 0; g8 < 32 / GS; ++g8) gm |= ((m >> (GS * g8)) & gmask) ? 1u << g8 : 0u;
     return gm;
+}
+
+// One pass (band kb of frame f, columns [0, NV)) of a warp; Task set up by the
+// caller.  NW < NB: windowed pass (KEY layout) -- win[k] holds bin T.base + k.
+template <int NB, int SL, bool SPARSE, int NW>
+__device__ __forceinline__ void run_pass(Task& T, const BandArgs& a, const ShearGeom& sg,
+                                         const std::uint32_t* bmask, int f, int yb, int xs,
+                                         unsigned long long* E, std::uint32_t* stage,
+                                         const std::uint32_t* recip, int base0) {
+    constexpr bool WIN = NW < NB;
+    unsigned long long win[NW];
+    if constexpr (WIN) T.base = base0;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) {
+        const int b = (WIN ? base0 : 0) + k;
+        win[k] = (SPARSE && OPC_SKEW_KEY) ? static_cast<unsigned long long>(31 - b) << 48 : 0ull;
+    }
+    for (int i = T.lane; i < NB * SL; i += 32) E[i] = 0ull;
+    __syncwarp();
+
+    const int nphases = ((T.NV - 1) >> 5) + 2;
+    // steady: every lane past warm-up and every flushed column valid
+    // From phase p on every step is steady: all lanes past warm-up
+    // (s - 31 >= w2 from s = 32p) and every flushed column valid
+    // (32p - 32 >= w2): 32p >= w2 + 32.
+    const int p_steady_lo = (T.w2 + 32 + 31) >> 5;
+    // The first init row (column 0, lane 0) is added at step -w2: phase -1
+    // starts there.  (Slots the skipped steps would clear are still zero.)
+    Loads cur = fetch<true>(T, -T.w2);
+    for (int p = -1; p < nphases; ++p) {
+        if constexpr (WIN) {
+            // keep the phase's bins inside the window [base, base + NW): the
+            // pass was admitted because every phase's range fits; words
+            // shifted out hold no pixel (the phase region contains every
+            // lane's window)
+            const std::uint32_t m = phase_bins(a, sg, bmask, f, yb, xs, 32 * p, T.w2, T.lane);
+            if (m) {
+                const int lo = __ffs(m) - 1, hi = 31 - __clz(m);
+                if (lo < T.base || hi >= T.base + NW) {
+                    int nb = lo - (NW - (hi - lo + 1)) / 2;
+                    nb = max(0, min(nb, NB - NW));
+                    while (T.base < nb) {
+#pragma unroll
+                        for (int k = 0; k + 1 < NW; ++k) win[k] = win[k + 1];
+                        win[NW - 1] = static_cast<unsigned long long>(31 - (T.base + NW)) << 48;
+                        ++T.base;
+                    }
+                    while (T.base > nb) {
+#pragma unroll
+                        for (int k = NW - 1; k > 0; --k) win[k] = win[k - 1];
+                        win[0] = static_cast<unsigned long long>(31 - (T.base - 1)) << 48;
+                        --T.base;
+                    }
+                }
+            }
+        }
+        // (A partial last band runs the steady path too: its rows past
+        // y_rows read valid plane rows and are never flushed.)
+        const bool steady = p >= p_steady_lo && 32 * p + 31 < T.NV;
+        if (steady) {
+            if constexpr (!WIN && SPARSE && OPC_SKEW_KEY && NB >= 24 && OPC_SKEW_GROUPS) {
+                T.gm = phase_groups(a, sg, bmask, f, yb, xs, 32 * p, T.w2, T.lane);
+            }
+            // Loads run two steps ahead; the diagonal first touched eight
+            // steps ahead (the init column's) is pulled into L2 now.
+            // Global loads run kLook steps ahead of their use (3 for NB <= 21:
+            // 1% faster on C4; 2 for more bins, where the registers run out).
+            constexpr int kLook = NB <= OPC_SKEW_LOOK3_MAXNB ? OPC_SKEW_LOOKAHEAD : 2;
+            Loads n1 = fetch<false>(T, 32 * p + 1);
+            Loads n2{};
+            if constexpr (kLook >= 3) n2 = fetch<false>(T, 32 * p + 2);
+#pragma unroll 1
+            for (int ss = 0; ss < 32; ss += 2) {
+                const int s = 32 * p + ss;
+                if (OPC_SKEW_PF_DIST > 0) prefetch_l2(T, s + OPC_SKEW_PF_DIST);
+                if constexpr (kLook >= 3) {
+                    const Loads n3 = fetch<false>(T, s + 3);
+                    step<NB, SL, SPARSE, false, NW>(T, s, cur, win, E, stage, recip);
+                    if (OPC_SKEW_PF_DIST > 0) prefetch_l2(T, s + OPC_SKEW_PF_DIST + 1);
+                    const Loads n4 = fetch<false>(T, s + 4);
+                    step<NB, SL, SPARSE, false, NW>(T, s + 1, n1, win, E, stage, recip);
+                    cur = n2;
+                    n1 = n3;
+                    n2 = n4;
+                } else {
+                    const Loads m2 = fetch<false>(T, s + 2);
+                    step<NB, SL, SPARSE, false, NW>(T, s, cur, win, E, stage, recip);
+                    if (OPC_SKEW_PF_DIST > 0) prefetch_l2(T, s + OPC_SKEW_PF_DIST + 1);
+                    const Loads m3 = fetch<false>(T, s + 3);
+                    step<NB, SL, SPARSE, false, NW>(T, s + 1, n1, win, E, stage, recip);
+                    cur = m2;
+                    n1 = m3;
+                }
+            }
+        } else {
+#pragma unroll 1
+            for (int ss = p < 0 ? 32 - T.w2 : 0; ss < 32; ++ss) {
+                const int s = 32 * p + ss;
+                const Loads nxt = fetch<true>(T, s + 1);
+                step<NB, SL, SPARSE, true, NW>(T, s, cur, win, E, stage, recip);
+                cur = nxt;
+            }
+        }
+    }
 }
 
 template <int NB, int SL, bool SPARSE>
@@ -687,72 +817,27 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
         T.Sf = S + sg.frame_elems * f;
         T.o0 = D0 * T.Hs + R0;
 
-        unsigned long long win[NB];
-#pragma unroll
-        for (int b = 0; b < NB; ++b) {
-            win[b] = (SPARSE && OPC_SKEW_KEY) ? static_cast<unsigned long long>(31 - b) << 48 : 0ull;
-        }
-        for (int i = lane; i < NB * SL; i += 32) E[i] = 0ull;
-        __syncwarp();
-
-        const int nphases = ((T.NV - 1) >> 5) + 2;
-        // steady: every lane past warm-up and every flushed column valid
-        // From phase p on every step is steady: all lanes past warm-up
-        // (s - 31 >= w2 from s = 32p) and every flushed column valid
-        // (32p - 32 >= w2): 32p >= w2 + 32.
-        const int p_steady_lo = (T.w2 + 32 + 31) >> 5;
-        // The first init row (column 0, lane 0) is added at step -w2: phase -1
-        // starts there.  (Slots the skipped steps would clear are still zero.)
-        Loads cur = fetch<true>(T, -T.w2);
-        for (int p = -1; p < nphases; ++p) {
-            // (A partial last band runs the steady path too: its rows past
-            // y_rows read valid plane rows and are never flushed.)
-            const bool steady = p >= p_steady_lo && 32 * p + 31 < T.NV;
-            if (steady) {
-                if constexpr (SPARSE && OPC_SKEW_KEY && NB >= 24 && OPC_SKEW_GROUPS) {
-                    T.gm = phase_groups(a, sg, bmask, f, yb, xs, 32 * p, T.w2, lane);
-                }
-                // Loads run two steps ahead; the diagonal first touched eight
-                // steps ahead (the init column's) is pulled into L2 now.
-                // Global loads run kLook steps ahead of their use (3 for NB <= 21:
-                // 1% faster on C4; 2 for more bins, where the registers run out).
-                constexpr int kLook = NB <= OPC_SKEW_LOOK3_MAXNB ? OPC_SKEW_LOOKAHEAD : 2;
-                Loads n1 = fetch<false>(T, 32 * p + 1);
-                Loads n2{};
-                if constexpr (kLook >= 3) n2 = fetch<false>(T, 32 * p + 2);
-#pragma unroll 1
-                for (int ss = 0; ss < 32; ss += 2) {
-                    const int s = 32 * p + ss;
-                    if (OPC_SKEW_PF_DIST > 0) prefetch_l2(T, s + OPC_SKEW_PF_DIST);
-                    if constexpr (kLook >= 3) {
-                        const Loads n3 = fetch<false>(T, s + 3);
-                        step<NB, SL, SPARSE, false>(T, s, cur, win, E, stage, recip);
-                        if (OPC_SKEW_PF_DIST > 0) prefetch_l2(T, s + OPC_SKEW_PF_DIST + 1);
-                        const Loads n4 = fetch<false>(T, s + 4);
-                        step<NB, SL, SPARSE, false>(T, s + 1, n1, win, E, stage, recip);
-                        cur = n2;
-                        n1 = n3;
-                        n2 = n4;
-                    } else {
-                        const Loads m2 = fetch<false>(T, s + 2);
-                        step<NB, SL, SPARSE, false>(T, s, cur, win, E, stage, recip);
-                        if (OPC_SKEW_PF_DIST > 0) prefetch_l2(T, s + OPC_SKEW_PF_DIST + 1);
-                        const Loads m3 = fetch<false>(T, s + 3);
-                        step<NB, SL, SPARSE, false>(T, s + 1, n1, win, E, stage, recip);
-                        cur = m2;
-                        n1 = m3;
-                    }
-                }
-            } else {
-#pragma unroll 1
-                for (int ss = p < 0 ? 32 - T.w2 : 0; ss < 32; ++ss) {
-                    const int s = 32 * p + ss;
-                    const Loads nxt = fetch<true>(T, s + 1);
-                    step<NB, SL, SPARSE, true>(T, s, cur, win, E, stage, recip);
-                    cur = nxt;
-                }
+        constexpr bool kWinOk = SPARSE && OPC_SKEW_KEY && NB >= 24 && OPC_SKEW_GROUPS &&
+                                OPC_SKEW_WINDOW > 0 && OPC_SKEW_WINDOW < NB;
+        if constexpr (kWinOk) {
+            // Windowed pass when every phase's bin range fits the window.
+            const int nph = ((T.NV - 1) >> 5) + 2;
+            bool fits = true;
+            int base0 = -1;
+            for (int p = -1; p < nph && fits; ++p) {
+                const std::uint32_t m = phase_bins(a, sg, bmask, f, yb, xs, 32 * p, T.w2, lane);
+                if (!m) continue;
+                const int lo = __ffs(m) - 1, hi = 31 - __clz(m);
+                fits = hi - lo < OPC_SKEW_WINDOW;
+                if (base0 < 0) base0 = max(0, min(lo - (OPC_SKEW_WINDOW - (hi - lo + 1)) / 2, NB - OPC_SKEW_WINDOW));
+            }
+            if (fits) {
+                run_pass<NB, SL, SPARSE, (kWinOk ? OPC_SKEW_WINDOW : NB)>(T, a, sg, bmask, f, yb, xs, E, stage,
+                                                                            recip, max(base0, 0));
+                continue;
             }
         }
+        run_pass<NB, SL, SPARSE, NB>(T, a, sg, bmask, f, yb, xs, E, stage, recip, 0);
     }
 }
 
