@@ -449,6 +449,12 @@ struct Task {
 #ifndef OPC_SKEW_GROUPS
 #define OPC_SKEW_GROUPS 1  // KEY launches with NB >= 24: skip the E rows of bin groups a phase never sees
 #endif
+#ifndef OPC_SKEW_GROUPS_MIN_NB
+#define OPC_SKEW_GROUPS_MIN_NB 24
+#endif
+#ifndef OPC_SKEW_WINDOW_MIN_NB
+#define OPC_SKEW_WINDOW_MIN_NB 24
+#endif
 #ifndef OPC_SKEW_GROUP_BINS
 #define OPC_SKEW_GROUP_BINS 8  // bins per group (4, 8 or 16)
 #endif
@@ -534,7 +540,7 @@ __device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
         // zero for every column of the phase: neither read nor added (the
         // winner first, then each active group's rows loaded and added).
         constexpr bool WIN = NW < NB;  // windowed pass: win[k] is bin T.base + k
-        constexpr bool GROUPED = KEY && NB >= 24 && OPC_SKEW_GROUPS && !EDGE && !WIN;
+        constexpr bool GROUPED = KEY && NB >= OPC_SKEW_GROUPS_MIN_NB && OPC_SKEW_GROUPS && !EDGE && !WIN;
         if constexpr (WIN) {
             unsigned long long e[NW];
             const unsigned long long* Eb = E + T.base * SL + slot;
@@ -722,7 +728,7 @@ __device__ __forceinline__ void run_pass(Task& T, const BandArgs& a, const Shear
         // y_rows read valid plane rows and are never flushed.)
         const bool steady = p >= p_steady_lo && 32 * p + 31 < T.NV;
         if (steady) {
-            if constexpr (!WIN && SPARSE && OPC_SKEW_KEY && NB >= 24 && OPC_SKEW_GROUPS) {
+            if constexpr (!WIN && SPARSE && OPC_SKEW_KEY && NB >= OPC_SKEW_GROUPS_MIN_NB && OPC_SKEW_GROUPS) {
                 T.gm = phase_groups(a, sg, bmask, f, yb, xs, 32 * p, T.w2, T.lane);
             }
             // Loads run two steps ahead; the diagonal first touched eight
@@ -817,7 +823,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
         T.Sf = S + sg.frame_elems * f;
         T.o0 = D0 * T.Hs + R0;
 
-        constexpr bool kWinOk = SPARSE && OPC_SKEW_KEY && NB >= 24 && OPC_SKEW_GROUPS &&
+        constexpr bool kWinOk = SPARSE && OPC_SKEW_KEY && NB >= OPC_SKEW_WINDOW_MIN_NB && OPC_SKEW_GROUPS &&
                                 OPC_SKEW_WINDOW > 0 && OPC_SKEW_WINDOW < NB;
         if constexpr (kWinOk) {
             // Windowed pass when every phase's bin range fits the window.
@@ -861,7 +867,8 @@ cudaError_t launch_nbs(const BandArgs& a, int* counter, void* scratch, int num_s
     std::uint32_t* S = static_cast<std::uint32_t*>(scratch);
     // block bin-mask table (GROUPED launches), after the plane
     std::uint32_t* bmask = nullptr;
-    if constexpr (SPARSE && OPC_SKEW_KEY && NB >= 24 && OPC_SKEW_GROUPS) {
+    if constexpr (SPARSE && OPC_SKEW_KEY && OPC_SKEW_GROUPS &&
+                  (NB >= OPC_SKEW_GROUPS_MIN_NB || NB >= OPC_SKEW_WINDOW_MIN_NB)) {
         bmask = S + sg.frame_elems * a.frames;
     }
     {
