@@ -7,10 +7,12 @@ Workload (config.workload): BASELINE.json's large-radius configuration, the one
 the north-star target is quoted on -- config 4, 16384x16384 uniform-noise RGB8,
 r=15, L=20, CopyInput (the other four configs are parity-test cases;
 --config selects them for manual runs).  A "step" is one pass of the filter over
-the whole image.  N>1 (torchrun, one process per GPU): the image's rows are
-split into N contiguous bands with r-row halos; every rank filters
-its band; no collective on the data path (NCCL is used only for the barrier and
-the max-over-ranks timing).
+the whole image.  N>1: one process per GPU (under torchrun, or -- when
+WORLD_SIZE is unset -- bench.py re-launches itself under torch.distributed.run
+with N ranks); the image's rows are split into N contiguous bands with r-row
+halos, every rank generates and filters only its own band; no
+collective on the data path (NCCL is used only for the barrier, the
+max-over-ranks timing and the per-rank report).
 
 Reported:
   value     output MP/s of the whole job, device-resident inputs, timed with CUDA
@@ -24,12 +26,18 @@ Reported:
             beside it.
   cpu_baseline  the unmodified reference library (oracle/_ref, apply_parallel's
             row-band engine) on all host cores of the box, on a bounded band of
-            the same image.
+            the same image (rank 0's band; every N, every config).
+
+--impl reference: the reference's own CPU engine on the same workload, metric
+and config (rank 0 only).  That arm loads only oracle/_ref (the reference
+library built from its sources, plus the harness generators of configs 2/3/5):
+it never imports paper_1405_1020_b200 or maps liboilpaint_b200.so; the
+workload table is read from paper_1405_1020_b200/workloads.py by file path.
 """
 from __future__ import annotations
 
 import argparse
-import ctypes
+import importlib.util
 import json
 import os
 import statistics
@@ -44,8 +52,23 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+METRIC = "output megapixels/sec at radius r, levels L (1/2/4/8 B200) and % of roofline"
+
+
+def load_workloads() -> dict:
+    """paper_1405_1020_b200/workloads.py by file path (plain data: no package
+    import, no library load)."""
+    name = "_opc_workloads"
+    if name not in sys.modules:
+        spec = importlib.util.spec_from_file_location(
+            name, ROOT / "paper_1405_1020_b200" / "workloads.py")
+        mod = importlib.util.module_from_spec(spec)
+        sys.modules[name] = mod
+        spec.loader.exec_module(mod)
+    return sys.modules[name].WORKLOADS
+
+
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}
-NUM_SMS_B200 = 148
 
 
 def load_peaks() -> tuple[dict, str]:
@@ -144,8 +167,9 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------
-# CPU legs: the reference library (oracle/_ref) or, if it was not built, the
-# C restatement (oracle/).  Used only for cpu_baseline and --impl reference.
+# CPU legs (TEST INFRASTRUCTURE as the checker / baseline): the reference
+# library (oracle/_ref) or, if it was not built, the C restatement (oracle/).
+# Used only for cpu_baseline and --impl reference.
 # ----------------------------------------------------------------------------
 
 def host_threads() -> int:
@@ -166,6 +190,10 @@ def cpu_model() -> str:
 
 
 class CpuEngine:
+    """The reference engine body (parallel_for_rows + filter_pixel, the engine
+    of apply_parallel, proj/src/parallel.cpp:110-132) from oracle/_ref, or the
+    oracle's C port when oracle/_ref is absent."""
+
     def __init__(self):
         sys.path.insert(0, str(ROOT / "tests"))
         import oracle_lib
@@ -177,8 +205,31 @@ class CpuEngine:
             self.kind = "port"
             self.oracle = oracle_lib.oracle()
 
+    def generate_rows(self, wl, nrows: int, frame: int = 0) -> np.ndarray:
+        """Rows [0, nrows) of the workload's input (frame `frame`): the
+        reference generator (proj/src/pattern.cpp:64-76, Noise{seed}) for the
+        noise configs, the harness generators in oracle/_ref for the others."""
+        out = np.empty((nrows, wl.width, 3), np.uint8)
+        if wl.pattern == 0:
+            # Noise: byte i = byte (i mod 8) of stream word i / 8 -- the first
+            # nrows rows of the W x H image are the W x nrows image
+            if self.ref is not None:
+                rc = self.ref.ref_generate(0, wl.seed, wl.width, nrows, out.ctypes.data)
+                assert rc == 0, self.ref.ref_last_error()
+            else:
+                self.oracle.oracle_noise(wl.seed, out.ctypes.data, out.size)
+            return out
+        if self.ref is None:
+            raise RuntimeError(f"{wl.name}: its generator lives in oracle/_ref, which is not built")
+        rc = self.ref.ref_harness_generate_rows(wl.pattern, wl.seed, wl.width, wl.height, frame, 0,
+                                                nrows, out.ctypes.data, 0)
+        assert rc == 0
+        return out
+
     def band(self, img: np.ndarray, out: np.ndarray, radius: int, levels: int, y0: int, y1: int,
              threads: int) -> None:
+        """Interior rows [y0, y1) of the image `img` (all of whose rows are
+        given) into the same rows of `out`."""
         h, w, _ = img.shape
         if self.ref is not None:
             rc = self.ref.ref_filter_band(img.ctypes.data, out.ctypes.data, w, h, radius, levels,
@@ -192,88 +243,78 @@ class CpuEngine:
             assert rc == 0
             out[y0:y1] = tmp[radius:radius + (y1 - y0)]
 
-    def calibrate_rows(self, img, out, cfg, threads, target_s) -> tuple[int, float]:
-        """Rows of the image whose filtering takes about target_s on `threads`
-        threads: probe with >= 4 rows per thread, grow until the probe takes
-        >= 0.5 s, then scale."""
-        r = cfg.radius
-        interior = cfg.height - 2 * r
-        rows = max(1, min(interior, 4 * threads))
+
+class CpuSample:
+    """A bounded sample of the workload for the CPU engine: interior rows
+    [r, r + rows) of an image whose first rows are `src` (a rank's band, or
+    rows generated by CpuEngine), full width -- rows chosen so one run takes
+    about target_s on `threads` threads."""
+
+    def __init__(self, eng: CpuEngine, wl, threads: int, target_s: float, src=None):
+        self.eng, self.wl, self.threads = eng, wl, threads
+        r = wl.radius
+        self.max_rows = (src.shape[0] if src is not None else wl.height) - 2 * r
+        self.src = src
+        rows = max(1, min(self.max_rows, 4 * threads))
         while True:
             t = time.perf_counter()
-            self.band(img, out, r, cfg.levels, r, r + rows, threads)
+            self._run(rows)
             dt = time.perf_counter() - t
-            if dt >= 0.5 or rows >= interior:
+            if dt >= 0.5 or rows >= self.max_rows:
                 break
-            rows = min(interior, rows * 4)
+            rows = min(self.max_rows, rows * 4)
         rate = rows / max(dt, 1e-6)
-        want = int(max(1, min(interior, rate * target_s)))
-        return want, rate
+        self.rows = int(max(1, min(self.max_rows, rate * target_s)))
+        self._image(self.rows)
 
+    def _image(self, rows: int) -> np.ndarray:
+        need = rows + 2 * self.wl.radius
+        if self.src is None or self.src.shape[0] < need:
+            self.src = self.eng.generate_rows(self.wl, min(self.wl.height, max(need, 64)))
+            self.out = np.zeros_like(self.src)
+        elif not hasattr(self, "out") or self.out.shape != self.src.shape:
+            self.out = np.zeros_like(self.src)
+        return self.src
 
-def cpu_sample_run(cfg, img, threads: int, target_s: float, steps: int = 1, warmup: int = 0):
-    """Times the reference engine on a bounded band of rows of the bench image."""
-    eng = CpuEngine()
-    out = np.zeros_like(img)
-    rows, _ = eng.calibrate_rows(img, out, cfg, threads, target_s)
-    y0 = cfg.radius
-    for _ in range(warmup):
-        eng.band(img, out, cfg.radius, cfg.levels, y0, y0 + rows, threads)
-    times = []
-    for _ in range(steps):
+    def _run(self, rows: int) -> None:
+        img = self._image(rows)
+        r = self.wl.radius
+        self.eng.band(img, self.out, r, self.wl.levels, r, r + rows, self.threads)
+
+    def run(self) -> float:
         t = time.perf_counter()
-        eng.band(img, out, cfg.radius, cfg.levels, y0, y0 + rows, threads)
-        times.append(time.perf_counter() - t)
-    mp = rows * cfg.width / 1e6  # output megapixels of the sample (rows x full width)
-    return eng.kind, rows, mp, times
+        self._run(self.rows)
+        return time.perf_counter() - t
+
+    @property
+    def megapixels(self) -> float:
+        return self.rows * self.wl.width / 1e6  # output MP: rows x full width
+
+    def describe(self, seconds: float) -> str:
+        r = self.wl.radius
+        what = ("reference apply_parallel row-band engine (parallel_for_rows + filter_pixel)"
+                if self.eng.kind == "reference" else "C port of the reference engine")
+        frame = " (frame 0)" if self.wl.frames > 1 else ""
+        return (f"rows [{r}, {r + self.rows}) x {self.wl.width} cols of the {self.wl.name} "
+                f"image{frame} per run ({self.megapixels:.2f} MP, {seconds:.2f} s), {what}, "
+                f"{self.threads} threads, {cpu_model()}")
 
 
-def reference_arm(args, cfg) -> None:
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
-    img = cfg.generate(0)
-    threads = host_threads()
-    step_s = float(os.environ.get("OILPAINT_REF_STEP_S", "4"))
-    kind, rows, mp, times = cpu_sample_run(cfg, img, threads, step_s, args.steps, args.warmup)
-    total = sum(times)
-    value = mp * len(times) / total
-    line = {
-        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "MP/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(1000 * total / len(times), 3), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": workload_config(cfg, args.gpus),
-        "cpu_baseline": {"value": round(value, 4), "unit": "MP/s", "cores": threads, "kind": kind,
-                         "sample": f"rows [{cfg.radius}, {cfg.radius + rows}) x {cfg.width} cols "
-                                   f"of the {cfg.name} image per step ({mp:.2f} MP), "
-                                   f"{'apply_parallel row-band engine (parallel_for_rows + filter_pixel)' if kind == 'reference' else 'C port'}, "
-                                   f"{threads} threads, {cpu_model()}"},
-        "e2e": {"value": round(value, 4), "unit": "MP/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
+def workload_config(wl, n: int) -> dict:
+    return {"workload": f"{wl.name}: {wl.description}", "width": wl.width,
+            "height": wl.height, "frames": wl.frames, "radius": wl.radius,
+            "levels": wl.levels, "border": "CopyInput", "partition":
+            ("frames" if wl.frames > 1 else "row bands with r-row halos") + f" over {n} GPU(s)",
+            "l2": l2_note(rank0_in_bytes(wl, n))}
 
 
-METRIC = "output megapixels/sec at radius r, levels L (1/2/4/8 B200) and % of roofline"
-
-
-def rank0_in_bytes(cfg, n: int) -> int:
+def rank0_in_bytes(wl, n: int) -> int:
     """Input bytes of rank 0 of an n-GPU run (its row band plus halos, or its frames)."""
-    W, H, F = cfg.width, cfg.height, cfg.frames
+    W, H, F = wl.width, wl.height, wl.frames
     if F == 1:
-        from paper_1405_1020_b200 import band_input_rows
-        lo, hi = band_input_rows(H, 0, H // n, cfg.radius)
-        return (hi - lo) * W * 3
+        y1 = H // n
+        return (min(H, y1 + wl.radius) - 0) * W * 3
     return (F // n) * H * W * 3
-
-
-def workload_config(cfg, n: int, in_bytes: int | None = None) -> dict:
-    return {"workload": f"{cfg.name}: {cfg.description}", "width": cfg.width,
-            "height": cfg.height, "frames": cfg.frames, "radius": cfg.radius,
-            "levels": cfg.levels, "border": "CopyInput", "partition":
-            ("frames" if cfg.frames > 1 else "row bands with r-row halos") + f" over {n} GPU(s)",
-            "l2": l2_note(rank0_in_bytes(cfg, n) if in_bytes is None else in_bytes)}
 
 
 def l2_note(in_bytes: int) -> str:
@@ -282,6 +323,50 @@ def l2_note(in_bytes: int) -> str:
     if mb >= 2 * 126:
         return f"input {mb:.0f} MiB per GPU > 126 MB L2 (no flush needed)"
     return f"input {mb:.1f} MiB per GPU < 2 x 126 MB L2: L2 flushed between timed steps (512 MiB memset, untimed)"
+
+
+def reference_arm(args, wl) -> None:
+    """--impl reference: the reference's own engine on the host cores, rank 0
+    only; loads oracle/_ref and nothing of the product."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = host_threads()
+    # each step a bounded sample; the whole run stays within about 2 minutes
+    step_s = float(os.environ.get("OILPAINT_REF_STEP_S",
+                                  min(4.0, 120.0 / max(1, args.steps + args.warmup))))
+    eng = CpuEngine()
+    sample = CpuSample(eng, wl, threads, step_s)
+    for _ in range(args.warmup):
+        sample.run()
+    times = [sample.run() for _ in range(args.steps)]
+    total = sum(times)
+    value = sample.megapixels * len(times) / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "MP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1000 * total / len(times), 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": workload_config(wl, args.gpus),
+        "cpu_baseline": {"value": round(value, 4), "unit": "MP/s", "cores": threads,
+                         "kind": eng.kind, "sample": sample.describe(total / len(times))},
+        "e2e": {"value": round(value, 4), "unit": "MP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def relaunch_under_torchrun(args) -> int:
+    """--gpus N > 1 without a torchrun environment: run this script as N ranks
+    (one process per GPU) under torch.distributed.run on 127.0.0.1."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main() -> None:
@@ -295,30 +380,47 @@ def main() -> None:
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
 
-    from paper_1405_1020_b200.patterns import CONFIGS
-    cfg = CONFIGS[args.config]
+    wl = load_workloads()[args.config]
     if args.impl == "reference":
-        reference_arm(args, cfg)
+        reference_arm(args, wl)
         return
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch_under_torchrun(args))
+    run_b200(args, wl)
 
+
+def run_b200(args, wl) -> None:
     import torch
     import torch.distributed as dist
     import paper_1405_1020_b200 as opc
     from paper_1405_1020_b200 import _lib
 
+    cfg = opc.CONFIGS[wl.name]
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: one process per "
+                         "GPU is required (launch with --nproc-per-node equal to --gpus)")
     # One process per GPU over NCCL.  OPC_BENCH_BACKEND=gloo with more ranks
     # than GPUs is a plumbing check only (ranks share devices; not a number
     # to report): the rank -> device map wraps around.
     backend = os.environ.get("OPC_BENCH_BACKEND", "nccl")
+    ndev = torch.cuda.device_count()
+    if backend == "nccl" and world > ndev:
+        raise SystemExit(f"bench.py: {world} ranks but {ndev} visible GPU(s)")
     if backend != "nccl":
-        local = local % torch.cuda.device_count()
+        local = local % ndev
     torch.cuda.set_device(local)
     if world > 1:
         if backend == "nccl":
+            # the communicator log (rank -> device, transport) goes to stderr
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
@@ -330,26 +432,28 @@ def main() -> None:
     ccfg = opc.CudaConfig(device=local, stream=stream.cuda_stream,
                           allow_levels_256=(L == 256))
 
-    # ---- this rank's share: row band (single image) or frames (batch) ----
+    # ---- this rank's share: row band (single image) or frames (batch); each
+    # rank generates only its own input rows / frames ----
     if F == 1:
-        y0, y1 = H * rank // world, H * (rank + 1) // world
+        y0, y1 = opc.band_begin(H, world, rank), opc.band_begin(H, world, rank + 1)
         lo, hi = opc.band_input_rows(H, y0, y1, r)
-        full = cfg.generate(0)
-        host_in = torch.from_numpy(np.ascontiguousarray(full[lo:hi])).pin_memory()
+        host_in = torch.empty((hi - lo, W, 3), dtype=torch.uint8).pin_memory()
+        cfg.generate_rows(lo, hi - lo, out=host_in.numpy())
         out_shape = (y1 - y0, W, 3)
         my_frames = 1
         out_pixels = (y1 - y0) * W
         interior = max(0, min(y1, H - r) - max(y0, r)) * (W - 2 * r)
+        share = {"rows": [y0, y1], "input_rows": [lo, hi]}
     else:
-        f0, f1 = F * rank // world, F * (rank + 1) // world
+        f0, f1 = opc.band_begin(F, world, rank), opc.band_begin(F, world, rank + 1)
         my_frames = f1 - f0
         host_in = torch.empty((my_frames, H, W, 3), dtype=torch.uint8).pin_memory()
         for i in range(my_frames):
             cfg.generate(f0 + i, out=host_in[i].numpy())
         out_shape = (my_frames, H, W, 3)
-        full = host_in[0].numpy()
         out_pixels = my_frames * H * W
         interior = my_frames * (H - 2 * r) * (W - 2 * r)
+        share = {"frames": [f0, f1]}
     dev_in = host_in.to(f"cuda:{local}")
     dev_out = torch.empty(out_shape, dtype=torch.uint8, device=f"cuda:{local}")
 
@@ -369,9 +473,10 @@ def main() -> None:
         step_device()
     stream.synchronize()
 
-    # Inputs smaller than twice the 126 MB L2 (configs 1-3): the L2 is flushed
-    # between timed steps (a 512 MB memset on the stream, outside the steps'
-    # event pairs), so every step reads its input from HBM.
+    # Inputs smaller than twice the 126 MB L2 (configs 1-3, and the bands of a
+    # wide split): the L2 is flushed between timed steps (a 512 MB memset on
+    # the stream, outside the steps' event pairs), so every step reads its
+    # input from HBM.
     flush = None
     if host_in.numel() < 2 * 126 * 2**20:
         flush = torch.empty(512 * 2**20, dtype=torch.uint8, device=f"cuda:{local}")
@@ -412,9 +517,9 @@ def main() -> None:
     pre_ms, _ = opc.kernel_timing_read(_lib.OPC_KID_PREPASS)
     border_ms, _ = opc.kernel_timing_read(_lib.OPC_KID_BORDER)
     opc.kernel_timing(False)
-    total_ms = ev[0].elapsed_time(ev[args.steps]) if flush is None else sum(step_ms)
+    my_total_ms = ev[0].elapsed_time(ev[args.steps]) if flush is None else sum(step_ms)
     red_dev = f"cuda:{local}" if backend == "nccl" else "cpu"
-    t = torch.tensor([total_ms], dtype=torch.float64, device=red_dev)
+    t = torch.tensor([my_total_ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
@@ -422,34 +527,43 @@ def main() -> None:
     job_pixels = F * W * H
     value = job_pixels / (ms_per_step / 1e3) / 1e6
 
-    # ---- end to end through the public C-ABI with pinned host buffers ----
-    host_out = torch.empty(out_shape, dtype=torch.uint8).pin_memory()
-    e2e_cfg = opc.CudaConfig(device=local, allow_levels_256=(L == 256))
+    # ---- end to end through the public C-ABI with host buffers ----
     import ctypes as _ct
     from paper_1405_1020_b200._lib import LIB
-    c_e2e = e2e_cfg.to_c()
+    host_out = torch.empty(out_shape, dtype=torch.uint8).pin_memory()
+    c_e2e = opc.CudaConfig(device=local, allow_levels_256=(L == 256)).to_c()
 
-    def step_e2e():
+    def step_e2e(src, dst):
         if F == 1:
-            rc = LIB.opc_filter_rgb8_band(host_in.data_ptr(), host_out.data_ptr(), W, H, y0, y1,
+            rc = LIB.opc_filter_rgb8_band(src.ctypes.data, dst.ctypes.data, W, H, y0, y1,
                                           r, L, 0, _ct.byref(c_e2e))
         else:
-            rc = LIB.opc_filter_rgb8_batch(host_in.data_ptr(), host_out.data_ptr(), my_frames, W,
+            rc = LIB.opc_filter_rgb8_batch(src.ctypes.data, dst.ctypes.data, my_frames, W,
                                            H, r, L, 0, _ct.byref(c_e2e))
         assert rc == 0, LIB.opc_last_error()
 
-    step_e2e()
-    barrier()
-    t0 = time.perf_counter()
-    for _ in range(args.e2e_steps):
-        step_e2e()
-    e2e_s = time.perf_counter() - t0
-    te = torch.tensor([e2e_s], dtype=torch.float64, device=red_dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = job_pixels * args.e2e_steps / float(te.item()) / 1e6
+    def time_e2e(src, dst) -> float:
+        step_e2e(src, dst)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            step_e2e(src, dst)
+        dt = time.perf_counter() - t0
+        te = torch.tensor([dt], dtype=torch.float64, device=red_dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        return job_pixels * args.e2e_steps / float(te.item()) / 1e6
+
+    e2e_value = time_e2e(host_in.numpy(), host_out.numpy())
     # the e2e output must equal the device-resident output
     assert torch.equal(host_out, dev_out.cpu()), "e2e output differs from device output"
+    # the same call from pageable buffers (a std::vector Image / numpy array):
+    # staged through the library's pinned ring
+    page_in = np.array(host_in.numpy(), copy=True)
+    page_out = np.empty(out_shape, np.uint8)
+    e2e_pageable = time_e2e(page_in, page_out)
+    assert np.array_equal(page_out, host_out.numpy()), "pageable e2e output differs"
+    del page_in, page_out
 
     # ---- roofline (issue-rate bound) ----
     peaks, peaks_kind = load_peaks()
@@ -464,19 +578,16 @@ def main() -> None:
     step_total_ms = sum(step_ms)
     traffic = None
     tp = ROOT / "profiles" / f"{cfg.name}_dram_bytes.json"
-    if tp.exists():
+    if tp.exists() and world == 1:
         traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
     hbm_gbs = float(peaks.get("hbm_gbs", 6650.0))
-    alg_bytes = 6 * out_pixels / max(1, 1)
+    alg_bytes = 6 * out_pixels
     roofline = {
         "bound": "issue", "achieved": round(achieved_ops / 1e12, 3),
         "peak": round(peak_ops / 1e12, 3), "unit": "Tlane-op/s",
         "frac": round(achieved_ops / peak_ops, 4), "traffic": traffic,
         "model": f"{model_name} {ops_px} lane-ops per interior pixel (SURVEY 8d best fit, B={L + 1}); "
-                 f"{num_sms} SMs x 4 x 32 x {sm_mhz:.0f} MHz ({peaks_kind} sm_max_mhz)"
-                 + ("; the slide kernel skips the updates of flat steps (no pixel of the "
-                    "entering column differs from the leaving one), which the model counts, so "
-                    "frac > 1 is possible on flat content" if family == 3 else ""),
+                 f"{num_sms} SMs x 4 x 32 x {sm_mhz:.0f} MHz ({peaks_kind} sm_max_mhz)",
         "algorithmic_ops_per_launch": ops_px * interior * args.steps // max(1, kernel_n),
         "kernel": {1: "direct", 2: "skew", 3: "slide", 4: "column"}.get(family, str(family)),
         "kernel_ms": round(kernel_ms, 4),
@@ -490,6 +601,17 @@ def main() -> None:
                 "frac": round(alg_bytes * args.steps / (step_total_ms / 1e3) / 1e9 / hbm_gbs, 4),
                 "bytes_per_launch": alg_bytes, "peak_kind": peaks_kind},
     }
+    if world > 1:
+        roofline["note"] = "rank 0's kernel and band; job value is max over ranks"
+
+    # ---- per-rank report (device, share, device time) ----
+    mine = {"rank": rank, "device": local, **share, "ms_per_step": round(my_total_ms / args.steps, 4),
+            "kernel_ms": round(kernel_ms, 4)}
+    if world > 1:
+        everyone = [None] * world
+        dist.all_gather_object(everyone, mine)
+    else:
+        everyone = [mine]
 
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "MP/s", "n_gpus": world,
@@ -498,21 +620,28 @@ def main() -> None:
         "data": "synthetic", "config": workload_config(cfg, world),
         "roofline": roofline,
         "e2e": {"value": round(e2e_value, 2), "unit": "MP/s",
-                "h2d_bytes_per_step": int(host_in.numel()),
-                "d2h_bytes_per_step": int(host_out.numel()),
+                "h2d_bytes_per_step": int(host_in.numel()) * world,
+                "d2h_bytes_per_step": int(host_out.numel()) * world,
                 "path": "opc_filter_rgb8_band / _batch (host pointers, pinned), "
-                        f"{args.e2e_steps} steps, wall clock, max over ranks"},
+                        f"{args.e2e_steps} steps, wall clock, max over ranks",
+                "pageable": {"value": round(e2e_pageable, 2), "unit": "MP/s",
+                             "path": "the same call from pageable numpy buffers (staged through "
+                                     "the library's pinned ring)"}},
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
+        "ranks": everyone,
+        "backend": backend if world > 1 else None,
     }
-    if rank == 0 and world == 1 and not args.no_cpu and F == 1:
+    if rank == 0 and not args.no_cpu:
         threads = host_threads()
-        kind, rows, mp, times = cpu_sample_run(cfg, full, threads, args.cpu_seconds)
-        line["cpu_baseline"] = {
-            "value": round(mp / times[0], 4), "unit": "MP/s", "cores": threads, "kind": kind,
-            "sample": f"rows [{r}, {r + rows}) x {W} cols of the {cfg.name} image "
-                      f"({mp:.2f} MP, {times[0]:.1f} s), reference apply_parallel row-band "
-                      f"engine on {threads} threads, {cpu_model()}"}
+        # rank 0's input: its band (rows [0, hi) of the image) or its first frame
+        src = host_in.numpy() if F == 1 else host_in[0].numpy()
+        eng = CpuEngine()
+        sample = CpuSample(eng, cfg, threads, args.cpu_seconds, src=src)
+        dt = sample.run()
+        line["cpu_baseline"] = {"value": round(sample.megapixels / dt, 4), "unit": "MP/s",
+                                "cores": threads, "kind": eng.kind,
+                                "sample": sample.describe(dt)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

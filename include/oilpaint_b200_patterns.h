@@ -31,6 +31,13 @@ extern "C" {
 int opc_generate(int32_t kind, uint64_t seed, int32_t width, int32_t height, int32_t frame,
                  uint8_t* out, int32_t threads);
 
+/* Rows [row0, row0 + nrows) of the same image (3*width*nrows bytes, the bytes
+ * opc_generate writes there): a rank of a row-band split generates only its
+ * band and halo rows.  Returns 0 or 1 (invalid argument / rows outside the
+ * image). */
+int opc_generate_rows(int32_t kind, uint64_t seed, int32_t width, int32_t height, int32_t frame,
+                      int32_t row0, int32_t nrows, uint8_t* out, int32_t threads);
+
 /* The same bytes written into DEVICE memory `d_out` (3*width*height bytes) on
  * `stream` (NULL: the library's stream of `device`; device < 0: current), for
  * every kind; OPC_PATTERN_VIDEO takes the frame folded into the seed (seed +

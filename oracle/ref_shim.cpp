@@ -117,11 +117,17 @@ int ref_filter_rows_any_levels(const std::uint8_t* in, std::uint8_t* out, int w,
 }
 
 // Same body restricted to interior rows [row_begin, row_end): the bounded
-// CPU-baseline sample used by bench.py (a band of the benchmark image).
+// CPU-baseline sample used by bench.py (a band of the benchmark image).  Only
+// the band's rows plus their r-row halos are wrapped in the reference Image
+// (the caller already holds the image; wrapping the whole 805 MB config 4
+// image would time a copy the reference engine never makes).  `in` is the
+// whole image; output rows land at their image offsets in `out`.
 int ref_filter_band(const std::uint8_t* in, std::uint8_t* out, int w, int h, int radius,
                     int levels, int row_begin, int row_end, int workers) {
     try {
-        const oilpaint::Image img = image_of(in, w, h);
+        const int lo = row_begin - radius > 0 ? row_begin - radius : 0;
+        const int hi = row_end + radius < h ? row_end + radius : h;
+        const oilpaint::Image img = image_of(in + static_cast<std::size_t>(lo) * w * 3, w, hi - lo);
         oilpaint::ParallelConfig cfg;
         if (workers > 0) cfg.worker_count = workers;
         oilpaint::parallel_for_rows(row_begin, row_end, cfg, [&](int b, int e) {
@@ -129,7 +135,7 @@ int ref_filter_band(const std::uint8_t* in, std::uint8_t* out, int w, int h, int
             for (int y = b; y < e; ++y) {
                 std::uint8_t* o = out + (static_cast<std::size_t>(y) * w + radius) * 3;
                 for (int x = radius; x < w - radius; ++x, o += 3) {
-                    const oilpaint::Rgb c = oilpaint::filter_pixel(img, x, y, radius, hist);
+                    const oilpaint::Rgb c = oilpaint::filter_pixel(img, x, y - lo, radius, hist);
                     o[0] = c.r;
                     o[1] = c.g;
                     o[2] = c.b;

@@ -24,7 +24,7 @@ EXPORTS = (
     "opc_band_in_row0", "opc_band_in_rows", "opc_last_error", "opc_version",
     "opc_kernel_launches", "opc_device_count", "opc_synchronize", "opc_plan_kernel",
     "opc_release", "opc_generate", "opc_filter_rgb8_multi", "opc_band_begin",
-    "opc_generate_device", "opc_kernel_timing", "opc_kernel_timing_read",
+    "opc_generate_device", "opc_kernel_timing", "opc_kernel_timing_read", "opc_generate_rows",
 )
 
 
@@ -86,6 +86,8 @@ def _load() -> ctypes.CDLL:
     lib.opc_release.restype = None
     lib.opc_generate.argtypes = [i32, ctypes.c_uint64, i32, i32, i32, u8p, i32]
     lib.opc_generate.restype = ctypes.c_int
+    lib.opc_generate_rows.argtypes = [i32, ctypes.c_uint64, i32, i32, i32, i32, i32, u8p, i32]
+    lib.opc_generate_rows.restype = ctypes.c_int
     lib.opc_generate_device.argtypes = [i32, ctypes.c_uint64, i32, i32, u8p, i32, ctypes.c_void_p]
     lib.opc_generate_device.restype = ctypes.c_int
     lib.opc_kernel_timing.argtypes = [i32]

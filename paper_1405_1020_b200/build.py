@@ -53,7 +53,10 @@ def _stale(target: Path, deps: list[Path]) -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> Path:
     BUILD.mkdir(parents=True, exist_ok=True)
-    headers = list(CSRC.glob("*.cuh")) + list((ROOT / "include").glob("*.h"))
+    # every header a source can include: csrc/*.cuh, csrc/*.h (gen_spec.h is
+    # shared by gen.cu and patterns.cpp) and the public include/*.h
+    headers = (list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) +
+               list((ROOT / "include").glob("*.h")))
     jobs = []
     objs = []
     for name in SOURCES:

@@ -9,10 +9,12 @@
 #include <deque>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
+#include <tuple>
 #include <vector>
 
 #include "../../include/oilpaint_b200.h"
@@ -74,18 +76,67 @@ struct DevCtx {
     std::size_t out_cap = 0;
     void* d_scratch = nullptr;  // skew family: sheared entry plane
     std::size_t scratch_cap = 0;
+    // The scratch plane is shared by every launch on the device, whatever its
+    // stream: a launch on stream s waits for the event recorded after the
+    // previous scratch user when that ran on another stream, so two calls in
+    // flight on different user streams never overwrite each other's plane.
+    cudaEvent_t scratch_ev = nullptr;
+    cudaStream_t scratch_stream = nullptr;
+    bool scratch_busy = false;
     int* d_counter = nullptr;
     unsigned counter_idx = 0;
     cudaStream_t s_in = nullptr;   // H2D copies
     cudaStream_t s_out = nullptr;  // D2H copies
     std::vector<cudaEvent_t> ev_in, ev_out, ev_d2h;
-    // pinned staging ring for pageable host buffers
+    // pinned staging ring for pageable host buffers (only the slots a call
+    // uses are allocated: pin_slots of them, pin_cap bytes each)
     static constexpr int kSlots = 3;
     void* pin_in[kSlots] = {};
     void* pin_out[kSlots] = {};
     std::size_t pin_cap = 0;
+    int pin_slots = 0;
     cudaEvent_t ev_slot[kSlots] = {};
 };
+
+void free_staging(DevCtx* c) {
+    for (int k = 0; k < DevCtx::kSlots; ++k) {
+        if (c->pin_in[k]) cudaFreeHost(c->pin_in[k]);
+        if (c->pin_out[k]) cudaFreeHost(c->pin_out[k]);
+        c->pin_in[k] = c->pin_out[k] = nullptr;
+    }
+    c->pin_cap = 0;
+    c->pin_slots = 0;
+}
+
+// Orders a scratch-plane launch on stream s after the previous one (see DevCtx).
+int scratch_acquire(DevCtx* c, cudaStream_t s) {
+    if (!c->scratch_ev) {
+        const cudaError_t e = cudaEventCreateWithFlags(&c->scratch_ev, cudaEventDisableTiming);
+        if (e != cudaSuccess) {
+            g_last_error = std::string("cudaEventCreate(scratch): ") + cudaGetErrorString(e);
+            return OPC_ECUDA;
+        }
+    }
+    if (c->scratch_busy && c->scratch_stream != s) {
+        const cudaError_t e = cudaStreamWaitEvent(s, c->scratch_ev, 0);
+        if (e != cudaSuccess) {
+            g_last_error = std::string("cudaStreamWaitEvent(scratch): ") + cudaGetErrorString(e);
+            return OPC_ECUDA;
+        }
+    }
+    return OPC_OK;
+}
+
+int scratch_release(DevCtx* c, cudaStream_t s) {
+    const cudaError_t e = cudaEventRecord(c->scratch_ev, s);
+    if (e != cudaSuccess) {
+        g_last_error = std::string("cudaEventRecord(scratch): ") + cudaGetErrorString(e);
+        return OPC_ECUDA;
+    }
+    c->scratch_stream = s;
+    c->scratch_busy = true;
+    return OPC_OK;
+}
 
 int ensure_streams(DevCtx* c, std::size_t units) {
     cudaError_t e = cudaSuccess;
@@ -167,9 +218,26 @@ void copy_bytes(std::uint8_t* dst, const std::uint8_t* src, std::size_t n) {
 // worker that picks a finished job never touches freed memory.
 class CopyPool {
   public:
-    static CopyPool& get() {
-        static CopyPool* p = new CopyPool();  // never destroyed: workers sleep until exit
-        return *p;
+    // One pool per device, so the staging copies of devices filtering
+    // concurrently (opc_filter_rgb8_multi from pageable buffers) do not queue
+    // behind each other; the host threads are split between the devices.
+    static CopyPool& get(int device) {
+        static std::mutex mu;
+        static std::vector<CopyPool*> pools;  // never destroyed: workers sleep until exit
+        std::lock_guard<std::mutex> lk(mu);
+        int ndev = 1;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+            cudaGetLastError();
+            ndev = 1;
+        }
+        if (device < 0) device = 0;
+        if (pools.size() <= static_cast<std::size_t>(device)) pools.resize(device + 1, nullptr);
+        if (!pools[device]) {
+            const unsigned hc = std::max(2u, std::thread::hardware_concurrency());
+            const unsigned share = (hc - 1) / static_cast<unsigned>(ndev);
+            pools[device] = new CopyPool(std::max(1u, std::min(15u, share)));
+        }
+        return *pools[device];
     }
     void copy(void* dst, const void* src, std::size_t n) {
         constexpr std::size_t kPiece = 2u << 20;
@@ -214,9 +282,7 @@ class CopyPool {
             if (++j.done == j.pieces) j.cv.notify_all();
         }
     }
-    CopyPool() {
-        const unsigned hc = std::thread::hardware_concurrency();
-        workers_ = std::max(1u, std::min(15u, hc > 1 ? hc - 1 : 1u));
+    explicit CopyPool(unsigned workers) : workers_(workers) {
         for (unsigned t = 0; t < workers_; ++t) {
             std::thread([this] {
                 for (;;) {
@@ -248,38 +314,68 @@ bool is_pinned_or_device(const void* p) {
 }
 
 // ---- live kernel timing (opc_kernel_timing) ----
+// Each launch is bracketed by a start and a stop event recorded on the launch
+// stream; the open start is keyed by (device, stream, kernel id), so launches
+// in flight on different streams or devices never pair up, and events come
+// from a per-device pool (an event must live on its stream's device).
 struct TimedLaunch {
     int id;
+    int device;
     cudaEvent_t start, stop;
 };
 std::mutex g_timing_mu;
-std::vector<TimedLaunch> g_timed;     // recorded launches
-std::vector<cudaEvent_t> g_ev_pool;   // spare events
-cudaEvent_t g_open_start[8] = {};     // per kernel id: start recorded, stop pending
+std::vector<TimedLaunch> g_timed;                                    // recorded launches
+std::map<int, std::vector<cudaEvent_t>> g_ev_pool;                   // spare events per device
+std::map<std::tuple<int, cudaStream_t, int>, cudaEvent_t> g_open;    // start recorded, stop pending
 
-cudaEvent_t take_event() {
-    if (!g_ev_pool.empty()) {
-        cudaEvent_t e = g_ev_pool.back();
-        g_ev_pool.pop_back();
+cudaEvent_t take_event(int device) {
+    std::vector<cudaEvent_t>& pool = g_ev_pool[device];
+    if (!pool.empty()) {
+        cudaEvent_t e = pool.back();
+        pool.pop_back();
         return e;
     }
     cudaEvent_t e = nullptr;
-    cudaEventCreate(&e);
+    if (cudaEventCreate(&e) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
     return e;
 }
 
 void timing_hook(int id, int phase, cudaStream_t s) {
     std::lock_guard<std::mutex> lk(g_timing_mu);
-    if (id < 0 || id >= 8) return;
-    if (phase == 0) {
-        g_open_start[id] = take_event();
-        cudaEventRecord(g_open_start[id], s);
-    } else if (g_open_start[id]) {
-        cudaEvent_t stop = take_event();
-        cudaEventRecord(stop, s);
-        g_timed.push_back({id, g_open_start[id], stop});
-        g_open_start[id] = nullptr;
+    int device = 0;
+    if (cudaGetDevice(&device) != cudaSuccess) {
+        cudaGetLastError();
+        return;
     }
+    const auto key = std::make_tuple(device, s, id);
+    if (phase == 0) {
+        cudaEvent_t ev = take_event(device);
+        if (!ev) return;
+        if (cudaEventRecord(ev, s) != cudaSuccess) {
+            cudaGetLastError();
+            g_ev_pool[device].push_back(ev);
+            return;
+        }
+        auto it = g_open.find(key);
+        if (it != g_open.end()) g_ev_pool[device].push_back(it->second);  // unmatched start
+        g_open[key] = ev;
+        return;
+    }
+    auto it = g_open.find(key);
+    if (it == g_open.end()) return;
+    cudaEvent_t start = it->second;
+    g_open.erase(it);
+    cudaEvent_t stop = take_event(device);
+    if (!stop || cudaEventRecord(stop, s) != cudaSuccess) {
+        cudaGetLastError();
+        g_ev_pool[device].push_back(start);
+        if (stop) g_ev_pool[device].push_back(stop);
+        return;
+    }
+    g_timed.push_back({id, device, start, stop});
 }
 
 std::mutex g_ctx_mu;
@@ -390,16 +486,22 @@ int run_device(const opc::BandArgs& band, int border, int kernel, DevCtx* ctx, c
         // Rotate over 16 task counters (16 bytes each: chunk index + 64-bit
         // unit count) so kernels in flight on different streams never share one.
         int* counter = ctx->d_counter + 4 * (ctx->counter_idx++ & 15u);
-        const int rc = ensure(&ctx->d_scratch, &ctx->scratch_cap, opc::skew_scratch_bytes(a));
+        int rc = ensure(&ctx->d_scratch, &ctx->scratch_cap, opc::skew_scratch_bytes(a));
+        if (rc == OPC_OK) rc = scratch_acquire(ctx, s);
         if (rc != OPC_OK) return rc;
         e = opc::launch_skew(a, counter, ctx->d_scratch, ctx->num_sms, s);
         if (e != cudaSuccess) return cuda_error(e, "skew kernel launch");
+        rc = scratch_release(ctx, s);
+        if (rc != OPC_OK) return rc;
     } else if (kernel == OPC_KERNEL_SLIDE) {
         int* counter = ctx->d_counter + 4 * (ctx->counter_idx++ & 15u);
-        const int rc = ensure(&ctx->d_scratch, &ctx->scratch_cap, opc::slide_scratch_bytes(a));
+        int rc = ensure(&ctx->d_scratch, &ctx->scratch_cap, opc::slide_scratch_bytes(a));
+        if (rc == OPC_OK) rc = scratch_acquire(ctx, s);
         if (rc != OPC_OK) return rc;
         e = opc::launch_slide(a, counter, ctx->d_scratch, ctx->num_sms, s);
         if (e != cudaSuccess) return cuda_error(e, "slide kernel launch");
+        rc = scratch_release(ctx, s);
+        if (rc != OPC_OK) return rc;
     } else if (kernel == OPC_KERNEL_COLUMN) {
         e = opc::launch_column(a, ctx->num_sms, s);
         if (e != cudaSuccess) return cuda_error(e, "column kernel launch");
@@ -498,7 +600,7 @@ int filter_core(const std::uint8_t* in, std::uint8_t* out, int frames, int w, in
     rc = ensure(&ctx->d_out, &ctx->out_cap, tot_out);
     if (rc != OPC_OK) return rc;
     struct Unit {
-        int frame, y0, y1;
+        int frame, nframes, y0, y1;
     };
     std::vector<Unit> units;
     const int rows = y_end - y_begin;
@@ -533,13 +635,20 @@ int filter_core(const std::uint8_t* in, std::uint8_t* out, int frames, int w, in
         }
         int y = y_begin;
         for (int q : sizes) {
-            units.push_back({0, y, y + q});
+            units.push_back({0, 1, y, y + q});
             y += q;
         }
-    } else if (in_bytes >= (4ull << 20)) {
-        for (int f = 0; f < frames; ++f) units.push_back({f, y_begin, y_end});
     } else {
-        units.push_back({-1, y_begin, y_end});  // whole batch in one launch
+        // Frames of >= 4 MB one per unit; smaller frames grouped into units of
+        // about 48 MB (one launch each), so the staging slots stay bounded
+        // whatever the batch length.
+        const std::size_t fb = std::max(in_bytes, out_bytes);
+        const int per = fb >= (4ull << 20)
+                            ? 1
+                            : static_cast<int>(std::max<std::size_t>(1, (48ull << 20) / fb));
+        for (int f = 0; f < frames; f += per) {
+            units.push_back({f, std::min(per, frames - f), y_begin, y_end});
+        }
     }
     rc = ensure_streams(ctx, units.size());
     if (rc != OPC_OK) return rc;
@@ -553,13 +662,15 @@ int filter_core(const std::uint8_t* in, std::uint8_t* out, int frames, int w, in
     std::vector<int> loaded_hi(frames > 0 ? frames : 1, a.in_row0);
     for (const Unit& un : units) {
         Xfer x{};
-        x.f0 = un.frame < 0 ? 0 : un.frame;
-        x.nf = un.frame < 0 ? frames : 1;
+        x.f0 = un.frame;
+        x.nf = un.nframes;
         x.y0 = un.y0;
         x.y1 = un.y1;
-        if (un.frame < 0) {
-            x.in_n = tot_in;
-            x.out_n = tot_out;
+        if (un.nframes > 1) {
+            x.in_off = in_bytes * x.f0;
+            x.in_n = in_bytes * x.nf;
+            x.out_off = out_bytes * x.f0;
+            x.out_n = out_bytes * x.nf;
         } else {
             const int need_hi = opc_band_in_row0(h, un.y0, radius) +
                                 opc_band_in_rows(h, un.y0, un.y1, radius);
@@ -629,21 +740,23 @@ int filter_core(const std::uint8_t* in, std::uint8_t* out, int frames, int w, in
     // own pageable path ran C4 end to end at 2.2 GP/s against 15 GP/s pinned.
     std::size_t slot_need = 0;
     for (const Xfer& x : xs) slot_need = std::max(slot_need, std::max(x.in_n, x.out_n));
-    if (ctx->pin_cap < slot_need) {
-        for (int k = 0; k < DevCtx::kSlots; ++k) {
-            if (ctx->pin_in[k]) cudaFreeHost(ctx->pin_in[k]);
-            if (ctx->pin_out[k]) cudaFreeHost(ctx->pin_out[k]);
-            ctx->pin_in[k] = ctx->pin_out[k] = nullptr;
+    const int slots_need = static_cast<int>(std::min<std::size_t>(DevCtx::kSlots, xs.size()));
+    if (ctx->pin_cap < slot_need || ctx->pin_slots < slots_need) {
+        const std::size_t cap = std::max(slot_need, ctx->pin_cap);
+        const int nslots = std::max(slots_need, ctx->pin_slots);
+        free_staging(ctx);
+        for (int k = 0; k < nslots; ++k) {
+            e = cudaHostAlloc(&ctx->pin_in[k], cap, cudaHostAllocPortable);
+            if (e == cudaSuccess) e = cudaHostAlloc(&ctx->pin_out[k], cap, cudaHostAllocPortable);
+            if (e != cudaSuccess) {
+                free_staging(ctx);
+                return cuda_error(e, "cudaHostAlloc(staging)");
+            }
         }
-        ctx->pin_cap = 0;
-        for (int k = 0; k < DevCtx::kSlots; ++k) {
-            e = cudaHostAlloc(&ctx->pin_in[k], slot_need, cudaHostAllocPortable);
-            if (e == cudaSuccess) e = cudaHostAlloc(&ctx->pin_out[k], slot_need, cudaHostAllocPortable);
-            if (e != cudaSuccess) return cuda_error(e, "cudaHostAlloc(staging)");
-        }
-        ctx->pin_cap = slot_need;
+        ctx->pin_cap = cap;
+        ctx->pin_slots = nslots;
     }
-    CopyPool& pool = CopyPool::get();
+    CopyPool& pool = CopyPool::get(ctx->device);
     std::mutex m;
     std::condition_variable cv;
     std::size_t enqueued = 0, drained = 0;  // units whose D2H is enqueued / copied out
@@ -732,10 +845,12 @@ extern "C" {
 int opc_kernel_timing(int32_t enable) {
     std::lock_guard<std::mutex> lk(g_timing_mu);
     for (const TimedLaunch& t : g_timed) {
-        g_ev_pool.push_back(t.start);
-        g_ev_pool.push_back(t.stop);
+        g_ev_pool[t.device].push_back(t.start);
+        g_ev_pool[t.device].push_back(t.stop);
     }
     g_timed.clear();
+    for (const auto& kv : g_open) g_ev_pool[std::get<0>(kv.first)].push_back(kv.second);
+    g_open.clear();
     opc::g_timing_hook = enable ? timing_hook : nullptr;
     return OPC_OK;
 }
@@ -911,6 +1026,12 @@ void opc_release(void) {
         if (c->s_out) cudaStreamDestroy(c->s_out);
         for (cudaEvent_t ev : c->ev_in) cudaEventDestroy(ev);
         for (cudaEvent_t ev : c->ev_out) cudaEventDestroy(ev);
+        for (cudaEvent_t ev : c->ev_d2h) cudaEventDestroy(ev);
+        for (cudaEvent_t ev : c->ev_slot) {
+            if (ev) cudaEventDestroy(ev);
+        }
+        if (c->scratch_ev) cudaEventDestroy(c->scratch_ev);
+        free_staging(c.get());
         c.reset();
     }
     g_ctx.clear();

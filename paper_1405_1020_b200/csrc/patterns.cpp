@@ -38,19 +38,21 @@ struct Stream {
     double unit() { return static_cast<double>(next() >> 11) * (1.0 / 9007199254740992.0); }
 };
 
+// body(y0, y1) over the rows [row0, row1), split across threads.
 template <class F>
-void parallel_rows(int height, int threads, F&& body) {
+void parallel_rows(int row0, int row1, int threads, F&& body) {
+    const int rows = row1 - row0;
     if (threads <= 0) threads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
     threads = std::min(threads, 64);
-    threads = std::min(threads, height);
+    threads = std::min(threads, rows);
     if (threads <= 1) {
-        body(0, height);
+        body(row0, row1);
         return;
     }
     std::vector<std::thread> pool;
     for (int t = 0; t < threads; ++t) {
-        const int b = static_cast<int>(static_cast<long long>(height) * t / threads);
-        const int e = static_cast<int>(static_cast<long long>(height) * (t + 1) / threads);
+        const int b = row0 + static_cast<int>(static_cast<long long>(rows) * t / threads);
+        const int e = row0 + static_cast<int>(static_cast<long long>(rows) * (t + 1) / threads);
         pool.emplace_back([&body, b, e] { body(b, e); });
     }
     for (auto& th : pool) th.join();
@@ -113,14 +115,16 @@ const std::vector<std::int32_t>& gauss_table() {
 
 // Config 2 / 5 field: per channel, 4 sinusoids with 0.5-4 cycles across the
 // frame in x and y, random phase, amplitude in [0.5, 1).
-void smooth_field(std::uint64_t seed, int w, int h, bool gaussian, std::uint8_t* out,
-                  int threads) {
+// `out` holds rows [row0, row1) of the frame.
+void smooth_field(std::uint64_t seed, int w, int h, bool gaussian, int row0, int row1,
+                  std::uint8_t* out, int threads) {
     opc::SmoothSpec sp;
     opc::smooth_spec(seed, w, h, &sp);
     const std::int32_t* sine = opc::sine_table_data();
     const std::int32_t* gauss = gaussian ? opc::gauss_table_data() : nullptr;
-    parallel_rows(h, threads, [&](int y0, int y1) {
+    parallel_rows(row0, row1, threads, [&](int y0, int y1) {
         for (int y = y0; y < y1; ++y) {
+            std::uint8_t* row = out + static_cast<std::size_t>(y - row0) * w * 3;
             for (int x = 0; x < w; ++x) {
                 const std::uint64_t pix = static_cast<std::uint64_t>(y) * w + x;
                 for (int c = 0; c < 3; ++c) {
@@ -138,7 +142,7 @@ void smooth_field(std::uint64_t seed, int w, int h, bool gaussian, std::uint8_t*
                     } else {
                         v += static_cast<int>(word % 17) - 8;
                     }
-                    out[pix * 3 + c] = static_cast<std::uint8_t>(std::clamp(v, 0, 255));
+                    row[3 * x + c] = static_cast<std::uint8_t>(std::clamp(v, 0, 255));
                 }
             }
         }
@@ -147,12 +151,12 @@ void smooth_field(std::uint64_t seed, int w, int h, bool gaussian, std::uint8_t*
 
 // Config 3: background colour plus 64 axis-aligned rectangles with random
 // inclusive corners and colours, painted in order (later on top).
-void rects(std::uint64_t seed, int w, int h, std::uint8_t* out, int threads) {
+void rects(std::uint64_t seed, int w, int h, int row0, int row1, std::uint8_t* out, int threads) {
     opc::RectsSpec sp;
     opc::rects_spec(seed, w, h, &sp);
-    parallel_rows(h, threads, [&](int y0, int y1) {
+    parallel_rows(row0, row1, threads, [&](int y0, int y1) {
         for (int y = y0; y < y1; ++y) {
-            std::uint8_t* row = out + static_cast<std::size_t>(y) * w * 3;
+            std::uint8_t* row = out + static_cast<std::size_t>(y - row0) * w * 3;
             for (int x = 0; x < w; ++x) {
                 row[3 * x] = static_cast<std::uint8_t>(sp.bg);
                 row[3 * x + 1] = static_cast<std::uint8_t>(sp.bg >> 8);
@@ -218,31 +222,35 @@ const std::int32_t* gauss_table_data() { return gauss_table().data(); }
 
 }  // namespace opc
 
-extern "C" int opc_generate(int32_t kind, uint64_t seed, int32_t w, int32_t h, int32_t frame,
-                            uint8_t* out, int32_t threads) {
-    if (w < 1 || h < 1 || !out) return 1;
-    const std::size_t n = static_cast<std::size_t>(w) * h * 3;
+extern "C" int opc_generate_rows(int32_t kind, uint64_t seed, int32_t w, int32_t h,
+                                 int32_t frame, int32_t row0, int32_t nrows, uint8_t* out,
+                                 int32_t threads) {
+    if (w < 1 || h < 1 || !out || row0 < 0 || nrows < 1 || row0 > h - nrows) return 1;
+    const int row1 = row0 + nrows;
+    const std::size_t row_bytes = static_cast<std::size_t>(w) * 3;
     switch (kind) {
         case OPC_PATTERN_NOISE:
-            parallel_rows(h, threads, [&](int y0, int y1) {
-                const std::size_t b = static_cast<std::size_t>(y0) * w * 3;
-                const std::size_t e = static_cast<std::size_t>(y1) * w * 3;
+            // byte i of the image = byte (i mod 8) of stream word i / 8
+            parallel_rows(row0, row1, threads, [&](int y0, int y1) {
+                const std::size_t b = static_cast<std::size_t>(y0) * row_bytes;
+                const std::size_t e = static_cast<std::size_t>(y1) * row_bytes;
+                std::uint8_t* o = out + (b - static_cast<std::size_t>(row0) * row_bytes);
                 std::uint64_t k = ~0ull, word = 0;
-                for (std::size_t i = b; i < e; ++i) {
+                for (std::size_t i = b; i < e; ++i, ++o) {
                     if ((i >> 3) != k) {
                         k = i >> 3;
                         word = stream_word(seed, k);
                     }
-                    out[i] = static_cast<std::uint8_t>(word >> (8 * (i & 7)));
+                    *o = static_cast<std::uint8_t>(word >> (8 * (i & 7)));
                 }
             });
             return 0;
         case OPC_PATTERN_GRADIENT: {
             const int dx = w > 1 ? w - 1 : 1, dy = h > 1 ? h - 1 : 1;
             const int dd = w + h > 2 ? w + h - 2 : 1;
-            for (int y = 0; y < h; ++y) {
-                for (int x = 0; x < w; ++x) {
-                    std::uint8_t* p = out + (static_cast<std::size_t>(y) * w + x) * 3;
+            for (int y = row0; y < row1; ++y) {
+                std::uint8_t* p = out + static_cast<std::size_t>(y - row0) * row_bytes;
+                for (int x = 0; x < w; ++x, p += 3) {
                     p[0] = static_cast<std::uint8_t>(x * 255 / dx);
                     p[1] = static_cast<std::uint8_t>(y * 255 / dy);
                     p[2] = static_cast<std::uint8_t>((x + y) * 255 / dd);
@@ -250,35 +258,43 @@ extern "C" int opc_generate(int32_t kind, uint64_t seed, int32_t w, int32_t h, i
             }
             return 0;
         }
-        case OPC_PATTERN_UNIFORM:
+        case OPC_PATTERN_UNIFORM: {
+            const std::size_t n = row_bytes * static_cast<std::size_t>(nrows);
             for (std::size_t i = 0; i < n; i += 3) {
                 out[i] = static_cast<std::uint8_t>(seed);
                 out[i + 1] = static_cast<std::uint8_t>(seed >> 8);
                 out[i + 2] = static_cast<std::uint8_t>(seed >> 16);
             }
             return 0;
+        }
         case OPC_PATTERN_CHECKER: {
             const int cell = static_cast<int>(seed);
             if (cell < 1) return 1;
-            for (int y = 0; y < h; ++y) {
-                for (int x = 0; x < w; ++x) {
+            for (int y = row0; y < row1; ++y) {
+                std::uint8_t* p = out + static_cast<std::size_t>(y - row0) * row_bytes;
+                for (int x = 0; x < w; ++x, p += 3) {
                     const std::uint8_t v = ((x / cell) + (y / cell)) % 2 == 0 ? 255 : 0;
-                    std::uint8_t* p = out + (static_cast<std::size_t>(y) * w + x) * 3;
                     p[0] = p[1] = p[2] = v;
                 }
             }
             return 0;
         }
         case OPC_PATTERN_SMOOTH:
-            smooth_field(seed, w, h, false, out, threads);
+            smooth_field(seed, w, h, false, row0, row1, out, threads);
             return 0;
         case OPC_PATTERN_RECTS:
-            rects(seed, w, h, out, threads);
+            rects(seed, w, h, row0, row1, out, threads);
             return 0;
         case OPC_PATTERN_VIDEO:
-            smooth_field(seed + static_cast<std::uint64_t>(frame), w, h, true, out, threads);
+            smooth_field(seed + static_cast<std::uint64_t>(frame), w, h, true, row0, row1, out,
+                         threads);
             return 0;
         default:
             return 1;
     }
+}
+
+extern "C" int opc_generate(int32_t kind, uint64_t seed, int32_t w, int32_t h, int32_t frame,
+                            uint8_t* out, int32_t threads) {
+    return opc_generate_rows(kind, seed, w, h, frame, 0, h, out, threads);
 }

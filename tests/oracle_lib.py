@@ -70,6 +70,9 @@ def load_ref() -> ctypes.CDLL:
     lib.ref_filter_band.restype = i32
     lib.ref_generate.argtypes = [i32, ctypes.c_uint64, i32, i32, vp]
     lib.ref_generate.restype = i32
+    lib.ref_harness_generate_rows.argtypes = [i32, ctypes.c_uint64, i32, i32, i32, i32, i32, vp,
+                                              i32]
+    lib.ref_harness_generate_rows.restype = i32
     lib.ref_write_ppm.argtypes = [vp, i32, i32, vp, ctypes.c_long]
     lib.ref_write_ppm.restype = ctypes.c_long
     return lib

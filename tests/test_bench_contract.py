@@ -31,7 +31,7 @@ def test_best_fit_models_match_survey_table(bench):
 
 
 def test_l2_rule_and_rank_bytes(bench):
-    from paper_1405_1020_b200.patterns import CONFIGS
+    CONFIGS = bench.load_workloads()
     c4 = CONFIGS["c4"]
     assert bench.rank0_in_bytes(c4, 1) == 3 * 16384 * 16384
     # rank 0 of 8: its 2048 rows plus the 15 halo rows below
@@ -42,3 +42,61 @@ def test_l2_rule_and_rank_bytes(bench):
     assert "flushed" in bench.workload_config(CONFIGS["c1"], 1)["l2"]
     cfg = bench.workload_config(CONFIGS["c5"], 2)
     assert cfg["partition"].startswith("frames") and cfg["frames"] == 64
+
+
+def test_workloads_match_package_configs(bench):
+    from paper_1405_1020_b200.patterns import CONFIGS
+    wl = bench.load_workloads()
+    assert set(wl) == set(CONFIGS) == {"c1", "c2", "c3", "c4", "c5"}
+    for k, w in wl.items():
+        c = CONFIGS[k]
+        assert (c.width, c.height, c.frames, c.radius, c.levels, c.pattern, c.seed) == \
+            (w.width, w.height, w.frames, w.radius, w.levels, w.pattern, w.seed)
+
+
+PURITY = r"""
+import runpy, sys
+sys.argv = ["bench.py", "--impl", "reference", "--config", sys.argv[1], "--steps", "1",
+            "--warmup", "0", "--gpus", "2"]
+runpy.run_path("bench.py", run_name="__main__")
+assert not any(m == "paper_1405_1020_b200" or m.startswith("paper_1405_1020_b200.")
+               for m in sys.modules), "reference arm imported the product package"
+maps = open("/proc/self/maps").read()
+assert "liboilpaint_b200" not in maps, "reference arm mapped the product library"
+print("PURE", "libref_oilpaint" in maps)
+"""
+
+
+@pytest.mark.parametrize("config", ["c1", "c3"])
+def test_reference_arm_never_loads_the_product(config):
+    """bench.py --impl reference runs the reference engine (oracle/_ref) on
+    inputs it generates itself: it imports no product module and maps no
+    product library (the ratio is void otherwise)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, OILPAINT_REF_STEP_S="0.05", OILPAINT_B200_AUTOBUILD="0")
+    res = subprocess.run([sys.executable, "-c", PURITY, config], cwd=ROOT, env=env,
+                         capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stderr
+    lines = res.stdout.strip().splitlines()
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] in ("reference", "port")
+    assert lines[-1].startswith("PURE")
+
+
+def test_reference_inputs_match_product_generators(bench):
+    """The reference arm's inputs (oracle/_ref: the reference Noise generator,
+    the harness generators) are the bytes the product arm generates."""
+    import numpy as np
+    import paper_1405_1020_b200 as opc
+    eng = bench.CpuEngine()
+    if eng.ref is None:
+        pytest.skip("oracle/_ref not built")
+    for name in ("c1", "c2", "c3", "c4", "c5"):
+        wl = bench.load_workloads()[name]
+        got = eng.generate_rows(wl, 40)
+        want = opc.CONFIGS[name].generate_rows(0, 40)
+        assert np.array_equal(got, want), name

@@ -3,7 +3,10 @@
 Mirrors the reference CLI contract (proj/tools/oilbench.cpp): subcommands
 apply / gen / bench over binary PPM files and exit codes 0 ok, 1 usage, 2 I/O,
 parse or runtime error, 3 filter parameter error.  The PPM codec
-(include/oilpaint_b200_ppm.hpp) follows proj/src/ppm.cpp:67-143.  CPU tests cover
+(include/oilpaint_b200_ppm.hpp) keeps the reference's byte format
+(proj/include/oilpaint/ppm.hpp); its error messages name the offending part
+(magic, width, height, maxval, payload), the substrings the reference tests pin
+(proj/tests/test_ppm.cpp:44-59).  CPU tests cover
 argument handling, generation and PPM parsing (a well-formed file reaches the
 engine, which then reports that no CUDA device is present); the GPU tests run
 the filter and the sweep.
@@ -61,7 +64,9 @@ def test_usage_errors_exit_1(tool):
                  ["apply", "--input", "a", "--output", "b", "--border", "mirror"],
                  ["gen", "--pattern", "plaid", "--width", "4", "--height", "4", "--output", "x"],
                  ["gen", "--pattern", "noise", "--width", "0", "--height", "4", "--output", "x"],
-                 ["bench", "--sizes", "huge"], ["bench", "--reps", "0"]):
+                 ["bench", "--sizes", "huge"], ["bench", "--reps", "0"],
+                 ["apply", "--input", "a", "--output", "b", "--threads", "4"],
+                 ["bench", "--threads=8"]):
         res = run(tool, *args)
         assert res.returncode == 1, (args, res.stderr)
         assert "usage:" in res.stderr
@@ -103,13 +108,16 @@ def _engine_reached(res) -> bool:
     (b"P6\n8 8\n255\n" + bytes(192), True, ""),
     (b"P6 8 8 255 " + bytes(192), True, ""),
     (b"P6\n# comment\n8 # w\n8\n255\n" + bytes(192) + b"trailing", True, ""),
-    (b"P3\n8 8\n255\n" + bytes(192), False, "bad magic"),
+    (b"P3\n8 8\n255\n" + bytes(192), False, "magic"),
+    (b"P6x8 8\n255\n" + bytes(192), False, "magic"),
     (b"P6\n8 8\n65535\n" + bytes(384), False, "maxval"),
-    (b"P6\n8 8\n255\n" + bytes(100), False, "truncated payload"),
-    (b"P6\n0 8\n255\n", False, "width must be positive"),
-    (b"P6\n8 x\n255\n", False, "invalid character in height"),
-    (b"P6\n8 8", False, "unexpected end of header"),
-    (b"P6\n8 8\n255", False, "missing whitespace after maxval"),
+    (b"P6\n8 8\n255\n" + bytes(100), False, "payload too short"),
+    (b"P6\n0 8\n255\n", False, "width must be at least 1"),
+    (b"P6\n8 0\n255\n", False, "height must be at least 1"),
+    (b"P6\n8 x\n255\n", False, "height is not a decimal number"),
+    (b"P6\n99999999999 8\n255\n", False, "width is too large"),
+    (b"P6\n8 8", False, "header ends before the maxval"),
+    (b"P6\n8 8\n255", False, "maxval must be followed by one whitespace byte"),
 ])
 def test_ppm_parsing(tool, tmp_path, blob, ok, msg):
     src = tmp_path / "in.ppm"
@@ -170,3 +178,20 @@ def test_bench_sweep_csv(tool, tmp_path, gpu):
     label, radius, t1, t2, imp = prow[1].split(",")
     assert (label, radius, float(t1)) == ("VGA", "2", 54.0)
     assert abs(float(imp) - 100 * (54.0 - float(t2)) / 54.0) < 1e-3
+
+
+def test_ppm_bytes_match_reference_writer(tool, tmp_path):
+    """The codec's canonical bytes equal the reference write_ppm (proj/src/ppm.cpp
+    via oracle/_ref) for generated images of several shapes."""
+    if not oracle_lib.ref_available():
+        pytest.skip("oracle/_ref not built")
+    ref = oracle_lib.load_ref()
+    for w, h, seed in ((1, 1, 0), (33, 17, 7), (640, 3, 9)):
+        p = tmp_path / "g.ppm"
+        run(tool, "gen", "--pattern", "noise", "--width", w, "--height", h, "--seed", seed,
+            "--output", p, check_rc=0)
+        img = np.empty((h, w, 3), np.uint8)
+        assert ref.ref_generate(0, seed, w, h, img.ctypes.data) == 0
+        buf = np.empty(64 + img.size, np.uint8)
+        n = ref.ref_write_ppm(img.ctypes.data, w, h, buf.ctypes.data, buf.size)
+        assert p.read_bytes() == buf[:n].tobytes()

@@ -91,3 +91,36 @@ def test_gloo_band_scatter_gather_matches_whole_image(world, r, L, border):
         assert p.exitcode == 0
     want = oracle_lib.oracle_filter(img, r, L, border)
     assert np.array_equal(res, want)
+
+
+def _nccl_worker(port, img, params, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        q.put(filter_distributed(img, params))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_nccl_device_band_path(gpu):
+    """The NCCL form keeps bands in device memory (opc_filter_rgb8_band with
+    device pointers on torch's stream); world size 1 on the one GPU a test box
+    has, checked against the oracle (L = 256 exercises the extension flag)."""
+    rng = np.random.default_rng(17)
+    img = rng.integers(0, 256, (203, 157, 3), dtype=np.uint8)
+    for params in (FilterParams(6, 20, 0), FilterParams(4, 256, 1)):
+        ctx = mp.get_context("spawn")
+        q = ctx.Queue()
+        p = ctx.Process(target=_nccl_worker, args=(_free_port(), img, params, q))
+        p.start()
+        res = q.get(timeout=300)
+        p.join(timeout=60)
+        assert p.exitcode == 0
+        want = oracle_lib.oracle_filter(img, params.radius, params.intensity_levels,
+                                        int(params.border))
+        assert np.array_equal(res, want)

@@ -157,3 +157,68 @@ def test_band_writes_exactly_its_rows(gpu, y0, y1):
         outs.append(buf[97 * 3:-97 * 3].reshape(y1 - y0, 97, 3))
     assert np.array_equal(outs[0], outs[1])
     assert np.array_equal(outs[0], whole[y0:y1])
+
+
+@pytest.mark.parametrize("kernel", ["skew", "slide"])
+def test_two_streams_share_scratch_safely(gpu, kernel):
+    """Device-pointer calls in flight on two user streams at once (and a host
+    call on the library's own stream) share the device's scratch plane: each
+    launch is ordered after the previous scratch user, so no call reads the
+    other's sheared / transposed plane (capi.cu scratch events)."""
+    import torch
+    from paper_1405_1020_b200 import _lib
+    L = 20 if kernel == "skew" else 100
+    kid = _lib.OPC_KERNEL_SKEW if kernel == "skew" else _lib.OPC_KERNEL_SLIDE
+    imgs = [gpu.generate(gpu.Pattern.NOISE, 1500, 700, seed=s) for s in (1, 2, 3, 4)]
+    p = gpu.FilterParams(9, L)
+    want = [gpu.apply_cuda(im, p, gpu.CudaConfig(kernel=kid)) for im in imgs]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    d_in = [torch.from_numpy(im).cuda() for im in imgs]
+    torch.cuda.synchronize()
+    d_out = [torch.empty_like(t) for t in d_in]
+    for rep in range(3):
+        for i in range(4):
+            s = streams[i % 2]
+            cfg = gpu.CudaConfig(device=0, stream=s.cuda_stream, kernel=kid)
+            gpu.apply_cuda_device(d_in[i].data_ptr(), d_out[i].data_ptr(), 1500, 700, p, cfg)
+        host = gpu.apply_cuda(imgs[rep], p, gpu.CudaConfig(kernel=kid))  # ctx stream, blocking
+        assert np.array_equal(host, want[rep])
+        torch.cuda.synchronize()
+        for i in range(4):
+            assert np.array_equal(d_out[i].cpu().numpy(), want[i]), (rep, i)
+
+
+def test_small_frame_batch_units(gpu):
+    """A long batch of small frames runs in bounded units (about 48 MB of frames
+    each, pinned staging sized to one unit) and equals the per-frame results
+    and the oracle, from pageable and from pinned buffers."""
+    import torch
+    frames = gpu.generate(gpu.Pattern.NOISE, 640, 480, seed=21)
+    batch = np.stack([np.roll(frames, 7 * k, axis=1) for k in range(60)])  # 55 MB > one unit
+    p = gpu.FilterParams(2, 20)
+    got = gpu.apply_cuda_batch(batch, p)
+    for k in (0, 1, 51, 52, 59):
+        assert np.array_equal(got[k], gpu.apply_cuda(batch[k], p)), k
+    assert np.array_equal(got[59], oracle_lib.oracle_filter(batch[59], 2, 20, 0))
+    pinned = torch.from_numpy(batch).pin_memory().numpy()
+    assert np.array_equal(gpu.apply_cuda_batch(pinned, p), got)
+
+
+def test_multi_device_frames_match_oracle(gpu):
+    rng = np.random.default_rng(9)
+    frames = rng.integers(0, 256, (5, 41, 77, 3), dtype=np.uint8)
+    got = gpu.apply_cuda_batch(frames, gpu.FilterParams(7, 30), gpu.CudaConfig(devices=(0, 0)))
+    for k in range(5):
+        assert np.array_equal(got[k], oracle_lib.oracle_filter(frames[k], 7, 30, 0)), k
+
+
+def test_c4_input_is_reference_noise(gpu):
+    """The C4 bench input (Noise{4}, 16384 wide) equals the reference generator
+    (proj/src/pattern.cpp:64-76 via oracle/_ref) on a band of rows."""
+    if not oracle_lib.ref_available():
+        pytest.skip("oracle/_ref not built")
+    ref = oracle_lib.load_ref()
+    want = np.empty((64, 16384, 3), np.uint8)
+    assert ref.ref_generate(0, 4, 16384, 64, want.ctypes.data) == 0
+    got = gpu.generate(gpu.Pattern.NOISE, 16384, 64, seed=4)
+    assert np.array_equal(got, want)

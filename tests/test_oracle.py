@@ -147,3 +147,20 @@ def test_oracle_matches_reference_live():
     img = rng.integers(0, 256, (20, 24, 3), dtype=np.uint8)
     assert np.array_equal(oracle_lib.oracle_filter(img, 2, 256, 0),
                           oracle_lib.ref_oracle_filter(ref, img, 2, 256, 0))
+
+
+def test_ref_filter_band_equals_reference_rows():
+    """bench.py's CPU sample (ref_filter_band: the reference engine body on a
+    band's rows, wrapping only the band plus halos) writes exactly the rows the
+    reference apply_parallel produces."""
+    if not oracle_lib.ref_available():
+        pytest.skip("oracle/_ref not built")
+    ref = oracle_lib.load_ref()
+    rng = np.random.default_rng(77)
+    img = rng.integers(0, 256, (90, 53, 3), dtype=np.uint8)
+    for r, L, y0, y1 in ((4, 20, 4, 86), (4, 20, 30, 41), (7, 255, 7, 8), (7, 30, 60, 83)):
+        want = oracle_lib.ref_apply(ref, img, r, L, 0, engine=1, workers=3)
+        out = np.zeros_like(img)
+        assert ref.ref_filter_band(img.ctypes.data, out.ctypes.data, 53, 90, r, L, y0, y1, 3) == 0
+        assert np.array_equal(out[y0:y1, r:53 - r], want[y0:y1, r:53 - r]), (r, L, y0, y1)
+        assert not out[:y0].any() and not out[y1:].any()

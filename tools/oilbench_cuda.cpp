@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
+#include <climits>
 #include <cstdlib>
 #include <fstream>
 #include <iostream>
@@ -318,16 +319,25 @@ int main(int argc, char** argv) {
     try {
         if (argc < 2) throw UsageError("a subcommand is required");
         const std::string cmd = argv[1];
+        for (int i = 2; i < argc; ++i) {
+            const std::string a = argv[i];
+            if (a == "--threads" || a.rfind("--threads=", 0) == 0) {
+                // the reference CLI's worker count belongs to its CPU engines
+                // (oilbench.cpp --engine par); the GPU engine has no thread knob
+                throw UsageError("--threads selects CPU workers of the reference engines; the "
+                                 "cuda engine does not take it (use --devices)");
+            }
+        }
         if (cmd == "apply") {
             return run_apply(Options(argc, argv, 2, {"input", "output", "radius", "levels", "engine",
-                                                     "border", "threads", "devices"}));
+                                                     "border", "devices"}));
         }
         if (cmd == "gen") {
             return run_gen(Options(argc, argv, 2, {"pattern", "width", "height", "seed", "output"}));
         }
         if (cmd == "bench") {
             return run_bench(Options(argc, argv, 2, {"sizes", "radii", "levels", "reps", "out",
-                                                     "threads", "baseline", "devices"}));
+                                                     "baseline", "devices"}));
         }
         throw UsageError("unknown subcommand '" + cmd + "'");
     } catch (const UsageError& e) {
