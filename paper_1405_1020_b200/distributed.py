@@ -58,16 +58,24 @@ def _default_band(in_rows, height, y0, y1, params):
 
 def _device_band(dev_in, height: int, y0: int, y1: int, params: FilterParams):
     """Band filter on device-resident rows (a torch uint8 CUDA tensor holding
-    the halo'd input rows): the output rows stay on the device, enqueued on
-    torch's current stream so the NCCL send that follows is ordered after it."""
+    the halo'd input rows): the output rows stay on the device.  The library
+    call runs on a side stream ordered after torch's current stream (which
+    wrote dev_in) and before it (which the NCCL send that follows uses); the
+    legacy default stream has no handle to pass to the C-ABI (a NULL stream
+    there means the library's own stream)."""
     import torch
 
     rows, w, _ = dev_in.shape
+    cur = torch.cuda.current_stream(dev_in.device)
+    side = torch.cuda.Stream(device=dev_in.device)
+    side.wait_stream(cur)
     out = torch.empty((y1 - y0, w, 3), dtype=torch.uint8, device=dev_in.device)
-    cfg = CudaConfig(device=dev_in.device.index,
-                     stream=torch.cuda.current_stream(dev_in.device).cuda_stream,
+    cfg = CudaConfig(device=dev_in.device.index, stream=side.cuda_stream,
                      allow_levels_256=params.intensity_levels == 256)
     apply_cuda_band_device(dev_in.data_ptr(), out.data_ptr(), w, height, y0, y1, params, cfg)
+    dev_in.record_stream(side)
+    out.record_stream(side)
+    cur.wait_stream(side)
     return out
 
 
