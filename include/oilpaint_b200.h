@@ -55,6 +55,8 @@ extern "C" {
 /* cfg->flags */
 #define OPC_FLAG_DEVICE_POINTERS 0x1u /* in/out are device pointers on cfg->device  */
 #define OPC_FLAG_ALLOW_LEVELS_256 0x2u /* documented extension: accept L = 256 (257 bins, config 3) */
+#define OPC_FLAG_COUNT_OPS 0x4u /* measurement run: the content-dependent kernel family (slide)
+                                   counts the primitives it executes (opc_op_counts) */
 
 /* cfg->kernel: 0 = automatic choice; the others force one kernel family
  * (test hooks, every family is bit-exact on every input it accepts). */
@@ -143,6 +145,17 @@ int opc_synchronize(const opc_config* cfg);
 #define OPC_KID_COLUMN 6
 int opc_kernel_timing(int32_t enable);
 int opc_kernel_timing_read(int32_t kernel_id, double* ms_total, int64_t* launches);
+
+/* Primitive counts accumulated on `device` by calls made with
+ * OPC_FLAG_COUNT_OPS (synchronizes the device): out[0] output pixels, [1]
+ * lane-steps, [2] histogram updates, [3] bins examined by argmax rescans,
+ * [4] window pixels examined to rebuild winner sums, [5] warp rescans,
+ * [6] winner changes, [7] warp-steps with updates.  n <= 8 entries are
+ * written; reset != 0 zeroes the counters afterwards.  The slide kernel's
+ * work depends on the content; bench.py turns these counts into the
+ * algorithmic lane-op count of its roofline (SURVEY.md 8(d) primitives). */
+#define OPC_OPCOUNT_N 8
+int opc_op_counts(int32_t device, uint64_t* out, int32_t n, int32_t reset);
 
 /* Which kernel family OPC_KERNEL_AUTO would use for these parameters
  * (OPC_KERNEL_*), or -1 if invalid.  Host logic only. */

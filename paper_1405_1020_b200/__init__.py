@@ -8,14 +8,14 @@ used by the tests and bench.py.
 from .filter import (BorderPolicy, CudaConfig, CudaError, FilterParams, InvalidArgument,
                      apply_cuda, apply_cuda_band, apply_cuda_band_device, apply_cuda_batch,
                      apply_cuda_device, band_begin, band_input_rows, device_count, kernel_launches,
-                     kernel_timing, kernel_timing_read,
+                     kernel_timing, kernel_timing_read, op_counts,
                      plan_kernel, synchronize, validate, version)
 from .patterns import CONFIGS, BenchConfig, Pattern, generate, generate_device, generate_rows
 
 __all__ = [
     "BorderPolicy", "CudaConfig", "CudaError", "FilterParams", "InvalidArgument", "apply_cuda",
     "apply_cuda_band", "apply_cuda_band_device", "band_begin", "apply_cuda_batch", "apply_cuda_device",
-    "band_input_rows", "device_count", "kernel_launches", "kernel_timing", "kernel_timing_read", "plan_kernel", "synchronize",
+    "band_input_rows", "device_count", "kernel_launches", "kernel_timing", "op_counts", "kernel_timing_read", "plan_kernel", "synchronize",
     "validate", "version", "CONFIGS", "BenchConfig", "Pattern", "generate", "generate_device",
     "generate_rows",
 ]

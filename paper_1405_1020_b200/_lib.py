@@ -16,6 +16,8 @@ LIB_PATH = Path(os.environ.get("OILPAINT_B200_LIB",
 OPC_OK, OPC_EINVAL, OPC_ECUDA, OPC_ENOMEM = 0, 1, 2, 3
 OPC_FLAG_DEVICE_POINTERS = 0x1
 OPC_FLAG_ALLOW_LEVELS_256 = 0x2
+OPC_FLAG_COUNT_OPS = 0x4
+OPC_OPCOUNT_N = 8
 OPC_KERNEL_AUTO, OPC_KERNEL_DIRECT, OPC_KERNEL_SKEW, OPC_KERNEL_SLIDE, OPC_KERNEL_COLUMN = 0, 1, 2, 3, 4
 
 # Every symbol include/oilpaint_b200.h and include/oilpaint_b200_patterns.h declare.
@@ -25,6 +27,7 @@ EXPORTS = (
     "opc_kernel_launches", "opc_device_count", "opc_synchronize", "opc_plan_kernel",
     "opc_release", "opc_generate", "opc_filter_rgb8_multi", "opc_band_begin",
     "opc_generate_device", "opc_kernel_timing", "opc_kernel_timing_read", "opc_generate_rows",
+    "opc_op_counts",
 )
 
 
@@ -90,6 +93,8 @@ def _load() -> ctypes.CDLL:
     lib.opc_generate_rows.restype = ctypes.c_int
     lib.opc_generate_device.argtypes = [i32, ctypes.c_uint64, i32, i32, u8p, i32, ctypes.c_void_p]
     lib.opc_generate_device.restype = ctypes.c_int
+    lib.opc_op_counts.argtypes = [i32, ctypes.POINTER(ctypes.c_uint64), i32, i32]
+    lib.opc_op_counts.restype = ctypes.c_int
     lib.opc_kernel_timing.argtypes = [i32]
     lib.opc_kernel_timing.restype = ctypes.c_int
     lib.opc_kernel_timing_read.argtypes = [i32, ctypes.POINTER(ctypes.c_double),

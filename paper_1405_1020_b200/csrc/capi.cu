@@ -85,6 +85,7 @@ struct DevCtx {
     bool scratch_busy = false;
     int* d_counter = nullptr;
     unsigned counter_idx = 0;
+    unsigned long long* d_opcounts = nullptr;  // OPC_FLAG_COUNT_OPS accumulators (kOpCountN)
     cudaStream_t s_in = nullptr;   // H2D copies
     cudaStream_t s_out = nullptr;  // D2H copies
     std::vector<cudaEvent_t> ev_in, ev_out, ev_d2h;
@@ -413,6 +414,9 @@ int get_ctx(int device, DevCtx** out) {
         if (e != cudaSuccess) return cuda_error(e, "cudaStreamCreate");
         e = cudaMalloc(&c->d_counter, 64 * sizeof(int));
         if (e != cudaSuccess) return cuda_error(e, "cudaMalloc(counter)");
+        e = cudaMalloc(&c->d_opcounts, opc::kOpCountN * sizeof(unsigned long long));
+        if (e == cudaSuccess) e = cudaMemset(c->d_opcounts, 0, opc::kOpCountN * sizeof(unsigned long long));
+        if (e != cudaSuccess) return cuda_error(e, "cudaMalloc(op counts)");
         g_ctx[device] = std::move(c);
     }
     *out = g_ctx[device].get();
@@ -565,6 +569,7 @@ int filter_core(const std::uint8_t* in, std::uint8_t* out, int frames, int w, in
     a.radius = radius;
     a.levels = levels;
     a.bin_mul = opc::bin_multiplier(levels);
+    a.op_counts = (flags & OPC_FLAG_COUNT_OPS) ? ctx->d_opcounts : nullptr;
     const std::size_t row_bytes = static_cast<std::size_t>(w) * 3;
     const std::size_t in_bytes = row_bytes * a.in_rows;
     const std::size_t out_bytes = row_bytes * (y_end - y_begin);
@@ -1002,6 +1007,27 @@ int opc_generate_device(int32_t kind, uint64_t seed, int32_t width, int32_t heig
     return OPC_OK;
 }
 
+int opc_op_counts(int32_t device, uint64_t* out, int32_t n, int32_t reset) {
+    DevCtx* ctx = nullptr;
+    int rc = get_ctx(device, &ctx);
+    if (rc != OPC_OK) return rc;
+    if (n < 0 || n > opc::kOpCountN || (n > 0 && !out)) {
+        return set_error(OPC_EINVAL, "opc_op_counts: n must be in [0, " +
+                                         std::to_string(opc::kOpCountN) + "]");
+    }
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    cudaError_t e = cudaSetDevice(ctx->device);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    unsigned long long tmp[opc::kOpCountN] = {};
+    if (e == cudaSuccess) {
+        e = cudaMemcpy(tmp, ctx->d_opcounts, sizeof(tmp), cudaMemcpyDeviceToHost);
+    }
+    if (e == cudaSuccess && reset) e = cudaMemset(ctx->d_opcounts, 0, sizeof(tmp));
+    if (e != cudaSuccess) return cuda_error(e, "opc_op_counts");
+    for (int i = 0; i < n; ++i) out[i] = tmp[i];
+    return OPC_OK;
+}
+
 int32_t opc_plan_kernel(int32_t width, int32_t height, int32_t radius, int32_t levels) {
     if (validate_params(width, height, 3ull * width * height, radius, levels,
                         OPC_FLAG_ALLOW_LEVELS_256) != OPC_OK) {
@@ -1021,6 +1047,7 @@ void opc_release(void) {
         if (c->d_out) cudaFree(c->d_out);
         if (c->d_scratch) cudaFree(c->d_scratch);
         if (c->d_counter) cudaFree(c->d_counter);
+        if (c->d_opcounts) cudaFree(c->d_opcounts);
         if (c->stream) cudaStreamDestroy(c->stream);
         if (c->s_in) cudaStreamDestroy(c->s_in);
         if (c->s_out) cudaStreamDestroy(c->s_out);

@@ -93,6 +93,23 @@ struct BandArgs {
     int levels;
     std::uint32_t bin_mul;  // bin = umulhi(r+g+b, bin_mul) == (r+g+b)*L/765
     BorderJob border;       // fused into the first kernel of the launch
+    // Non-null (OPC_FLAG_COUNT_OPS): the content-dependent families (slide)
+    // launch their counting instantiation, which adds its executed primitive
+    // counts (OpCount indices) here -- a measurement run, never the timed one.
+    unsigned long long* op_counts;
+};
+
+// Primitive counts of a counted launch (SURVEY.md 8(d) primitives).
+enum OpCount {
+    kOpPixels = 0,       // output pixels written by the filter kernel (12 lane-ops each)
+    kOpSteps = 1,        // lane-steps of the slide (the per-step flat check, 3 lane-ops)
+    kOpUpdates = 2,      // histogram count updates executed (7 lane-ops each)
+    kOpBinsExamined = 3, // bins examined by argmax rescans (3 lane-ops each)
+    kOpSumPixels = 4,    // window pixels examined to rebuild a winner's channel sums (7 each)
+    kOpRescans = 5,      // warp-wide rescans (diagnostic)
+    kOpWinnerChanges = 6,// lanes whose winner changed (diagnostic)
+    kOpNonFlatSteps = 7, // warp-steps that applied updates (diagnostic)
+    kOpCountN = 8
 };
 
 // Exact magic multiplier for floor(s * L / 765), s in [0, 765], L in [1, 256];

@@ -166,10 +166,17 @@ __device__ __forceinline__ unsigned long long gtime() {
 }
 #endif
 
-template <int kRingCols>
+// COUNT: the measurement instantiation (OPC_FLAG_COUNT_OPS): the same
+// kernel, also counting the primitives it executes (OpCount) per lane and
+// adding them to a.op_counts at exit.
+template <int kRingCols, bool COUNT = false>
 __global__ void __launch_bounds__(kWarps * 32)
     slide_kernel(BandArgs a, const std::uint32_t* __restrict__ T, TGeom tg, int* task_counter,
                  WorkSplit g) {
+    unsigned long long opc_n[kOpCountN] = {};
+    auto tally = [&](int k, unsigned long long v) {
+        if constexpr (COUNT) opc_n[k] += v;
+    };
     extern __shared__ __align__(16) unsigned char smem[];
     std::uint32_t* recip = reinterpret_cast<std::uint32_t*>(smem);
     const int lane = threadIdx.x & 31;
@@ -278,7 +285,9 @@ __global__ void __launch_bounds__(kWarps * 32)
         if (flat0) {
             const int b0 = static_cast<int>(bin_of(e0, bm));
             cnt[b0 * 32 + lane] = static_cast<std::uint16_t>(cnt[b0 * 32 + lane] + w2 * w2 * inc);
+            tally(kOpUpdates, 1);
         } else {
+            tally(kOpUpdates, static_cast<unsigned long long>(w2) * w2);
             for (int c = 0; c < w2; ++c) {
                 const std::uint32_t* col = ringp(c);
                 for (int k = 0; k < w2; ++k) {
@@ -293,6 +302,8 @@ __global__ void __launch_bounds__(kWarps * 32)
         // ones, and swap halves at the end of each group -- half the loads and
         // one packed max per word.  Groups are combined lowest first, strict >.
         auto rescan = [&](int& best, int& bc) {
+            tally(kOpBinsExamined, static_cast<unsigned long long>(bins));
+            if (lane == 0) tally(kOpRescans, 1);
             const std::uint32_t* cw = reinterpret_cast<const std::uint32_t*>(cnt) + (lane >> 1);
             const unsigned sh = (lane & 1) * 16;
             best = 0;
@@ -313,6 +324,7 @@ __global__ void __launch_bounds__(kWarps * 32)
         };
         auto window_sums = [&](int x_rel, int best, std::uint32_t& sr, std::uint32_t& sg,
                                std::uint32_t& sb) {
+            tally(kOpSumPixels, static_cast<unsigned long long>(w2) * w2);
             sr = sg = sb = 0;
             for (int c = x_rel - r; c <= x_rel + r; ++c) {
                 const std::uint32_t* col = ringp(c + r);
@@ -353,6 +365,7 @@ __global__ void __launch_bounds__(kWarps * 32)
             const int xend = min(n, kPhase * p + kPhase);
             for (int x = kPhase * p; x < xend; ++x) {
                 if (x > 0) {
+                    tally(kOpSteps, 1);
                     // Slide: add ring column x + 2r (image x + r), remove x - 1 (image x - r - 1).
                     const std::uint32_t* cin = ringp(x + 2 * r);
                     const std::uint32_t* cout = ringp(x - 1);
@@ -364,6 +377,8 @@ __global__ void __launch_bounds__(kWarps * 32)
                     bool diff = cinb[lane] != coutb[lane];
                     if (lane < 2 * r) diff |= cinb[lane + 32] != coutb[lane + 32];
                     if (__any_sync(FULL, diff)) {
+                        tally(kOpUpdates, 2ull * w2);
+                        if (lane == 0) tally(kOpNonFlatSteps, 1);
                         const int best0 = best;
                         bool lost = false, cand = false;
                         int cand_b = 0, cand_c = 0;
@@ -421,6 +436,10 @@ __global__ void __launch_bounds__(kWarps * 32)
                         // window at a time with lane c < 2r+1 summing its column c
                         // (2r+1 loads per lane instead of (2r+1)^2 on one lane
                         // while the others wait).
+                        if (changed) {
+                            tally(kOpSumPixels, static_cast<unsigned long long>(w2) * w2);
+                            tally(kOpWinnerChanges, 1);
+                        }
                         for (unsigned todo = __ballot_sync(FULL, changed); todo; todo &= todo - 1) {
                             const int j = __ffs(todo) - 1;
                             const int bj = __shfl_sync(FULL, best, j);
@@ -448,6 +467,7 @@ __global__ void __launch_bounds__(kWarps * 32)
                     }
                 }
                 if (row_ok) {
+                    tally(kOpPixels, 1);
                     const std::uint32_t m = recip[bc];
                     const std::uint32_t rgb = __umulhi(sr << 1, m) | (__umulhi(sg << 1, m) << 8) |
                                               (__umulhi(sb << 1, m) << 16);
@@ -478,6 +498,15 @@ __global__ void __launch_bounds__(kWarps * 32)
         cp_async_wait0();
         __syncwarp();
     }
+    if constexpr (COUNT) {
+#pragma unroll
+        for (int k = 0; k < kOpCountN; ++k) {
+            unsigned long long v = opc_n[k];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(FULL, v, o);
+            if (lane == 0 && v) atomicAdd(a.op_counts + k, v);
+        }
+    }
 }
 
 }  // namespace
@@ -503,10 +532,16 @@ cudaError_t launch_slide(const BandArgs& a, int* counter, void* scratch, int num
     while (warps > 1 && kRecipBytes + warps * pw > limit) --warps;
     const std::size_t smem = kRecipBytes + warps * pw;
     const int rc = ring_cols(a.radius);
-    const void* kfn = rc == 64   ? reinterpret_cast<const void*>(slide_kernel<64>)
-                      : rc == 80 ? reinterpret_cast<const void*>(slide_kernel<80>)
-                      : rc == 88 ? reinterpret_cast<const void*>(slide_kernel<88>)
-                                 : reinterpret_cast<const void*>(slide_kernel<96>);
+    const bool count = a.op_counts != nullptr;
+    const void* kfn =
+        count ? (rc == 64   ? reinterpret_cast<const void*>(slide_kernel<64, true>)
+                 : rc == 80 ? reinterpret_cast<const void*>(slide_kernel<80, true>)
+                 : rc == 88 ? reinterpret_cast<const void*>(slide_kernel<88, true>)
+                            : reinterpret_cast<const void*>(slide_kernel<96, true>))
+              : (rc == 64   ? reinterpret_cast<const void*>(slide_kernel<64>)
+                 : rc == 80 ? reinterpret_cast<const void*>(slide_kernel<80>)
+                 : rc == 88 ? reinterpret_cast<const void*>(slide_kernel<88>)
+                            : reinterpret_cast<const void*>(slide_kernel<96>));
     cudaError_t e = set_smem_attr(kfn, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     int per_sm = 0;
@@ -539,16 +574,13 @@ cudaError_t launch_slide(const BandArgs& a, int* counter, void* scratch, int num
     if (e != cudaSuccess) return e;
     timing_mark(kIdSlide, 0, s);
     const dim3 grid(static_cast<unsigned>(blocks)), block(warps * 32);
-    if (rc == 64) {
-        slide_kernel<64><<<grid, block, smem, s>>>(a, T, tg, counter, g);
-    } else if (rc == 80) {
-        slide_kernel<80><<<grid, block, smem, s>>>(a, T, tg, counter, g);
-    } else if (rc == 88) {
-        slide_kernel<88><<<grid, block, smem, s>>>(a, T, tg, counter, g);
-    } else {
-        slide_kernel<96><<<grid, block, smem, s>>>(a, T, tg, counter, g);
-    }
+    // (the launch goes through the function pointer: the counting and the
+    // timed instantiations share the launcher)
+    void* args[] = {const_cast<BandArgs*>(&a), &T, const_cast<TGeom*>(&tg), &counter,
+                    const_cast<WorkSplit*>(&g)};
+    e = cudaLaunchKernel(kfn, grid, block, args, smem, s);
     timing_mark(kIdSlide, 1, s);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

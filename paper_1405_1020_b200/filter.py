@@ -46,6 +46,7 @@ class CudaConfig:
     stream: Optional[int] = None   # cudaStream_t handle for device-pointer calls
     kernel: int = _lib.OPC_KERNEL_AUTO
     allow_levels_256: bool = False  # documented C-ABI extension (config 3)
+    count_ops: bool = False    # measurement run: count executed primitives (op_counts())
 
     def to_c(self, device_pointers: bool = False) -> _lib.opc_config:
         flags = 0
@@ -53,6 +54,8 @@ class CudaConfig:
             flags |= _lib.OPC_FLAG_DEVICE_POINTERS
         if self.allow_levels_256:
             flags |= _lib.OPC_FLAG_ALLOW_LEVELS_256
+        if self.count_ops:
+            flags |= _lib.OPC_FLAG_COUNT_OPS
         return _lib.opc_config(self.device, flags, self.stream or 0, self.kernel, 0)
 
 
@@ -201,6 +204,18 @@ def kernel_timing_read(kernel_id: int) -> tuple[float, int]:
     n = ctypes.c_int64(0)
     _raise(LIB.opc_kernel_timing_read(kernel_id, ctypes.byref(ms), ctypes.byref(n)))
     return ms.value, n.value
+
+
+OP_COUNT_NAMES = ("pixels", "steps", "updates", "bins_examined", "sum_pixels", "rescans",
+                  "winner_changes", "nonflat_steps")
+
+
+def op_counts(device: int = -1, reset: bool = True) -> dict:
+    """Primitive counts accumulated by count_ops calls on `device` (see
+    include/oilpaint_b200.h opc_op_counts)."""
+    buf = (ctypes.c_uint64 * _lib.OPC_OPCOUNT_N)()
+    _raise(LIB.opc_op_counts(device, buf, _lib.OPC_OPCOUNT_N, 1 if reset else 0))
+    return dict(zip(OP_COUNT_NAMES, (int(v) for v in buf)))
 
 
 def device_count() -> int:
