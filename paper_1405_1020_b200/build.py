@@ -75,6 +75,30 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+def build_variant(out: Path, defines: list[str]) -> Path:
+    """An experiment build of the library with extra -D flags (A/B runs and
+    instrumented builds; load it with OILPAINT_B200_LIB=<out>).  Objects go
+    to build/var_<name>/."""
+    out = Path(out)
+    objdir = ROOT / "build" / ("var_" + out.stem)
+    objdir.mkdir(parents=True, exist_ok=True)
+    flags = [f"-D{d}" for d in defines]
+    def one(name):
+        obj = objdir / (name + ".o")
+        cmd = [_nvcc(), *NVCC_FLAGS, *flags, "-c", str(CSRC / name), "-o", str(obj)]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {name}:\n{res.stdout}\n{res.stderr}")
+        return obj
+    with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(one, SOURCES))
+    cmd = [_nvcc(), *ARCH, "-shared", "-o", str(out), *map(str, objs), "-lpthread"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")
+    return out
+
+
 TOOL_SRC = ROOT / "tools" / "oilbench_cuda.cpp"
 TOOL = ROOT / "build" / "oilbench_cuda"
 

@@ -518,8 +518,12 @@ int run_device(const opc::BandArgs& band, int border, int kernel, DevCtx* ctx, c
     // and so does the generic direct kernel.
     if (interior) {
         const bool own_border = kernel == OPC_KERNEL_DIRECT && !opc::direct_fuses_border(a);
-        g_launches.fetch_add((kernel == OPC_KERNEL_DIRECT || kernel == OPC_KERNEL_COLUMN ? 1 : 2) +
-                             (own_border && a.border.nblocks > 0 ? 1 : 0));
+        // direct / column: one kernel; skew: shear + skew; slide: transpose,
+        // plan + slide
+        const int n = kernel == OPC_KERNEL_DIRECT || kernel == OPC_KERNEL_COLUMN ? 1
+                      : kernel == OPC_KERNEL_SLIDE                                ? 3
+                                                                                  : 2;
+        g_launches.fetch_add(n + (own_border && a.border.nblocks > 0 ? 1 : 0));
     } else {
         e = opc::launch_border(a, s);
         if (e != cudaSuccess) return cuda_error(e, "border kernel launch");

@@ -17,10 +17,16 @@
 //    the window (2r+1)^2 when the winner changes; output = truncating quotient
 //    (filter.cpp:41-43) via the exact reciprocal table.
 // Pixels come from a transposed (column-major) entry plane written by the
-// shared pre-pass, so a ring column (32+2r rows) is one contiguous run that
-// cp.async copies 16 bytes at a time, one phase (kPhase columns) ahead.
+// shared pre-pass, so a ring column (32+2r rows) is one contiguous run: the
+// ring is filled by TMA (one 2D box of 16 columns x the band's rows per
+// chunk, completion on an mbarrier), two chunks ahead of the slide.  Finished
+// 16-column output blocks leave through a TMA store (the rows' 48 bytes each,
+// clipped by the hardware at the interior end and the band end).
+#include <cstdio>
+
 #include "kernels.cuh"
 #include "border.cuh"
+#include "tma.cuh"
 #include "worksplit.cuh"
 
 
@@ -46,59 +52,141 @@ namespace {
 #ifndef OPC_SLIDE_DYN_PER_WARP
 #define OPC_SLIDE_DYN_PER_WARP 2
 #endif
+#ifndef OPC_SLIDE_ATOMICS
+#define OPC_SLIDE_ATOMICS 1  // count updates of a step as shared-memory atomics (no RMW chain)
+#endif
+#ifndef OPC_SLIDE_UNROLL_CHANGE
+#define OPC_SLIDE_UNROLL_CHANGE 7  // winner-change column sums: loads in flight per lane
+#endif
+#ifndef OPC_SLIDE_PLAN
+#define OPC_SLIDE_PLAN 1  // equal-cost chunks from the column-change masks (0: static + dynamic split)
+#endif
+#ifndef OPC_SLIDE_PLAN_CPW
+#define OPC_SLIDE_PLAN_CPW 4  // planned chunks per resident warp
+#endif
+#ifndef OPC_SLIDE_COST_K
+#define OPC_SLIDE_COST_K 24  // cost of a window-changing step in flat steps (work plan)
+#endif
+#ifndef OPC_SLIDE_PAR_SUMS
+#define OPC_SLIDE_PAR_SUMS 4  // winner changes in one step from which lanes sum their windows in parallel
+#endif
 #ifndef OPC_SLIDE_STATIC_PCT
 #define OPC_SLIDE_STATIC_PCT 50  // content-dependent step costs: 90 measured 20% slower on C3
 #endif
 
 constexpr int kWarps = 8;  // upper bound; the launcher fits as many as 227 KB allows
-// Ring of entry columns: the window (2r+1) + the phase being slid + the phase
-// being fetched + the leaving column, a compile-time size so the modulo stays
-// cheap; the smaller rings for small radii fit more warps per SM (config 3,
-// r = 10: 88 columns and 16-column output staging give 6 warps instead of 5).
-#ifndef OPC_SLIDE_PHASE
-#define OPC_SLIDE_PHASE 32  // 16 (64-column ring, 7 warps/SM on C3) measured 25% slower:
-                            // a 16-column lead no longer hides the fetch latency on flat runs
-#endif
-constexpr int kPhase = OPC_SLIDE_PHASE;  // columns fetched / slid per phase
-__host__ __device__ constexpr int ring_cols(int r) {
-    return kPhase == 16 ? 64 : r <= 7 ? 80 : r <= 11 ? 88 : 96;  // >= 2r+1 + 2 kPhase + 1
-}
+// Ring of entry columns, filled by TMA in chunks of kChunk columns: kSlots
+// chunks, i.e. the window (2r+1 <= 31 columns) + the phase being slid + two
+// chunks in flight.  Column c of a pass (image column xs - r + c) lives in
+// chunk k = (c - B) / kChunk with B = 2r - kChunk * K0, K0 = ceil(2r / kChunk):
+// phase p (output columns 16p .. 16p+15) enters exactly chunk p + K0.
+constexpr int kChunk = 16;
+constexpr int kSlots = 5;
+constexpr int kRingCols = kChunk * kSlots;
 constexpr int kUnrollScan = OPC_SLIDE_UNROLL_SCAN;
 constexpr int kUnrollSums = OPC_SLIDE_UNROLL_SUMS;
-constexpr int kStageCols = 16;   // output columns staged per flush
+constexpr int kUnrollChange = OPC_SLIDE_UNROLL_CHANGE;
+constexpr int kStageCols = 16;   // output columns staged per flush (== kChunk)
 constexpr int kStageStride = 17;
 constexpr int kRecipBytes = 1024 * 4;
 constexpr int kTRows = 32;
 constexpr int kTCols = 128;
 
 __host__ __device__ inline int ring_rows(int r) { return (32 + 2 * r + 3) & ~3; }  // 16-B rows
+__host__ __device__ inline int chunk_k0(int r) { return (2 * r + kChunk - 1) / kChunk; }
 
+// Per-warp shared memory, 128-byte aligned pieces (TMA boxes):
+//   ring  kRingCols x ring_rows u32 | out tile 32 rows x 48 bytes |
+//   counts bins x 32 lanes u16 | stage 32 x kStageStride u32 | kSlots mbarriers
+__host__ __device__ inline std::size_t ring_bytes(int r) {
+    return static_cast<std::size_t>(kRingCols) * ring_rows(r) * 4;
+}
+constexpr std::size_t kOutTileBytes = 32 * 3 * kStageCols;
+__host__ __device__ inline std::size_t cnt_bytes(int bins) {
+    return ((static_cast<std::size_t>(bins) * 32 * 2) + 15) & ~std::size_t(15);
+}
 __host__ __device__ inline std::size_t per_warp_bytes(int bins, int r) {
-    const std::size_t ring = static_cast<std::size_t>(ring_cols(r)) * ring_rows(r) * 4;
-    const std::size_t cnt = ((static_cast<std::size_t>(bins) * 32 * 2) + 15) & ~std::size_t(15);
-    return ring + cnt + 32 * kStageStride * 4;
+    const std::size_t b = ring_bytes(r) + kOutTileBytes + cnt_bytes(bins) + 32 * kStageStride * 4 +
+                          kSlots * 8;
+    return (b + 127) & ~std::size_t(127);
 }
 
+// Geometry of a launch's transposed plane and of the work plan built from it.
+// Scratch layout: plane | column-change masks | nonflat bits | block costs |
+// chunk starts.
 struct TGeom {
     int y_base;
     int Hs;  // rows per column (multiple of 32)
     std::size_t frame_elems;
+    int ncols;    // plane columns: W + 64
+    int ntr;      // 32-row tiles per column: Hs / 32
+    int nbands;   // 32-row bands of the launch
+    int nblk;     // 32-column blocks per band: ceil((x_hi - x_lo) / 32)
+    int nch;      // chunks of the cost-balanced split
+    std::uint32_t* dmask;  // [frame][ntr][ncols]: bit y of (tile, column c) = plane rows
+                           // 32 tile + y of columns c and c - (2r + 1) differ
+    std::uint32_t* nf;     // [frame][nband][nblk]: bit x = step at interior column
+                           // 32 blk + x changes the window (not flat)
+    std::uint32_t* bc;     // [frame][nband][nblk]: cost of the block's columns
+    int* cs;               // [nch + 1]: first block of each chunk
 };
 
-__host__ inline TGeom tgeom(const BandArgs& a) {
+__host__ inline int plan_chunks(long long blocks, long long resident);
+
+__host__ inline TGeom tgeom(const BandArgs& a, void* scratch = nullptr, long long resident = 0) {
     TGeom g{};
     g.y_base = a.y_lo - a.radius;
-    const int nbands = (a.y_hi - a.y_lo + 31) / 32;
-    g.Hs = 32 * nbands + 64;
-    g.frame_elems = static_cast<std::size_t>(a.width + 64) * g.Hs;
+    g.nbands = (a.y_hi - a.y_lo + 31) / 32;
+    g.Hs = 32 * g.nbands + 64;
+    g.ncols = a.width + 64;
+    g.ntr = g.Hs / 32;
+    g.frame_elems = static_cast<std::size_t>(g.ncols) * g.Hs;
+    g.nblk = (a.x_hi - a.x_lo + 31) / 32;
+    const long long blocks = static_cast<long long>(a.frames) * g.nbands * g.nblk;
+    g.nch = plan_chunks(blocks, resident);
+    if (scratch) {
+        std::uint32_t* p = static_cast<std::uint32_t*>(scratch) + g.frame_elems * a.frames;
+        g.dmask = p;
+        p += static_cast<std::size_t>(a.frames) * g.ntr * g.ncols;
+        g.nf = p;
+        p += blocks;
+        g.bc = p;
+        p += blocks;
+        g.cs = reinterpret_cast<int*>(p);
+    }
     return g;
 }
 
+__host__ inline std::size_t tgeom_bytes(const BandArgs& a) {
+    const TGeom g = tgeom(a);
+    const long long blocks = static_cast<long long>(a.frames) * g.nbands * g.nblk;
+    // plan_chunks never exceeds the block count (+1 for the end marker)
+    return (g.frame_elems * a.frames + static_cast<std::size_t>(a.frames) * g.ntr * g.ncols +
+            2 * static_cast<std::size_t>(blocks) + static_cast<std::size_t>(blocks) + 2) *
+           sizeof(std::uint32_t);
+}
+
+// Chunks of the cost-balanced split: OPC_SLIDE_PLAN_CPW per resident warp, at
+// most one per 32-column block.
+__host__ inline int plan_chunks(long long blocks, long long resident) {
+    long long n = resident > 0 ? resident * OPC_SLIDE_PLAN_CPW : blocks;
+    if (n > blocks) n = blocks;
+    if (n < 1) n = 1;
+    return static_cast<int>(n);
+}
+
 // Column-major plane of raw RGB (R | G << 8 | B << 16), rows [y_base, y_base + Hs);
-// rows past the input are zero.  32x128 tiles through shared memory: each
-// column's 32 rows are one 128-byte store.
-__global__ void __launch_bounds__(256) transpose_kernel(BandArgs a, std::uint32_t* T, TGeom g) {
-    __shared__ std::uint32_t tile[kTRows * (kTCols + 1)];
+// rows past the input are zero.  32 x 128 tiles through shared memory, plus
+// 32 halo columns on the left; each column's 32 rows are one 128-byte store.
+// The same tile gives the column-change masks of the work plan: for plane
+// column c, the rows where c and c - (2r + 1) differ (a slide step at output
+// column c - r adds column c and removes column c - 2r - 1).  Interior tiles
+// load 3 words (4 pixels) per lane and row.
+constexpr int kTStride = 32 + kTCols + 1;  // odd: lane-per-row column reads hit distinct banks
+__device__ __forceinline__ std::uint32_t brg_word(std::uint32_t t) { return t & 0xFFFFFFu; }
+
+__global__ void __launch_bounds__(256) transpose_kernel(BandArgs a, std::uint32_t* T, TGeom g, int vec_ok) {
+    __shared__ std::uint32_t tile[kTRows * kTStride];
     if (static_cast<int>(blockIdx.y) >= g.Hs / kTRows) {  // appended border blocks
         const int b = (blockIdx.y - g.Hs / kTRows) * gridDim.x + blockIdx.x;
         if (b < a.border.nblocks) border_block(a, b, blockIdx.z, threadIdx.x);
@@ -112,47 +200,201 @@ __global__ void __launch_bounds__(256) transpose_kernel(BandArgs a, std::uint32_
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const std::size_t stride = static_cast<std::size_t>(a.width) * 3;
     const int in_hi = a.in_row0 + a.in_rows;
+    if (vec_ok && x0 >= 32 && x0 + kTCols <= a.width && y0 + kTRows <= in_hi) {
+        // words of pixels [x0 - 32, x0 + 128): 120 per row; lane l loads words
+        // 3l .. 3l+2 (pixels 4l .. 4l+3) and lanes < 8 also words 96 + 3l ..
 #pragma unroll
-    for (int k = 0; k < kTRows / 8; ++k) {
-        const int row = warp + 8 * k;
-        const int y = y0 + row;
+        for (int k = 0; k < kTRows / 8; ++k) {
+            const int row = warp + 8 * k;
+            const std::uint32_t* src = reinterpret_cast<const std::uint32_t*>(
+                in + static_cast<std::size_t>(y0 + row - a.in_row0) * stride +
+                static_cast<std::size_t>(x0 - 32) * 3);
+            std::uint32_t* trow = tile + row * kTStride;
 #pragma unroll
-        for (int j = 0; j < kTCols / 32; ++j) {
-            const int c = lane + 32 * j;
-            const int x = x0 + c;
-            std::uint32_t e = 0;
-            if (x < a.width && y < in_hi) {
-                const std::uint8_t* p = in + static_cast<std::size_t>(y - a.in_row0) * stride +
-                                        static_cast<std::size_t>(x) * 3;
-                e = p[0] | (static_cast<std::uint32_t>(p[1]) << 8) |
-                    (static_cast<std::uint32_t>(p[2]) << 16);
+            for (int h = 0; h < 2; ++h) {
+                const int l = lane + 32 * h;  // 4-pixel group
+                if (l < 40) {
+                    const std::uint32_t w0 = __ldg(src + 3 * l), w1 = __ldg(src + 3 * l + 1),
+                                        w2_ = __ldg(src + 3 * l + 2);
+                    // bytes R0 G0 B0 R1 | G1 B1 R2 G2 | B2 R3 G3 B3
+                    trow[4 * l + 0] = brg_word(w0);
+                    trow[4 * l + 1] = __byte_perm(w0, w1, 0x0543) & 0xFFFFFFu;  // (byte 3: zero)
+                    trow[4 * l + 2] = __byte_perm(w1, w2_, 0x0432) & 0xFFFFFFu;
+                    trow[4 * l + 3] = w2_ >> 8;
+                }
             }
-            tile[row * (kTCols + 1) + c] = e;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kTRows / 8; ++k) {
+            const int row = warp + 8 * k;
+            const int y = y0 + row;
+#pragma unroll
+            for (int j = 0; j < (32 + kTCols) / 32; ++j) {
+                const int c = lane + 32 * j;
+                const int x = x0 - 32 + c;
+                std::uint32_t e = 0;
+                if (x >= 0 && x < a.width && y < in_hi) {
+                    const std::uint8_t* p = in + static_cast<std::size_t>(y - a.in_row0) * stride +
+                                            static_cast<std::size_t>(x) * 3;
+                    e = p[0] | (static_cast<std::uint32_t>(p[1]) << 8) |
+                        (static_cast<std::uint32_t>(p[2]) << 16);
+                }
+                tile[row * kTStride + c] = e;
+            }
         }
     }
     __syncthreads();
     const int ymax = g.y_base + g.Hs;
+    const int w2 = 2 * a.radius + 1;
+    std::uint32_t* dm = g.dmask + (static_cast<std::size_t>(frame) * g.ntr + blockIdx.y) * g.ncols;
     for (int c = warp; c < kTCols; c += 8) {
         const int x = x0 + c, y = y0 + lane;
-        if (x < a.width + 64 && y < ymax) {
-            Tf[static_cast<std::size_t>(x) * g.Hs + (y - g.y_base)] = tile[lane * (kTCols + 1) + c];
+        const std::uint32_t v = tile[lane * kTStride + 32 + c];
+        const std::uint32_t m = __ballot_sync(0xFFFFFFFFu, v != tile[lane * kTStride + 32 + c - w2]);
+        if (x < g.ncols) {
+            if (y < ymax) Tf[static_cast<std::size_t>(x) * g.Hs + (y - g.y_base)] = v;
+            if (lane == 0) dm[x] = m;
         }
     }
+}
+
+// Work plan.  Step 1 (a warp per 4 blocks of 32 interior columns of a band):
+// the nonflat bit of every interior column -- a step changes the window iff
+// any of the band's 32 + 2r ring rows differs between the entering and the
+// leaving column (tile rows kb and the first 2r rows of kb + 1) -- and the
+// cost of every block: its columns + OPC_SLIDE_COST_K per nonflat step.
+// Step 2, by the last CTA to finish (threadfence + counter): the exclusive
+// prefix of the block costs and the first block of each of nch equal-cost
+// chunks (a block heavier than a chunk leaves empty chunks behind it; any
+// monotone block -> chunk map gives a valid partition, so the float scaling
+// is exact enough).
+constexpr int kCostBlocksPerWarp = 4;
+constexpr int kPlanThreads = 1024;
+constexpr long long kPlanSmemCap = 40 * 1024;  // block costs staged in shared memory (160 KB)
+__global__ void __launch_bounds__(kPlanThreads) slide_plan_kernel(BandArgs a, TGeom g, long long nblocks,
+                                                                  unsigned* done, int smem_cap) {
+    extern __shared__ std::uint32_t sbc[];  // the block costs, when they fit (smem_cap entries)
+    __shared__ std::uint32_t s_total_;
+    __shared__ bool last;
+    const int lane = threadIdx.x & 31;
+    const int nq = (g.nblk + kCostBlocksPerWarp - 1) / kCostBlocksPerWarp;
+    const long long wid = static_cast<long long>(blockIdx.x) * (kPlanThreads / 32) + (threadIdx.x >> 5);
+    const int r = a.radius;
+    if (wid < static_cast<long long>(a.frames) * g.nbands * nq) {
+        const int band = static_cast<int>(wid / nq), q = static_cast<int>(wid - static_cast<long long>(band) * nq);
+        const int f = band / g.nbands, kb = band - f * g.nbands;
+        const int iw = a.x_hi - a.x_lo;
+        const std::uint32_t low = r > 0 ? (0xFFFFFFFFu >> (32 - 2 * r)) : 0u;
+        const std::uint32_t* d0 = g.dmask + (static_cast<std::size_t>(f) * g.ntr + kb) * g.ncols;
+        const std::uint32_t* d1 = d0 + g.ncols;
+        std::uint32_t m[kCostBlocksPerWarp];
+#pragma unroll
+        for (int i = 0; i < kCostBlocksPerWarp; ++i) {
+            const int x = 32 * (kCostBlocksPerWarp * q + i) + lane;
+            const int c = a.x_lo + x + r;  // entering plane column of the step at x
+            m[i] = x < iw ? (d0[c] | (d1[c] & low)) : 0u;
+        }
+#pragma unroll
+        for (int i = 0; i < kCostBlocksPerWarp; ++i) {
+            const int j = kCostBlocksPerWarp * q + i;
+            const std::uint32_t word = __ballot_sync(0xFFFFFFFFu, m[i] != 0u);
+            if (lane == 0 && j < g.nblk) {
+                const std::size_t o = static_cast<std::size_t>(band) * g.nblk + j;
+                g.nf[o] = word;
+                g.bc[o] = static_cast<std::uint32_t>(min(32, iw - 32 * j)) + OPC_SLIDE_COST_K * __popc(word);
+            }
+        }
+    }
+    if (!OPC_SLIDE_PLAN) return;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    // ---- step 2: the last CTA ----
+#if OPC_PLAN_CLOCK
+    long long ck[8];
+    ck[0] = clock64();
+#define PLAN_TICK(i) ck[i] = clock64()
+#else
+#define PLAN_TICK(i)
+#endif
+    // The block costs are staged in shared memory when they fit (one
+    // coalesced copy through L2 -- other CTAs wrote them).
+    const int t = threadIdx.x;
+    if (t == 0) *done = 0u;  // every CTA has arrived: ready for the next launch
+    const bool staged = nblocks <= smem_cap;
+    if (staged) {
+        // (padded: entry b at b + b / 16, so 16 consecutive blocks per lane
+        // read conflict-free)
+        for (long long i = t; i < nblocks; i += kPlanThreads) sbc[i + (i >> 4)] = __ldcg(g.bc + i);
+    }
+    for (int i = t; i <= g.nch; i += kPlanThreads) g.cs[i] = static_cast<int>(nblocks);
+    __syncthreads();
+    PLAN_TICK(1);
+    auto cost = [&](long long b) -> std::uint32_t { return staged ? sbc[b + (b >> 4)] : __ldcg(g.bc + b); };
+    // Thread t owns a contiguous run of blocks [t * per, (t + 1) * per): the
+    // run sums, one CTA scan of the 1024 sums (warp shuffles + the 32 warp
+    // totals), then each thread walks its run in registers to get every
+    // block's exclusive prefix E_b.  32-bit arithmetic (totals past 2^32 are
+    // clamped) and the block -> chunk map E_b * nch / total in float: any
+    // monotone map gives a valid partition.
+    __shared__ std::uint32_t wsum[32];
+    const int w = t >> 5;
+    const long long per = (nblocks + kPlanThreads - 1) / kPlanThreads;
+    const long long b0 = min(nblocks, per * t), b1 = min(nblocks, b0 + per);
+    std::uint32_t mine = 0;
+    for (long long b = b0; b < b1; ++b) mine += cost(b);
+    std::uint32_t incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const std::uint32_t u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += u;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    if (t < 32) {
+        const std::uint32_t v = wsum[t];
+        std::uint32_t wi = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const std::uint32_t u = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+            if (t >= o) wi += u;
+        }
+        __syncwarp();
+        wsum[t] = wi - v;  // exclusive
+        if (t == 31) s_total_ = wi;
+    }
+    __syncthreads();
+    PLAN_TICK(2);
+    const std::uint32_t total = static_cast<std::uint32_t>(s_total_);
+    if (total == 0) return;
+    const float scale = static_cast<float>(g.nch) / static_cast<float>(total);
+    auto chunk_of = [&](std::uint32_t e) { return static_cast<int>(static_cast<float>(e) * scale); };
+    std::uint32_t e_b = wsum[w] + incl - mine;  // cost before b0
+    int prev = b0 == 0 ? -1 : chunk_of(e_b - cost(b0 - 1));
+    for (long long b = b0; b < b1; ++b) {
+        // block b belongs to chunk(E_b), E_b = cost before b; the chunks
+        // starting at b are (chunk(E_{b-1}), chunk(E_b)]
+        const int cur = chunk_of(e_b);
+        for (int i = prev + 1; i <= cur && i < g.nch; ++i) g.cs[i] = static_cast<int>(b);
+        prev = cur;
+        e_b += cost(b);
+    }
+    PLAN_TICK(3);
+#if OPC_PLAN_CLOCK
+    if (t == 0) {
+        printf("plan clocks: stage %lld sums %lld walk %lld\n", ck[1] - ck[0], ck[2] - ck[1], ck[3] - ck[2]);
+    }
+#endif
 }
 
 __device__ __forceinline__ std::uint32_t bin_of(std::uint32_t e, std::uint32_t bin_mul) {
     const std::uint32_t s = __dp4a(e, 0x00010101u, 0u);  // R + G + B
     return __umulhi(s, bin_mul);                          // filter.hpp:31-35
 }
-
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
-    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;"); }
-__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;"); }
-
 
 #if OPC_SLIDE_TRACE
 // Debug trace of the passes (OPC_SLIDE_TRACE builds only): per pass
@@ -168,16 +410,18 @@ __device__ __forceinline__ unsigned long long gtime() {
 
 // COUNT: the measurement instantiation (OPC_FLAG_COUNT_OPS): the same
 // kernel, also counting the primitives it executes (OpCount) per lane and
-// adding them to a.op_counts at exit.
-template <int kRingCols, bool COUNT = false>
+// adding them to a.op_counts at exit.  TMA_OUT: output blocks leave through
+// TMA stores (needs 16-byte aligned rows: width % 16 == 0); otherwise byte
+// stores.
+template <bool COUNT, bool TMA_OUT>
 __global__ void __launch_bounds__(kWarps * 32)
-    slide_kernel(BandArgs a, const std::uint32_t* __restrict__ T, TGeom tg, int* task_counter,
-                 WorkSplit g) {
+    slide_kernel(BandArgs a, TGeom tg, int* task_counter, WorkSplit g,
+                 const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout) {
     unsigned long long opc_n[kOpCountN] = {};
     auto tally = [&](int k, unsigned long long v) {
         if constexpr (COUNT) opc_n[k] += v;
     };
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];
     std::uint32_t* recip = reinterpret_cast<std::uint32_t*>(smem);
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -190,20 +434,33 @@ __global__ void __launch_bounds__(kWarps * 32)
     const int RR = ring_rows(r);
     unsigned char* wbase = smem + kRecipBytes + warp * per_warp_bytes(bins, r);
     std::uint32_t* ring = reinterpret_cast<std::uint32_t*>(wbase);
-    std::uint16_t* cnt =
-        reinterpret_cast<std::uint16_t*>(wbase + static_cast<std::size_t>(kRingCols) * RR * 4);
-    std::uint32_t* stage = reinterpret_cast<std::uint32_t*>(
-        wbase + static_cast<std::size_t>(kRingCols) * RR * 4 +
-        (((static_cast<std::size_t>(bins) * 64) + 15) & ~std::size_t(15)));
+    std::uint32_t* const ring_end = ring + kRingCols * RR;
+    std::uint8_t* otile = wbase + ring_bytes(r);
+    std::uint16_t* cnt = reinterpret_cast<std::uint16_t*>(otile + kOutTileBytes);
+    std::uint32_t* stage = reinterpret_cast<std::uint32_t*>(reinterpret_cast<unsigned char*>(cnt) +
+                                                            cnt_bytes(bins));
+    std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(stage + 32 * kStageStride);
 
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
         recip[i] = i ? 0x80000000u / static_cast<std::uint32_t>(i) + 1u : 0u;
+    }
+    if (lane == 0) {
+        for (int k = 0; k < kSlots; ++k) mbar_init(bar + k, 1);
+        fence_mbar_init();
+        if (warp == 0) {
+            prefetch_tensor_map(&tin);
+            if constexpr (TMA_OUT) prefetch_tensor_map(&tout);
+        }
     }
     __syncthreads();
 
     const std::size_t stride = static_cast<std::size_t>(a.width) * 3;
     const std::uint32_t bm = a.bin_mul;
     const unsigned FULL = 0xFFFFFFFFu;
+    const int K0 = chunk_k0(r);
+    const int B = 2 * r - kChunk * K0;  // first column of chunk 0 (<= 0)
+    const unsigned box_bytes = static_cast<unsigned>(kChunk * RR * 4);
+    unsigned q0 = 0;  // chunks this warp has issued before the current pass (slot = q % kSlots)
 
     long long u = 0, u_end = 0;
     int f, kb, x0, x1;
@@ -234,33 +491,37 @@ __global__ void __launch_bounds__(kWarps * 32)
         const int yb = a.y_lo + 32 * kb;
         const int xs = a.x_lo + x0;
         const int xe = a.x_lo + x1;
-        const int ncols = xe - xs + 2 * r;  // ring-relative columns [0, ncols]: image xs-r ..
+        const int n = xe - xs;
         const bool row_ok = yb + lane < a.y_hi;
-        const std::uint32_t* Tf = T + tg.frame_elems * f +
-                                  static_cast<std::size_t>(yb - r - tg.y_base);
+        const int row0 = yb - r - tg.y_base;  // plane row of ring row 0
         std::uint8_t* out = a.out + a.out_frame_stride * f;
-
-        // Ring column c (relative) <- image column xs - r + c, rows yb - r .. + RR.
-        auto load_chunk = [&](int c0, int n) {
-            const int pieces = RR / 4;
-            for (int i = lane; i < n * pieces; i += 32) {
-                const int c = c0 + i / pieces;
-                const int q = i - (i / pieces) * pieces;
-                if (c > ncols) continue;
-                const std::uint32_t* src =
-                    Tf + static_cast<std::size_t>(xs - r + c) * tg.Hs + q * 4;
-                cp_async16(ring + (c % kRingCols) * RR + q * 4, src);
-            }
+        // chunks of this pass: columns up to n - 1 + 2r
+        const int kmax = (n - 1 + 2 * r - B) / kChunk;
+        // ring position (u32 offset) of pass column c: chunk (c - B) / 16 in
+        // slot (q0 + chunk) % kSlots -- i.e. (16 * (q0 % kSlots) + c - B) mod 80
+        const int pos0 = kChunk * static_cast<int>(q0 % kSlots) - B;
+        auto ringp = [&](int c) { return ring + ((pos0 + c) % kRingCols) * RR + lane; };
+        auto issue = [&](int k) {  // lane 0: chunk k of the pass
+            const unsigned q = q0 + static_cast<unsigned>(k);
+            std::uint64_t* b = bar + q % kSlots;
+            mbar_arrive_expect_tx(b, box_bytes);
+            tma_load_3d(ring + (q % kSlots) * kChunk * RR, &tin, row0, xs - r + B + kChunk * k, f, b);
         };
-        auto ringp = [&](int c) { return ring + (c % kRingCols) * RR + lane; };
-
-        // First window: columns [0, w2) plus phase 0's entering columns.
-        load_chunk(0, w2 + kPhase);
-        cp_async_commit();
-        load_chunk(w2 + kPhase, kPhase);
-        cp_async_commit();
-        cp_async_wait1();
+        auto wait = [&](int k) {
+            const unsigned q = q0 + static_cast<unsigned>(k);
+            mbar_wait(bar + q % kSlots, (q / kSlots) & 1u);
+        };
+        // The ring's previous contents were last read before this point
+        // (same warp); order those generic reads before the TMA writes.
+        fence_proxy_async_smem();
         __syncwarp();
+        const int kfirst = min(kmax, kSlots - 1);
+        if (lane == 0) {
+            for (int k = 0; k <= kfirst; ++k) issue(k);
+        }
+        int kissued = kfirst;
+        for (int k = 0; k <= min(K0, kmax); ++k) wait(k);
+        int kwaited = min(K0, kmax);
 
         // Counts are kept as keys count << kb_ | (G-1 - b mod G), G = 2^kb_ bins,
         // so within a group of G bins the largest key is the lowest-index
@@ -275,11 +536,11 @@ __global__ void __launch_bounds__(kWarps * 32)
         // Fast path: the first windows of all lanes lie in ring columns
         // [0, 2r] x rows [0, 32 + 2r); when that block is one colour (flat
         // content, config 3) every lane's window is (2r+1)^2 copies of it.
-        const std::uint32_t e0 = ring[0];
+        const std::uint32_t e0 = *(ringp(0) - lane);
         bool uni = true;
-        for (int i = lane; i < w2 * (32 + 2 * r); i += 32) {
-            const int c = i / (32 + 2 * r), k = i - c * (32 + 2 * r);
-            uni &= ring[c * RR + k] == e0;  // ring columns 0..2r: no wrap
+        for (int c = 0; c < w2; ++c) {
+            const std::uint32_t* col = ringp(c) - lane;
+            for (int k = lane; k < 32 + 2 * r; k += 32) uni &= col[k] == e0;
         }
         const bool flat0 = __all_sync(FULL, uni);
         if (flat0) {
@@ -288,46 +549,75 @@ __global__ void __launch_bounds__(kWarps * 32)
             tally(kOpUpdates, 1);
         } else {
             tally(kOpUpdates, static_cast<unsigned long long>(w2) * w2);
+            // (shared-memory atomics on the word holding this lane's u16 count:
+            // no read-modify-write chain through the counts)
+            std::uint32_t* const cw32 = reinterpret_cast<std::uint32_t*>(cnt) + (lane >> 1);
+            const unsigned add = inc << ((lane & 1) * 16);
             for (int c = 0; c < w2; ++c) {
                 const std::uint32_t* col = ringp(c);
-                for (int k = 0; k < w2; ++k) {
-                    const std::uint32_t bn = bin_of(col[k], bm);
-                    cnt[bn * 32 + lane] = static_cast<std::uint16_t>(cnt[bn * 32 + lane] + inc);
-                }
+#pragma unroll 7
+                for (int k = 0; k < w2; ++k) atomicAdd(cw32 + bin_of(col[k], bm) * 16, add);
             }
+            __syncwarp();
         }
         // Full scan for the lowest-index maximum (filter.hpp:71-82), all lanes
         // together: lanes 2k and 2k+1 read the 32-bit words holding both their
         // counts of one bin, the even lane the even bins, the odd lane the odd
         // ones, and swap halves at the end of each group -- half the loads and
         // one packed max per word.  Groups are combined lowest first, strict >.
-        auto rescan = [&](int& best, int& bc) {
+        // The rescan also returns U, the largest count of any other bin (the
+        // top two keys per lane half, packed u16x2 min/max): a later step
+        // whose winner lost pixels keeps it without a rescan while its count
+        // stays above U (U grows with the other bins' increments).
+        auto rescan = [&](int& best, int& bc, int& ub) {
             tally(kOpBinsExamined, static_cast<unsigned long long>(bins));
             if (lane == 0) tally(kOpRescans, 1);
             const std::uint32_t* cw = reinterpret_cast<const std::uint32_t*>(cnt) + (lane >> 1);
             const unsigned sh = (lane & 1) * 16;
             best = 0;
             bc = -1;
+            ub = 0;
             for (int g0 = 0; g0 < bins; g0 += gsize) {
                 const int gend = min(bins, g0 + gsize);
-                std::uint32_t m = 0;
+                std::uint32_t m = 0, m2 = 0;
 #pragma unroll kUnrollScan
-                for (int b = g0 + (lane & 1); b < gend; b += 2) m = __vmaxu2(m, cw[b * 16]);
+                for (int b = g0 + (lane & 1); b < gend; b += 2) {
+                    const std::uint32_t v = cw[b * 16];
+                    m2 = __vmaxu2(m2, __vminu2(m, v));
+                    m = __vmaxu2(m, v);
+                }
                 const std::uint32_t o = __shfl_xor_sync(FULL, m, 1);
-                const std::uint32_t key = max((m >> sh) & 0xFFFFu, (o >> sh) & 0xFFFFu);
+                const std::uint32_t o2 = __shfl_xor_sync(FULL, m2, 1);
+                const std::uint32_t k1 = (m >> sh) & 0xFFFFu, k1o = (o >> sh) & 0xFFFFu;
+                const std::uint32_t key = max(k1, k1o);
+                const std::uint32_t key2 = max(min(k1, k1o), max((m2 >> sh) & 0xFFFFu, (o2 >> sh) & 0xFFFFu));
                 const int c = static_cast<int>(key >> kb_);
+                const int c2 = static_cast<int>(key2 >> kb_);
                 if (c > bc) {
+                    ub = max(ub, max(bc, c2));
                     bc = c;
                     best = g0 + static_cast<int>(gmask - (key & gmask));
+                } else {
+                    ub = max(ub, c);
                 }
             }
         };
-        auto window_sums = [&](int x_rel, int best, std::uint32_t& sr, std::uint32_t& sg,
-                               std::uint32_t& sb) {
+        int best, bc, ub;  // winner, its count, an upper bound of every other bin's count
+        std::uint32_t sr, sg, sb;
+        if (flat0) {
+            const std::uint32_t n0 = static_cast<std::uint32_t>(w2 * w2);
+            best = static_cast<int>(bin_of(e0, bm));
+            bc = w2 * w2;
+            ub = 0;
+            sr = n0 * (e0 & 0xFFu);
+            sg = n0 * ((e0 >> 8) & 0xFFu);
+            sb = n0 * ((e0 >> 16) & 0xFFu);
+        } else {
+            rescan(best, bc, ub);
             tally(kOpSumPixels, static_cast<unsigned long long>(w2) * w2);
             sr = sg = sb = 0;
-            for (int c = x_rel - r; c <= x_rel + r; ++c) {
-                const std::uint32_t* col = ringp(c + r);
+            for (int c = 0; c < w2; ++c) {
+                const std::uint32_t* col = ringp(c);
 #pragma unroll kUnrollSums
                 for (int k = 0; k < w2; ++k) {
                     const std::uint32_t e = col[k];
@@ -338,114 +628,157 @@ __global__ void __launch_bounds__(kWarps * 32)
                     }
                 }
             }
-        };
-        int best, bc;
-        std::uint32_t sr, sg, sb;
-        if (flat0) {
-            const std::uint32_t n0 = static_cast<std::uint32_t>(w2 * w2);
-            best = static_cast<int>(bin_of(e0, bm));
-            bc = w2 * w2;
-            sr = n0 * (e0 & 0xFFu);
-            sg = n0 * ((e0 >> 8) & 0xFFu);
-            sb = n0 * ((e0 >> 16) & 0xFFu);
-        } else {
-            rescan(best, bc);
-            window_sums(0, best, sr, sg, sb);
         }
+        // the output of the current window (recomputed only after a step
+        // that changed the window: a flat step repeats the previous pixel)
+        auto quotient = [&]() {
+            const std::uint32_t m = recip[bc];
+            return __umulhi(sr << 1, m) | (__umulhi(sg << 1, m) << 8) | (__umulhi(sb << 1, m) << 16);
+        };
+        std::uint32_t rgb = quotient();
 
-        int n = xe - xs;
-        for (int p = 0; kPhase * p < n; ++p) {
-            if (p > 0) {
-                // Phase p's entering columns were requested a phase ago; request p+1's.
-                load_chunk(w2 + kPhase * (p + 1), kPhase);
-                cp_async_commit();
-                cp_async_wait1();
-                __syncwarp();
+        // entering column x + 2r and leaving column x - 1 of step x, as ring
+        // pointers advanced by one column per step (the leaving pointer wraps)
+        const std::uint32_t* cin = ringp(2 * r);
+        const std::uint32_t* cout = ringp(kRingCols - 1);  // column -1 (unused at x = 0)
+        // nonflat bits of this band (work plan): bit x of word j = the step at
+        // interior column 32 j + x changes the window
+        const std::uint32_t* nfb = tg.nf + (static_cast<std::size_t>(f) * tg.nbands + kb) * tg.nblk;
+        for (int p = 0; kStageCols * p < n; ++p) {
+            std::uint32_t nfm;  // bit i: the step at pass column 16p + i is not flat
+            {
+                const int xi = x0 + kStageCols * p;
+                const int j = xi >> 5;
+                const std::uint32_t lo = nfb[j];
+                const std::uint32_t hi = j + 1 < tg.nblk ? nfb[j + 1] : 0u;
+                nfm = __funnelshift_r(lo, hi, xi & 31);
             }
-            const int xend = min(n, kPhase * p + kPhase);
-            for (int x = kPhase * p; x < xend; ++x) {
+            if (p > 0) {
+                // phase p enters chunk p + K0; the slot of chunk p - 1 is free:
+                // request chunk p + kSlots - 1
+                if (p + K0 > kwaited) {
+                    wait(p + K0);
+                    kwaited = p + K0;
+                }
+                if (p + kSlots - 1 <= kmax) {
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) issue(p + kSlots - 1);
+                    kissued = p + kSlots - 1;
+                }
+            }
+            const int xend = min(n, kStageCols * p + kStageCols);
+            for (int x = kStageCols * p; x < xend; ++x) {
                 if (x > 0) {
                     tally(kOpSteps, 1);
                     // Slide: add ring column x + 2r (image x + r), remove x - 1 (image x - r - 1).
-                    const std::uint32_t* cin = ringp(x + 2 * r);
-                    const std::uint32_t* cout = ringp(x - 1);
                     // Warp-wide flat check: the lanes' windows cover ring rows
-                    // 0 .. 31 + 2r, two rows per lane (was 2r+1 per lane: 23% of
-                    // the kernel's stall samples on C3).
-                    const std::uint32_t* cinb = cin - lane;
-                    const std::uint32_t* coutb = cout - lane;
-                    bool diff = cinb[lane] != coutb[lane];
-                    if (lane < 2 * r) diff |= cinb[lane + 32] != coutb[lane + 32];
-                    if (__any_sync(FULL, diff)) {
+                    // 0 .. 31 + 2r, two rows per lane.
+                    bool nonflat;
+                    if (OPC_SLIDE_PLAN) {
+                        nonflat = (nfm >> (x - kStageCols * p)) & 1u;
+                    } else {
+                        const std::uint32_t* cinb = cin - lane;
+                        const std::uint32_t* coutb = cout - lane;
+                        bool diff = cinb[lane] != coutb[lane];
+                        if (lane < 2 * r) diff |= cinb[lane + 32] != coutb[lane + 32];
+                        nonflat = __any_sync(FULL, diff);
+                    }
+                    if (nonflat) {
                         tally(kOpUpdates, 2ull * w2);
                         if (lane == 0) tally(kOpNonFlatSteps, 1);
                         const int best0 = best;
-                        bool lost = false, cand = false;
-                        int cand_b = 0, cand_c = 0;
+                        int cand_c = -1;  // the largest post-increment count of another bin
                         // Branch-free form: every row pays two count updates (of
                         // zero when the pixel does not change bin), so lanes whose
                         // changes sit at different rows do not diverge.
+                        // (atomics: the two updates of a row are shared-memory
+                        // atomics on the 32-bit word holding this lane's u16 count,
+                        // so the rows' updates are in flight together instead of
+                        // one read-modify-write chain; same-address atomics of a
+                        // thread apply in order, and a count never drops below
+                        // its key, so no borrow crosses into the other lane's half)
+                        std::uint32_t* const cw32 = reinterpret_cast<std::uint32_t*>(cnt) + (lane >> 1);
+                        const unsigned csh = (lane & 1) * 16;
                         for (int k = 0; k < w2; ++k) {
                             const std::uint32_t ei = cin[k], eo = cout[k];
                             const int bi = bin_of(ei, bm), bo = bin_of(eo, bm);
                             const bool mv = bi != bo;
                             const unsigned d = mv ? inc : 0u;
-                            const unsigned ki = cnt[bi * 32 + lane] + d;
-                            cnt[bi * 32 + lane] = static_cast<std::uint16_t>(ki);
-                            cnt[bo * 32 + lane] = static_cast<std::uint16_t>(cnt[bo * 32 + lane] - d);
+                            unsigned ki;
+                            if (OPC_SLIDE_ATOMICS) {
+                                const unsigned old = atomicAdd(cw32 + bi * 16, d << csh);
+                                atomicSub(cw32 + bo * 16, d << csh);
+                                ki = ((old >> csh) & 0xFFFFu) + d;
+                            } else {
+                                ki = cnt[bi * 32 + lane] + d;
+                                cnt[bi * 32 + lane] = static_cast<std::uint16_t>(ki);
+                                cnt[bo * 32 + lane] = static_cast<std::uint16_t>(cnt[bo * 32 + lane] - d);
+                            }
                             const int ci = static_cast<int>(ki >> kb_);
-                            lost |= mv && bo == best0;
-                            const bool better = mv && (ci > cand_c || (ci == cand_c && bi < cand_b));
-                            cand_b = better ? bi : cand_b;
-                            cand_c = better ? ci : cand_c;
-                            cand |= better;
+                            cand_c = (mv && bi != best0) ? max(cand_c, ci) : cand_c;
                             const std::uint32_t mi = bi == best0 ? 0xFFFFFFFFu : 0u;
                             const std::uint32_t mo = bo == best0 ? 0xFFFFFFFFu : 0u;
                             sr += (ei & mi & 0xFFu) - (eo & mo & 0xFFu);
                             sg += ((ei & mi) >> 8 & 0xFFu) - ((eo & mo) >> 8 & 0xFFu);
                             sb += ((ei & mi) >> 16 & 0xFFu) - ((eo & mo) >> 16 & 0xFFu);
                         }
-                        // Resolve the winner (filter.hpp:71-82).
+                        // Resolve the winner (filter.hpp:71-82): it stays while its
+                        // count is above every other bin's (bounded by ub);
+                        // otherwise a rescan finds the lowest-index maximum.
+                        ub = max(ub, cand_c);
                         const int bcf = cnt[best0 * 32 + lane] >> kb_;
-                        bool changed = false, need = false;
-                        if (lost && bcf < bc) {
-                            need = true;
-                        } else {
-                            bc = bcf;
-                            if (cand) {
-                                const int cf = cnt[cand_b * 32 + lane] >> kb_;
-                                if (cf < cand_c) {
-                                    need = true;
-                                } else if (cf > bc || (cf == bc && cand_b < best)) {
-                                    best = cand_b;
-                                    bc = cf;
-                                    changed = true;
-                                }
-                            }
-                        }
+                        bool changed = false;
+                        const bool need = bcf <= ub;
+                        if (!need) bc = bcf;
                         if (__any_sync(FULL, need)) {
-                            int nb, nc;
-                            rescan(nb, nc);
+                            int nb, nc, nu;
+                            rescan(nb, nc, nu);
                             if (need) {
                                 best = nb;
                                 bc = nc;
+                                ub = nu;
                                 changed = best != best0;
                             }
+                        }
+                        if (changed) {
+                            tally(kOpSumPixels, static_cast<unsigned long long>(w2) * w2);
+                            tally(kOpWinnerChanges, 1);
                         }
                         // Winner changed: the new winner's window sums, one lane's
                         // window at a time with lane c < 2r+1 summing its column c
                         // (2r+1 loads per lane instead of (2r+1)^2 on one lane
                         // while the others wait).
-                        if (changed) {
-                            tally(kOpSumPixels, static_cast<unsigned long long>(w2) * w2);
-                            tally(kOpWinnerChanges, 1);
+                        const unsigned chg = __ballot_sync(FULL, changed);
+                        if (__popc(chg) >= OPC_SLIDE_PAR_SUMS) {
+                            // many lanes changed at once (an edge crossing all
+                            // rows): each sums its own window, in parallel
+                            if (changed) {
+                                std::uint32_t cr = 0, cg = 0, cbb = 0;
+                                for (int c = 0; c < w2; ++c) {
+                                    const std::uint32_t* col = ringp(x + c);
+#pragma unroll kUnrollSums
+                                    for (int k = 0; k < w2; ++k) {
+                                        const std::uint32_t e = col[k];
+                                        if (static_cast<int>(bin_of(e, bm)) == best) {
+                                            cr += e & 0xFFu;
+                                            cg += (e >> 8) & 0xFFu;
+                                            cbb += (e >> 16) & 0xFFu;
+                                        }
+                                    }
+                                }
+                                sr = cr;
+                                sg = cg;
+                                sb = cbb;
+                            }
                         }
-                        for (unsigned todo = __ballot_sync(FULL, changed); todo; todo &= todo - 1) {
+                        for (unsigned todo = __popc(chg) >= OPC_SLIDE_PAR_SUMS ? 0u : chg; todo; todo &= todo - 1) {
                             const int j = __ffs(todo) - 1;
                             const int bj = __shfl_sync(FULL, best, j);
                             std::uint32_t cr = 0, cg = 0, cbb = 0;
                             if (lane < w2) {
-                                const std::uint32_t* col = ring + ((x + lane) % kRingCols) * RR + j;
+                                const std::uint32_t* col = ringp(x + lane) - lane + j;
+#pragma unroll kUnrollChange
                                 for (int k = 0; k < w2; ++k) {
                                     const std::uint32_t e = col[k];
                                     if (static_cast<int>(bin_of(e, bm)) == bj) {
@@ -464,39 +797,78 @@ __global__ void __launch_bounds__(kWarps * 32)
                                 sb = cbb;
                             }
                         }
+                        rgb = quotient();
                     }
                 }
-                if (row_ok) {
-                    tally(kOpPixels, 1);
-                    const std::uint32_t m = recip[bc];
-                    const std::uint32_t rgb = __umulhi(sr << 1, m) | (__umulhi(sg << 1, m) << 8) |
-                                              (__umulhi(sb << 1, m) << 16);
-                    stage[lane * kStageStride + (x & (kStageCols - 1))] = rgb;
-                }
-                if ((x & (kStageCols - 1)) == kStageCols - 1 || x == n - 1) {  // flush the block
+                if (row_ok) tally(kOpPixels, 1);
+                // Output blocks are 16 image columns [16m, 16m + 15] (a TMA
+                // store box must start 16-byte aligned: 48m bytes); the partial
+                // blocks at the ends of a pass are written with byte stores.
+                const int xa = xs + x;
+                stage[lane * kStageStride + (xa & (kStageCols - 1))] = rgb;
+                if ((xa & (kStageCols - 1)) == kStageCols - 1 || x == n - 1) {  // flush the block
                     __syncwarp();
-                    const int xb = x & ~(kStageCols - 1);
-                    const int cols = x - xb + 1;
-                    const int c = lane & (kStageCols - 1);
-                    for (int f0 = 0; f0 < 32; f0 += 32 / kStageCols) {  // 2 rows per store
-                        const int fr = f0 + lane / kStageCols;
-                        if (yb + f0 >= a.y_hi) break;
-                        if (c < cols && yb + fr < a.y_hi) {
-                            const std::uint32_t rgb = stage[fr * kStageStride + c];
-                            std::uint8_t* o = out +
-                                              static_cast<std::size_t>(yb + fr - a.out_row0) * stride +
-                                              static_cast<std::size_t>(xs + xb + c) * 3;
-                            o[0] = static_cast<std::uint8_t>(rgb);
-                            o[1] = static_cast<std::uint8_t>(rgb >> 8);
-                            o[2] = static_cast<std::uint8_t>(rgb >> 16);
+                    const int xb = xa & ~(kStageCols - 1);      // image column of stage column 0
+                    const int c_lo = max(xs, xb) - xb;          // valid stage columns [c_lo, c_hi]
+                    const int c_hi = xa - xb;
+                    if (TMA_OUT && c_lo == 0 && c_hi == kStageCols - 1) {
+                        // lane t packs row t's 16 pixels into 48 bytes of the out
+                        // tile; one TMA store writes the 32 x 48-byte box (rows
+                        // past the band end are clipped by the tensor map)
+                        if (lane == 0) bulk_wait_read0();  // the previous store has read the tile
+                        __syncwarp();
+                        const std::uint32_t* srow = stage + lane * kStageStride;
+                        std::uint32_t wv[12];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {  // pixels 4j .. 4j+3 -> words 3j .. 3j+2
+                            const std::uint32_t p0 = srow[4 * j], p1 = srow[4 * j + 1],
+                                                p2 = srow[4 * j + 2], p3 = srow[4 * j + 3];
+                            wv[3 * j] = p0 | (p1 << 24);
+                            wv[3 * j + 1] = (p1 >> 8) | (p2 << 16);
+                            wv[3 * j + 2] = (p2 >> 16) | (p3 << 8);
+                        }
+                        uint4* orow = reinterpret_cast<uint4*>(otile + lane * 48);
+                        orow[0] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                        orow[1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
+                        orow[2] = make_uint4(wv[8], wv[9], wv[10], wv[11]);
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tma_store_3d(&tout, otile, 3 * xb, yb - a.out_row0, f);
+                            bulk_commit();
+                        }
+                    } else {
+                        const int c = lane & (kStageCols - 1);
+                        for (int f0 = 0; f0 < 32; f0 += 32 / kStageCols) {  // 2 rows per store
+                            const int fr = f0 + lane / kStageCols;
+                            if (yb + f0 >= a.y_hi) break;
+                            if (c >= c_lo && c <= c_hi && yb + fr < a.y_hi) {
+                                const std::uint32_t v = stage[fr * kStageStride + c];
+                                std::uint8_t* o = out +
+                                                  static_cast<std::size_t>(yb + fr - a.out_row0) * stride +
+                                                  static_cast<std::size_t>(xb + c) * 3;
+                                o[0] = static_cast<std::uint8_t>(v);
+                                o[1] = static_cast<std::uint8_t>(v >> 8);
+                                o[2] = static_cast<std::uint8_t>(v >> 16);
+                            }
                         }
                     }
                     __syncwarp();
                 }
+                cin += RR;
+                cout += RR;
+                if (cout >= ring_end) cout -= kRingCols * RR;
+                if (cin >= ring_end) cin -= kRingCols * RR;
             }
         }
-        cp_async_wait0();
+        // chunks requested but not consumed: wait, so no TMA write lands in
+        // the next pass's ring and the slot parities stay in step
+        for (int k = kwaited + 1; k <= kissued; ++k) wait(k);
+        q0 += static_cast<unsigned>(kissued + 1);
         __syncwarp();
+    }
+    if constexpr (TMA_OUT) {
+        if (lane == 0) bulk_wait0();
     }
     if constexpr (COUNT) {
 #pragma unroll
@@ -519,7 +891,7 @@ bool slide_supported(int levels, int radius) {
 
 std::size_t slide_scratch_bytes(const BandArgs& a) {
     if (a.y_hi <= a.y_lo || a.x_hi <= a.x_lo) return 0;
-    return tgeom(a).frame_elems * a.frames * sizeof(std::uint32_t);
+    return tgeom_bytes(a);
 }
 
 cudaError_t launch_slide(const BandArgs& a, int* counter, void* scratch, int num_sms,
@@ -531,53 +903,103 @@ cudaError_t launch_slide(const BandArgs& a, int* counter, void* scratch, int num
     int warps = kWarps;
     while (warps > 1 && kRecipBytes + warps * pw > limit) --warps;
     const std::size_t smem = kRecipBytes + warps * pw;
-    const int rc = ring_cols(a.radius);
+
+    const std::size_t row_bytes = static_cast<std::size_t>(a.width) * 3;
+    bool tma_out = row_bytes % 16 == 0 && a.out_frame_stride % 16 == 0 &&
+                   reinterpret_cast<std::uintptr_t>(a.out) % 16 == 0;
     const bool count = a.op_counts != nullptr;
-    const void* kfn =
-        count ? (rc == 64   ? reinterpret_cast<const void*>(slide_kernel<64, true>)
-                 : rc == 80 ? reinterpret_cast<const void*>(slide_kernel<80, true>)
-                 : rc == 88 ? reinterpret_cast<const void*>(slide_kernel<88, true>)
-                            : reinterpret_cast<const void*>(slide_kernel<96, true>))
-              : (rc == 64   ? reinterpret_cast<const void*>(slide_kernel<64>)
-                 : rc == 80 ? reinterpret_cast<const void*>(slide_kernel<80>)
-                 : rc == 88 ? reinterpret_cast<const void*>(slide_kernel<88>)
-                            : reinterpret_cast<const void*>(slide_kernel<96>));
-    cudaError_t e = set_smem_attr(kfn, static_cast<int>(smem));
+    // (TMA_OUT decided below; both variants get their attributes set)
+    const void* kfn_t = count ? reinterpret_cast<const void*>(slide_kernel<true, true>)
+                              : reinterpret_cast<const void*>(slide_kernel<false, true>);
+    const void* kfn_b = count ? reinterpret_cast<const void*>(slide_kernel<true, false>)
+                              : reinterpret_cast<const void*>(slide_kernel<false, false>);
+    cudaError_t e = set_smem_attr(kfn_t, static_cast<int>(smem));
+    if (e == cudaSuccess) e = set_smem_attr(kfn_b, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = blocks_per_sm(kfn, warps * 32, smem, &per_sm);
+    e = blocks_per_sm(kfn_t, warps * 32, smem, &per_sm);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    const long long resident = static_cast<long long>(num_sms) * per_sm * warps;
 
-    const TGeom tg = tgeom(a);
+    const TGeom tg = tgeom(a, scratch, resident);
     std::uint32_t* T = static_cast<std::uint32_t*>(scratch);
+    // TMA maps: the transposed plane (rows, columns, frames) read in boxes of
+    // ring_rows x 16 columns; the output (bytes of the interior columns, rows
+    // up to the band's interior end, frames) written in 48-byte x 32-row boxes.
+    CUtensorMap tin{}, tout{};
     {
-        const unsigned gx = static_cast<unsigned>((a.width + 64 + kTCols - 1) / kTCols);
+        const cuuint64_t dims[3] = {static_cast<cuuint64_t>(tg.Hs), static_cast<cuuint64_t>(tg.ncols),
+                                    static_cast<cuuint64_t>(a.frames)};
+        const cuuint64_t strides[2] = {static_cast<cuuint64_t>(tg.Hs) * 4,
+                                       static_cast<cuuint64_t>(tg.frame_elems) * 4};
+        const cuuint32_t box[3] = {static_cast<cuuint32_t>(ring_rows(a.radius)),
+                                   static_cast<cuuint32_t>(kChunk), 1};
+        if (encode_tensor_map(&tin, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, T, dims, strides, box) != 0) {
+            return cudaErrorInvalidValue;
+        }
+    }
+    if (tma_out) {
+        const cuuint64_t dims[3] = {static_cast<cuuint64_t>(a.x_hi) * 3,
+                                    static_cast<cuuint64_t>(a.y_hi - a.out_row0),
+                                    static_cast<cuuint64_t>(a.frames)};
+        const cuuint64_t strides[2] = {static_cast<cuuint64_t>(row_bytes),
+                                       static_cast<cuuint64_t>(a.out_frame_stride)};
+        const cuuint32_t box[3] = {3 * kStageCols, 32, 1};
+        tma_out = encode_tensor_map(&tout, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, a.out, dims, strides,
+                                    box) == 0;
+    }
+    const void* kfn = tma_out ? kfn_t : kfn_b;
+
+    // Pre-pass and work plan: the transposed plane with its column-change
+    // masks (border job appended), the nonflat bits and block costs, the
+    // equal-cost chunk starts.
+    e = cudaMemsetAsync(counter, 0, 4 * sizeof(int), s);
+    if (e != cudaSuccess) return e;
+    timing_mark(kIdPrePass, 0, s);
+    {
+        const unsigned gx = static_cast<unsigned>((tg.ncols + kTCols - 1) / kTCols);
         const dim3 grid(gx, static_cast<unsigned>(tg.Hs / kTRows) + border_grid_rows(a, gx),
                         static_cast<unsigned>(a.frames));
-        timing_mark(kIdPrePass, 0, s);
-        transpose_kernel<<<grid, 256, 0, s>>>(a, T, tg);
-        timing_mark(kIdPrePass, 1, s);
+        const int vec_ok = (reinterpret_cast<std::uintptr_t>(a.in) % 4 == 0) && (row_bytes % 4 == 0) &&
+                           (a.in_frame_stride % 4 == 0);
+        transpose_kernel<<<grid, 256, 0, s>>>(a, T, tg, vec_ok);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
-    const long long resident = static_cast<long long>(num_sms) * per_sm * warps;
-    // Each pass pays a full window build, rescan and window sums (~3(2r+1)^2 +
-    // L updates per lane): keep chunks >= 128 columns.
-    const WorkSplit g = make_split(a.frames, (a.y_hi - a.y_lo + 31) / 32, a.x_hi - a.x_lo, resident,
-                                   OPC_SLIDE_STATIC_PCT, OPC_SLIDE_MIN_CHUNK, OPC_SLIDE_DYN_PER_WARP,
-                                   OPC_SLIDE_GUIDED_K);
+    const long long nblocks = static_cast<long long>(a.frames) * tg.nbands * tg.nblk;
+    {
+        const long long nq = (tg.nblk + kCostBlocksPerWarp - 1) / kCostBlocksPerWarp;
+        const long long nwarps = static_cast<long long>(a.frames) * tg.nbands * nq;
+        const long long ctas = (nwarps + kPlanThreads / 32 - 1) / (kPlanThreads / 32);
+        // counter[1]: the plan kernel's done count (zeroed with the task
+        // counter before the pre-pass)
+        // block costs staged in shared memory by the last CTA when they fit
+        const int cap = static_cast<int>(std::min<long long>(nblocks, kPlanSmemCap));
+        const int bytes = (cap + cap / 16 + 1) * 4;  // (padded layout)
+        e = set_smem_attr(reinterpret_cast<const void*>(slide_plan_kernel), bytes);
+        if (e != cudaSuccess) return e;
+        slide_plan_kernel<<<static_cast<unsigned>(ctas), kPlanThreads, bytes, s>>>(
+            a, tg, nblocks, reinterpret_cast<unsigned*>(counter) + 1, cap);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    timing_mark(kIdPrePass, 1, s);
+    const WorkSplit g =
+        OPC_SLIDE_PLAN
+            ? make_planned_split(a.frames, tg.nbands, a.x_hi - a.x_lo, tg.nblk, 32, tg.nch, tg.cs)
+            : make_split(a.frames, tg.nbands, a.x_hi - a.x_lo, resident, OPC_SLIDE_STATIC_PCT,
+                         OPC_SLIDE_MIN_CHUNK, OPC_SLIDE_DYN_PER_WARP, OPC_SLIDE_GUIDED_K);
     long long blocks = (g.nchunks + warps - 1) / warps;
     if (blocks > static_cast<long long>(num_sms) * per_sm) blocks = num_sms * per_sm;
     if (blocks < 1) blocks = 1;
-    e = cudaMemsetAsync(counter, 0, 4 * sizeof(int), s);
-    if (e != cudaSuccess) return e;
     timing_mark(kIdSlide, 0, s);
     const dim3 grid(static_cast<unsigned>(blocks)), block(warps * 32);
-    // (the launch goes through the function pointer: the counting and the
-    // timed instantiations share the launcher)
-    void* args[] = {const_cast<BandArgs*>(&a), &T, const_cast<TGeom*>(&tg), &counter,
-                    const_cast<WorkSplit*>(&g)};
+    // (through the function pointer: the four instantiations share the launcher)
+    BandArgs aa = a;
+    TGeom tgg = tg;
+    WorkSplit gg = g;
+    void* args[] = {&aa, &tgg, &counter, &gg, &tin, &tout};
     e = cudaLaunchKernel(kfn, grid, block, args, smem, s);
     timing_mark(kIdSlide, 1, s);
     if (e != cudaSuccess) return e;

@@ -39,7 +39,29 @@ struct WorkSplit {
     // guided_div) -- large first, small at the end -- for kernels whose step
     // cost depends on the content (slide), where equal chunks leave a tail.
     long long guided_div;
+    // Planned mode (cs != nullptr, device memory): chunk i is the unit range
+    // [cs[i] * blk, cs[i + 1] * blk) -- chunk boundaries computed on the device
+    // from the content (the slide kernel's equal-cost split), blk units per
+    // block, pitch = blocks per band * blk.
+    const int* cs;
+    int blk;
 };
+
+// The planned split (see WorkSplit::cs): nchunks chunks over frames x nbands
+// bands of nblk blocks of blk units (the last block of a band may be partial).
+inline WorkSplit make_planned_split(int frames, int nbands, int iw, int nblk, int blk, int nchunks,
+                                    const int* cs) {
+    WorkSplit g{};
+    g.nbands = nbands;
+    g.iw = iw;
+    g.pitch = nblk * blk;
+    g.units = static_cast<long long>(frames) * nbands * g.pitch;
+    g.nstatic = 0;
+    g.nchunks = nchunks;
+    g.cs = cs;
+    g.blk = blk;
+    return g;
+}
 
 inline WorkSplit make_split(int frames, int nbands, int iw, long long resident, int static_pct,
                             long long min_chunk, int dyn_per_warp = 2, int guided_k = 0) {
@@ -90,7 +112,10 @@ inline WorkSplit make_split(int frames, int nbands, int iw, long long resident, 
 
 // Units [u, u_end) of chunk i (i < nchunks).
 OPC_HD inline void chunk_range(const WorkSplit& g, int i, long long& u, long long& u_end) {
-    if (i < g.nstatic) {
+    if (g.cs) {
+        u = static_cast<long long>(g.cs[i]) * g.blk;
+        u_end = static_cast<long long>(g.cs[i + 1]) * g.blk;
+    } else if (i < g.nstatic) {
         u = static_cast<long long>(i) * g.s1;
         u_end = u + g.s1;
     } else {
