@@ -464,7 +464,8 @@ __global__ void __launch_bounds__(kWarps * 32)
 
     long long u = 0, u_end = 0;
     int f, kb, x0, x1;
-    while (next_pass<(OPC_SLIDE_GUIDED_K > 0)>(g, task_counter, lane, u, u_end, f, kb, x0, x1)) {
+    while (next_pass<(OPC_SLIDE_GUIDED_K > 0), (OPC_SLIDE_PLAN != 0)>(g, task_counter, lane, u, u_end, f, kb,
+                                                                       x0, x1)) {
 #if OPC_SLIDE_TRACE
         int pass_cols = x1 - x0;
         const unsigned long long t_start = gtime();
