@@ -574,7 +574,38 @@ def run_b200(args, wl) -> None:
     # achieved = algorithmic lane-ops of the timed steps / time inside the
     # dominant kernel (its launches, CUDA events on the launch stream)
     kernel_ms = kernel_total_ms / max(1, kernel_n)
-    achieved_ops = ops_px * interior * args.steps / (kernel_total_ms / 1e3)
+    ops_per_step = ops_px * interior
+    model_label = (f"{model_name} {ops_px} lane-ops per interior pixel (SURVEY 8d best fit, "
+                   f"B={L + 1})")
+    executed = None
+    if family == 3:
+        # The slide family adapts to the content (flat steps skip their
+        # updates, the argmax rescans only when the winner may have changed),
+        # so a per-pixel model overstates its work.  Its op count is what one
+        # counting launch of the same step on the same input executed
+        # (OPC_FLAG_COUNT_OPS, outside the timed region), priced with SURVEY
+        # 8(d)'s primitive costs.
+        cnt_cfg = opc.CudaConfig(device=local, stream=stream.cuda_stream,
+                                 allow_levels_256=(L == 256), count_ops=True)
+        opc.op_counts(local, reset=True)
+        with torch.cuda.stream(stream):
+            if F == 1:
+                opc.apply_cuda_band_device(dev_in.data_ptr(), dev_out.data_ptr(), W, H, y0, y1,
+                                           params, cnt_cfg)
+            else:
+                opc.apply_cuda_device(dev_in.data_ptr(), dev_out.data_ptr(), W, H, params,
+                                      cnt_cfg, frames=my_frames)
+        stream.synchronize()
+        executed = opc.op_counts(local, reset=True)
+        ops_per_step = (12 * executed["pixels"] + 3 * executed["steps"] +
+                        7 * executed["updates"] + 3 * executed["bins_examined"] +
+                        7 * executed["sum_pixels"])
+        model_label = ("slide, executed primitives of one counted launch (OPC_FLAG_COUNT_OPS): "
+                       "12 x pixels + 3 x lane-steps + 7 x count updates + 3 x bins examined "
+                       "by rescans + 7 x window pixels summed on winner changes (SURVEY 8d "
+                       f"costs); the best-fit per-pixel model ({model_name} {ops_px}/px) would "
+                       f"be {ops_px * interior} per launch")
+    achieved_ops = ops_per_step * args.steps / (kernel_total_ms / 1e3)
     step_total_ms = sum(step_ms)
     traffic = None
     tp = ROOT / "profiles" / f"{cfg.name}_dram_bytes.json"
@@ -586,21 +617,23 @@ def run_b200(args, wl) -> None:
         "bound": "issue", "achieved": round(achieved_ops / 1e12, 3),
         "peak": round(peak_ops / 1e12, 3), "unit": "Tlane-op/s",
         "frac": round(achieved_ops / peak_ops, 4), "traffic": traffic,
-        "model": f"{model_name} {ops_px} lane-ops per interior pixel (SURVEY 8d best fit, B={L + 1}); "
+        "model": f"{model_label}; "
                  f"{num_sms} SMs x 4 x 32 x {sm_mhz:.0f} MHz ({peaks_kind} sm_max_mhz)",
-        "algorithmic_ops_per_launch": ops_px * interior * args.steps // max(1, kernel_n),
+        "algorithmic_ops_per_launch": ops_per_step * args.steps // max(1, kernel_n),
         "kernel": {1: "direct", 2: "skew", 3: "slide", 4: "column"}.get(family, str(family)),
         "kernel_ms": round(kernel_ms, 4),
         "kernel_launches": kernel_n,
         "step_share": {"kernel": round(kernel_total_ms / step_total_ms, 4),
                        "pre_pass_and_border": round(pre_ms / step_total_ms, 4),
                        "border_alone": round(border_ms / step_total_ms, 4)},
-        "frac_of_step": round(ops_px * interior * args.steps / (step_total_ms / 1e3) / peak_ops, 4),
+        "frac_of_step": round(ops_per_step * args.steps / (step_total_ms / 1e3) / peak_ops, 4),
         "hbm": {"achieved_gbs": round(alg_bytes * args.steps / (step_total_ms / 1e3) / 1e9, 1),
                 "peak_gbs": hbm_gbs,
                 "frac": round(alg_bytes * args.steps / (step_total_ms / 1e3) / 1e9 / hbm_gbs, 4),
                 "bytes_per_launch": alg_bytes, "peak_kind": peaks_kind},
     }
+    if executed is not None:
+        roofline["executed_counts"] = executed
     if world > 1:
         roofline["note"] = "rank 0's kernel and band; job value is max over ranks"
 

@@ -65,6 +65,7 @@ extern "C" {
 #define OPC_KERNEL_SKEW 2   /* warp-skewed column-difference sliding, L+1 <= 32, r <= 15 */
 #define OPC_KERNEL_SLIDE 3  /* per-lane O(r) sliding histogram, any L, r <= 15 (L+1 > 32 default) */
 #define OPC_KERNEL_COLUMN 4 /* per-thread column-segment sliding, L+1 <= 32, r <= 7 (small images) */
+#define OPC_KERNEL_PLANES 5 /* bit-plane counts + column-sum histograms per warp, L+1 <= 32, 1 <= r <= 7 */
 
 typedef struct opc_config {
     int32_t device;  /* CUDA device ordinal; -1 = current device              */
@@ -136,13 +137,14 @@ int opc_synchronize(const opc_config* cfg);
  * opc_kernel_timing(1) starts (and clears), opc_kernel_timing(0) stops;
  * opc_kernel_timing_read sums the recorded launches of one kernel
  * (synchronizing on their events).  Ids: 1 direct, 2 skew, 3 slide, 4 the
- * pre-pass (shear / transpose), 5 border, 6 column. */
+ * pre-pass (shear / transpose), 5 border, 6 column, 7 planes. */
 #define OPC_KID_DIRECT 1
 #define OPC_KID_SKEW 2
 #define OPC_KID_SLIDE 3
 #define OPC_KID_PREPASS 4
 #define OPC_KID_BORDER 5
 #define OPC_KID_COLUMN 6
+#define OPC_KID_PLANES 7
 int opc_kernel_timing(int32_t enable);
 int opc_kernel_timing_read(int32_t kernel_id, double* ms_total, int64_t* launches);
 

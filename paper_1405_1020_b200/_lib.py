@@ -19,6 +19,7 @@ OPC_FLAG_ALLOW_LEVELS_256 = 0x2
 OPC_FLAG_COUNT_OPS = 0x4
 OPC_OPCOUNT_N = 8
 OPC_KERNEL_AUTO, OPC_KERNEL_DIRECT, OPC_KERNEL_SKEW, OPC_KERNEL_SLIDE, OPC_KERNEL_COLUMN = 0, 1, 2, 3, 4
+OPC_KERNEL_PLANES = 5
 
 # Every symbol include/oilpaint_b200.h and include/oilpaint_b200_patterns.h declare.
 EXPORTS = (
@@ -32,6 +33,7 @@ EXPORTS = (
 
 
 OPC_KID_DIRECT, OPC_KID_SKEW, OPC_KID_SLIDE, OPC_KID_PREPASS, OPC_KID_BORDER, OPC_KID_COLUMN = 1, 2, 3, 4, 5, 6
+OPC_KID_PLANES = 7
 
 
 class opc_config(ctypes.Structure):

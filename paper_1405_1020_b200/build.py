@@ -23,7 +23,7 @@ LIB = PKG / "liboilpaint_b200.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
               "--expt-relaxed-constexpr", "-I", str(ROOT / "include")] + ARCH
-SOURCES = ["capi.cu", "direct.cu", "column.cu", "skew.cu", "slide.cu", "gen.cu", "patterns.cpp"]
+SOURCES = ["capi.cu", "direct.cu", "column.cu", "planes.cu", "skew.cu", "slide.cu", "gen.cu", "patterns.cpp"]
 
 
 def _nvcc() -> str:

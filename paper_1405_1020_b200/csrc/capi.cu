@@ -447,6 +447,9 @@ int plan(int levels, int radius, int forced, long long interior_px) {
     if (forced == OPC_KERNEL_SLIDE) {
         return opc::slide_supported(levels, radius) ? OPC_KERNEL_SLIDE : -1;
     }
+    if (forced == OPC_KERNEL_PLANES) {
+        return opc::planes_supported(levels, radius) ? OPC_KERNEL_PLANES : -1;
+    }
     // Small images: the column family, while its per-pixel cost (~ 2r+1
     // updates per pixel) stays below the skew family's fill-bound launch
     // (scripts/size_sweep.py on one B200, noise, L = 20: column wins up to
@@ -509,6 +512,9 @@ int run_device(const opc::BandArgs& band, int border, int kernel, DevCtx* ctx, c
     } else if (kernel == OPC_KERNEL_COLUMN) {
         e = opc::launch_column(a, ctx->num_sms, s);
         if (e != cudaSuccess) return cuda_error(e, "column kernel launch");
+    } else if (kernel == OPC_KERNEL_PLANES) {
+        e = opc::launch_planes(a, ctx->num_sms, s);
+        if (e != cudaSuccess) return cuda_error(e, "planes kernel launch");
     } else {
         e = opc::launch_direct(a, s);
         if (e != cudaSuccess) return cuda_error(e, "direct kernel launch");
@@ -520,7 +526,9 @@ int run_device(const opc::BandArgs& band, int border, int kernel, DevCtx* ctx, c
         const bool own_border = kernel == OPC_KERNEL_DIRECT && !opc::direct_fuses_border(a);
         // direct / column: one kernel; skew: shear + skew; slide: transpose,
         // plan + slide
-        const int n = kernel == OPC_KERNEL_DIRECT || kernel == OPC_KERNEL_COLUMN ? 1
+        const int n = kernel == OPC_KERNEL_DIRECT || kernel == OPC_KERNEL_COLUMN ||
+                              kernel == OPC_KERNEL_PLANES
+                          ? 1
                       : kernel == OPC_KERNEL_SLIDE                                ? 3
                                                                                   : 2;
         g_launches.fetch_add(n + (own_border && a.border.nblocks > 0 ? 1 : 0));

@@ -50,7 +50,9 @@ inline cudaError_t blocks_per_sm(const void* func, int threads, std::size_t smem
 // Live kernel timing (opc_kernel_timing in the C-ABI): when a hook is set, the
 // launchers call it right before (phase 0) and after (phase 1) each kernel
 // launch, on the launch's stream, and the C-ABI records CUDA events there.
-enum KernelId { kIdDirect = 1, kIdSkew = 2, kIdSlide = 3, kIdPrePass = 4, kIdBorder = 5, kIdColumn = 6 };
+enum KernelId {
+    kIdDirect = 1, kIdSkew = 2, kIdSlide = 3, kIdPrePass = 4, kIdBorder = 5, kIdColumn = 6, kIdPlanes = 7
+};
 using TimingHook = void (*)(int id, int phase, cudaStream_t s);
 extern TimingHook g_timing_hook;
 inline void timing_mark(int id, int phase, cudaStream_t s) {
@@ -126,6 +128,10 @@ cudaError_t launch_border(const BandArgs& a, cudaStream_t s);
 // Column family (small images): L + 1 <= 32, radius <= 7; border fused.
 bool column_supported(int levels, int radius);
 cudaError_t launch_column(const BandArgs& a, int num_sms, cudaStream_t s);
+
+// Bit-plane column family: L + 1 <= 32, 1 <= radius <= 7; border fused.
+bool planes_supported(int levels, int radius);
+cudaError_t launch_planes(const BandArgs& a, int num_sms, cudaStream_t s);
 
 // Skew family: L + 1 <= 32, radius <= 15.  `task_counter` is a device int
 // (zeroed by the launcher on the stream).

@@ -1,0 +1,439 @@
+// planes.cu -- the bit-plane column family (L+1 <= 32, r <= 7): window counts
+// as bit planes in registers, channel sums from per-warp column histograms.
+//
+// The column family (column.cu) keeps every thread's window histogram in
+// shared memory and pays two 32-bit read-modify-writes per updated pixel
+// (2(2r+1) per output row): ~166 shared-memory wavefronts per 32 pixels on
+// config 2, which bounds it at the L1 data pipe (profiles/r01_c2_column_ncu.md).
+// Here the same vertical slide is split in two:
+//
+//  * COUNTS, bit-sliced in registers.  Bit k of plane word Wk holds bit k of
+//    the count of bin b at bit position b (<= 32 bins, one bit each).  The
+//    row histogram of the entering window row (2r+1 one-hot masks 1 << bin)
+//    is a carry-save adder tree (XOR3 / MAJ, one LOP3 each: 16 for 11 masks);
+//    the window counts advance by W += RH(y+r+1) - RH(y-r) with the leaving
+//    row's planes kept in a register ring of 2r+1 slots (the row loop is
+//    unrolled by 2r+1).  The lowest-index bin with the largest count
+//    (filter.hpp:71-82) falls out of a walk down the planes from the top:
+//    keep the candidates that have bit k set if any does -- the survivors are
+//    the bins with the maximum count, the lowest one is __ffs, and the taken
+//    branches spell the count.  No shared memory, no dynamic indexing.
+//
+//  * SUMS of the winning bin only, from column histograms.  Each warp owns 32
+//    output columns; its 32 + 2r input columns keep per-bin channel sums over
+//    the current 2r+1 window rows, CS[bin][column] = (R, G << 16 | B) in two
+//    [bin][64] u32 arrays (r <= 7: column sums < 2^12, window sums < 2^16).
+//    Per output row a lane updates its column (and one halo column if lane <
+//    2r): minus the leaving pixel, plus the entering one -- and then reads
+//    the winner's 2r+1 column sums CS[best][x .. x+2r]: with a 64-word bin
+//    pitch lane l always reads bank (l + j) mod 32, conflict-free whatever
+//    the bins of the lanes.
+//
+// Per output pixel (r = 5): 11 mask loads, 22 column-sum loads, ~8 shared
+// RMW words, ~150 ALU ops; against ~166 wavefronts and ~520 instructions per
+// pixel of the column kernel (profiles/r01_c2_column_ncu.md).
+//
+// Truncating quotient per channel (filter.cpp:41-43): umulhi(2*sum, m_c),
+// m_c = floor(2^31/c) + 1 (exact for c <= 1023, sum <= 255c; checked
+// exhaustively by tests/test_oracle.py::test_reciprocal_division_exact).
+// The border pixels of the launch ride on extra blocks (border.cuh).
+#include "kernels.cuh"
+#include "border.cuh"
+
+#include <algorithm>
+
+#ifndef OPC_PLANES_THMAX
+#define OPC_PLANES_THMAX 64  // rows per block when the image needs several rounds of blocks
+#endif
+
+namespace opc {
+
+namespace {
+
+constexpr int kPlWarps = 4;
+constexpr int kPlThreads = 32 * kPlWarps;
+constexpr int kPlCols = 32 * kPlWarps;  // output columns per block
+constexpr int kPlMaxR = 7;
+constexpr int kPlPitch = 64;            // CS words per bin row: >= 32 + 2r, a multiple of 32
+
+struct PlGeom {
+    int th;  // output rows per block
+    int nb;  // bins (L + 1)
+};
+
+template <int R>
+__host__ __device__ constexpr int pl_planes() {
+    // bits of the largest window count (2R+1)^2
+    int n = (2 * R + 1) * (2 * R + 1), p = 0;
+    while (n) {
+        ++p;
+        n >>= 1;
+    }
+    return p;
+}
+
+template <int R>
+__host__ __device__ constexpr int pl_tile_cols() {
+    return kPlCols + 2 * R;
+}
+
+template <int R>
+__host__ inline std::size_t pl_smem_bytes(const PlGeom& g) {
+    const std::size_t cs = static_cast<std::size_t>(kPlWarps) * g.nb * kPlPitch * 8;
+    const std::size_t tile = static_cast<std::size_t>(pl_tile_cols<R>()) * (g.th + 2 * R) * 4;
+    const std::size_t recip = static_cast<std::size_t>((2 * R + 1) * (2 * R + 1) + 1) * 4;
+    return cs + tile + ((recip + 15) & ~std::size_t(15));
+}
+
+// Tile entry of one pixel: bin | R << 8 | G << 16 | B << 24.
+__device__ __forceinline__ std::uint32_t pl_hi(std::uint32_t e) { return __byte_perm(e, 0u, 0x4441); }  // R
+__device__ __forceinline__ std::uint32_t pl_lo(std::uint32_t e) { return __byte_perm(e, 0u, 0x4243); }  // G << 16 | B
+__device__ __forceinline__ std::uint32_t pl_mask(std::uint32_t e) { return 1u << (e & 31u); }
+
+__device__ __forceinline__ std::uint32_t maj3(std::uint32_t a, std::uint32_t b, std::uint32_t c) {
+    return (a & b) | (a & c) | (b & c);
+}
+
+// Carry-save adder tree: N signals of weight 2^K (bit-sliced one-hot masks or
+// carries) reduced into plane K of q and N/2 carries of weight 2^(K+1).
+template <int N, int K, int NP>
+struct Csa {
+    __device__ __forceinline__ static void run(const std::uint32_t* in, std::uint32_t (&q)[NP]) {
+        constexpr int NC = N / 2;
+        std::uint32_t c[NC];
+        std::uint32_t s = in[0];
+#pragma unroll
+        for (int i = 1, k = 0; i < N; i += 2, ++k) {
+            if (i + 1 < N) {  // full adder
+                const std::uint32_t x = in[i], y = in[i + 1];
+                c[k] = maj3(s, x, y);
+                s = s ^ x ^ y;
+            } else {  // half adder
+                c[k] = s & in[i];
+                s ^= in[i];
+            }
+        }
+        q[K] = s;
+        Csa<NC, K + 1, NP>::run(c, q);
+    }
+};
+template <int K, int NP>
+struct Csa<1, K, NP> {
+    __device__ __forceinline__ static void run(const std::uint32_t* in, std::uint32_t (&q)[NP]) {
+        q[K] = in[0];
+#pragma unroll
+        for (int k = K + 1; k < NP; ++k) q[k] = 0u;
+    }
+};
+template <int K, int NP>
+struct Csa<0, K, NP> {
+    __device__ __forceinline__ static void run(const std::uint32_t*, std::uint32_t (&q)[NP]) {
+#pragma unroll
+        for (int k = K; k < NP; ++k) q[k] = 0u;
+    }
+};
+
+// Row histogram (4 planes: counts <= 15) of the 2R+1 entries at row[0 .. 2R].
+template <int R>
+__device__ __forceinline__ void row_planes(const std::uint32_t* row, std::uint32_t (&q)[4]) {
+    constexpr int W2 = 2 * R + 1;
+    std::uint32_t m[W2];
+#pragma unroll
+    for (int j = 0; j < W2; ++j) m[j] = pl_mask(row[j]);
+    Csa<W2, 0, 4>::run(m, q);
+}
+
+// w += d (d: 4 planes), modulo 2^P per bin.
+template <int P>
+__device__ __forceinline__ void planes_add(std::uint32_t (&w)[P], const std::uint32_t (&d)[4]) {
+    std::uint32_t c = 0u;
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+        const std::uint32_t x = k < 4 ? d[k] : 0u, a = w[k];
+        w[k] = a ^ x ^ c;
+        c = maj3(a, x, c);
+    }
+}
+
+// w += a - d in one pass: w + a + ~d + 1, a carry-save layer (planes >= 4
+// of a are 0 and of ~d are 1: sum ~w, carry w) and one ripple with carry-in 1.
+template <int P>
+__device__ __forceinline__ void planes_update(std::uint32_t (&w)[P], const std::uint32_t (&a)[4],
+                                              const std::uint32_t (&d)[4]) {
+    std::uint32_t s[P], c[P + 1];
+    c[0] = 0u;
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+        const std::uint32_t x = w[k], y = k < 4 ? a[k] : 0u, z = k < 4 ? ~d[k] : 0xFFFFFFFFu;
+        s[k] = x ^ y ^ z;
+        c[k + 1] = maj3(x, y, z);
+    }
+    std::uint32_t cin = 0xFFFFFFFFu;
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+        const std::uint32_t x = s[k], y = c[k];
+        w[k] = x ^ y ^ cin;
+        cin = maj3(x, y, cin);
+    }
+}
+
+// w -= d: w + ~d + 1.
+template <int P>
+__device__ __forceinline__ void planes_sub(std::uint32_t (&w)[P], const std::uint32_t (&d)[4]) {
+    std::uint32_t c = 0xFFFFFFFFu;
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+        const std::uint32_t x = k < 4 ? ~d[k] : 0xFFFFFFFFu, a = w[k];
+        w[k] = a ^ x ^ c;
+        c = maj3(a, x, c);
+    }
+}
+
+template <int R>
+__global__ void __launch_bounds__(kPlThreads) planes_kernel(BandArgs a, PlGeom g) {
+    constexpr int W2 = 2 * R + 1;
+    constexpr int P = pl_planes<R>();
+    constexpr int TW = pl_tile_cols<R>();
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int main_rows = (a.y_hi - a.y_lo + g.th - 1) / g.th;
+    if (static_cast<int>(blockIdx.y) >= main_rows) {  // appended border blocks (256-thread jobs)
+        const int b = (blockIdx.y - main_rows) * gridDim.x + blockIdx.x;
+        if (b < a.border.nblocks) {
+            border_block(a, b, blockIdx.z, tid);
+            border_block(a, b, blockIdx.z, tid + kPlThreads);
+        }
+        return;
+    }
+    const int nb = g.nb;
+    const int TR = g.th + 2 * R;
+    uint2* cs_all = reinterpret_cast<uint2*>(smem);  // [warp][nb][64] (R, G << 16 | B)
+    std::uint32_t* tile = reinterpret_cast<std::uint32_t*>(cs_all + kPlWarps * nb * kPlPitch);  // [TR][TW]
+    std::uint32_t* recip = tile + TR * TW;
+    recip = reinterpret_cast<std::uint32_t*>((reinterpret_cast<std::uintptr_t>(recip) + 15) & ~std::uintptr_t(15));
+
+    const int x0 = a.x_lo + blockIdx.x * kPlCols;  // first output column of the block
+    const int y0 = a.y_lo + blockIdx.y * g.th;     // first output row of the block
+    const int frame = blockIdx.z;
+    const std::size_t stride = static_cast<std::size_t>(a.width) * 3;
+    const std::uint8_t* in = a.in + a.in_frame_stride * frame;
+    const int in_last = a.in_row0 + a.in_rows - 1;
+
+    // ---- tile: (TR rows) x (TW columns) entries, input rows y0-R .., columns
+    // x0-R ..; columns past the image and rows past the band are clamped (they
+    // only feed outputs that are not stored) ----
+    {
+        constexpr int kBatch = 8;
+        const int n = TR * TW;
+        for (int i0 = tid; i0 < n; i0 += kBatch * kPlThreads) {
+            std::uint32_t R_[kBatch], G_[kBatch], B_[kBatch];
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) {
+                const int i = min(i0 + j * kPlThreads, n - 1);
+                const int ty = i / TW, tx = i - ty * TW;
+                const int x = min(x0 - R + tx, a.width - 1);
+                const int y = min(y0 - R + ty, in_last);
+                const std::uint8_t* q = in + static_cast<std::size_t>(y - a.in_row0) * stride + static_cast<std::size_t>(x) * 3;
+                R_[j] = q[0];
+                G_[j] = q[1];
+                B_[j] = q[2];
+            }
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) {
+                const int i = i0 + j * kPlThreads;
+                if (i < n) {
+                    tile[i] = __umulhi(R_[j] + G_[j] + B_[j], a.bin_mul) | (R_[j] << 8) | (G_[j] << 16) |
+                              (B_[j] << 24);
+                }
+            }
+        }
+    }
+    constexpr int nrec = W2 * W2 + 1;
+    for (int i = tid; i < nrec; i += kPlThreads) recip[i] = i ? 0x80000000u / static_cast<std::uint32_t>(i) + 1u : 0u;
+    uint2* cs = cs_all + warp * nb * kPlPitch;
+    for (int i = lane; i < nb * kPlPitch; i += 32) cs[i] = make_uint2(0u, 0u);
+    __syncthreads();
+
+    const int nrows = min(g.th, a.y_hi - y0);  // warp-uniform
+    if (nrows <= 0) return;
+    // lane's window: tile columns c0 .. c0 + 2R, its own CS column c0 (and the
+    // halo column c0 + 32 for lanes < 2R)
+    const int c0 = warp * 32 + lane;
+    const bool halo = lane < 2 * R;
+    const std::uint32_t* trow = tile + c0;  // tile row 0, the lane's window start
+
+    // ---- first window: tile rows 0 .. 2R ----
+    std::uint32_t ring[W2][4];
+    std::uint32_t w[P];
+#pragma unroll
+    for (int k = 0; k < P; ++k) w[k] = 0u;
+#pragma unroll
+    for (int i = 0; i < W2; ++i) {
+        row_planes<R>(trow + i * TW, ring[i]);
+        planes_add<P>(w, ring[i]);
+    }
+#pragma unroll 1
+    for (int i = 0; i < W2; ++i) {
+        const std::uint32_t e = trow[i * TW];
+        uint2& v = cs[(e & 31u) * kPlPitch + lane];
+        v.x += pl_hi(e);
+        v.y += pl_lo(e);
+        if (halo) {
+            const std::uint32_t eh = trow[i * TW + 32];
+            uint2& vh = cs[(eh & 31u) * kPlPitch + lane + 32];
+            vh.x += pl_hi(eh);
+            vh.y += pl_lo(eh);
+        }
+    }
+    __syncwarp();
+
+    const int x = x0 + lane + warp * 32;
+    const bool store = x < a.x_hi;
+    std::uint8_t* o = a.out + a.out_frame_stride * frame +
+                      static_cast<std::size_t>(y0 - a.out_row0) * stride + static_cast<std::size_t>(x) * 3;
+    const uint2* csl = cs + lane;
+
+    // output row k of the block from the current planes and column sums
+    auto emit = [&](int k) {
+        std::uint32_t cand = 0xFFFFFFFFu, cnt = 0u;
+#pragma unroll
+        for (int p = P - 1; p >= 0; --p) {
+            const std::uint32_t t = cand & w[p];
+            const bool nz = t != 0u;
+            cand = nz ? t : cand;
+            cnt = (cnt << 1) | (nz ? 1u : 0u);
+        }
+        const uint2* pb = csl + (__ffs(cand) - 1) * kPlPitch;
+        std::uint32_t sr = 0u, sgb = 0u;
+#pragma unroll
+        for (int j = 0; j < W2; ++j) {
+            const uint2 v = pb[j];
+            sr += v.x;
+            sgb += v.y;
+        }
+        const std::uint32_t m = recip[cnt];
+        if (store) {
+            std::uint8_t* q = o + static_cast<std::size_t>(k) * stride;
+            q[0] = static_cast<std::uint8_t>(__umulhi(sr << 1, m));
+            q[1] = static_cast<std::uint8_t>(__umulhi((sgb >> 16) << 1, m));
+            q[2] = static_cast<std::uint8_t>(__umulhi((sgb & 0xFFFFu) << 1, m));
+        }
+    };
+
+    emit(0);
+    if (nrows <= 1) return;
+    // ---- slide down: output row k's window is tile rows k .. k + 2R.  The
+    // entries of step k (entering row k + 2R: the lane's 2R+1 window columns
+    // and its halo column; leaving row k - 1: its own and halo column) are
+    // loaded one step ahead, before the step's warp syncs ----
+    std::uint32_t ent[W2], eh, el, elh;
+    {
+        const std::uint32_t* erow = trow + (1 + 2 * R) * TW;
+#pragma unroll
+        for (int j = 0; j < W2; ++j) ent[j] = erow[j];
+        eh = halo ? erow[32] : 0u;  // (column c0 + 32 exists for halo lanes only)
+        el = trow[0];
+        elh = halo ? trow[32] : 0u;
+    }
+    int k = 1;
+    for (;;) {
+#pragma unroll
+        for (int s = 0; s < W2; ++s) {  // ring slot s holds tile row k - 1 (k - 1 == s mod W2)
+            std::uint32_t rin[4];
+            {
+                std::uint32_t m[W2];
+#pragma unroll
+                for (int j = 0; j < W2; ++j) m[j] = pl_mask(ent[j]);
+                Csa<W2, 0, 4>::run(m, rin);
+            }
+            planes_update<P>(w, rin, ring[s]);
+#pragma unroll
+            for (int p = 0; p < 4; ++p) ring[s][p] = rin[p];
+            const std::uint32_t ee = ent[0], ehe = eh, el0 = el, elh0 = elh;
+            const bool more = k + 1 < nrows;
+            if (more) {  // next step's entries
+                const std::uint32_t* erow = trow + (k + 1 + 2 * R) * TW;
+#pragma unroll
+                for (int j = 0; j < W2; ++j) ent[j] = erow[j];
+                eh = halo ? erow[32] : 0u;
+                el = trow[k * TW];
+                elh = halo ? trow[k * TW + 32] : 0u;
+            }
+            __syncwarp();  // every lane has read the previous row's column sums
+            {
+                uint2& vl = cs[(el0 & 31u) * kPlPitch + lane];
+                vl.x -= pl_hi(el0);
+                vl.y -= pl_lo(el0);
+                uint2& ve = cs[(ee & 31u) * kPlPitch + lane];
+                ve.x += pl_hi(ee);
+                ve.y += pl_lo(ee);
+                if (halo) {
+                    uint2& hl = cs[(elh0 & 31u) * kPlPitch + lane + 32];
+                    hl.x -= pl_hi(elh0);
+                    hl.y -= pl_lo(elh0);
+                    uint2& he = cs[(ehe & 31u) * kPlPitch + lane + 32];
+                    he.x += pl_hi(ehe);
+                    he.y += pl_lo(ehe);
+                }
+            }
+            __syncwarp();  // column sums of row k complete
+            emit(k);
+            ++k;
+            if (!more) return;
+        }
+    }
+}
+
+template <int R>
+cudaError_t launch_r(const BandArgs& a, int num_sms, cudaStream_t s) {
+    PlGeom g{};
+    g.nb = a.levels + 1;
+    const long long iw = a.x_hi - a.x_lo, ih = a.y_hi - a.y_lo;
+    const long long bx = (iw + kPlCols - 1) / kPlCols;
+    // rows per block: one round of resident blocks when the image is small
+    // (the first window's (2r+1) rows are amortised over as many rows as
+    // possible), OPC_PLANES_THMAX rows per block otherwise
+    int bps = 4;
+    for (; bps > 1; --bps) {
+        long long th = (bx * ih * a.frames + static_cast<long long>(num_sms) * bps - 1) /
+                       (static_cast<long long>(num_sms) * bps);
+        g.th = static_cast<int>(std::max(4ll, std::min<long long>(OPC_PLANES_THMAX, th)));
+        if (pl_smem_bytes<R>(g) * bps + bps * 1024 <= 228u * 1024) break;
+    }
+    if (bps == 1) {
+        long long th = (bx * ih * a.frames + num_sms - 1) / num_sms;
+        g.th = static_cast<int>(std::max(4ll, std::min<long long>(OPC_PLANES_THMAX, th)));
+    }
+    const std::size_t smem = pl_smem_bytes<R>(g);
+    cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(planes_kernel<R>), static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    const unsigned gx = static_cast<unsigned>(bx);
+    const dim3 grid(gx, static_cast<unsigned>((ih + g.th - 1) / g.th) + border_grid_rows(a, gx),
+                    static_cast<unsigned>(a.frames));
+    timing_mark(kIdPlanes, 0, s);
+    planes_kernel<R><<<grid, kPlThreads, smem, s>>>(a, g);
+    timing_mark(kIdPlanes, 1, s);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+bool planes_supported(int levels, int radius) {
+    return levels >= 1 && levels + 1 <= 32 && radius >= 1 && radius <= kPlMaxR && bin_multiplier(levels) != 0;
+}
+
+cudaError_t launch_planes(const BandArgs& a, int num_sms, cudaStream_t s) {
+    if (a.y_hi <= a.y_lo || a.x_hi <= a.x_lo || a.frames <= 0) return cudaSuccess;
+    switch (a.radius) {
+        case 1: return launch_r<1>(a, num_sms, s);
+        case 2: return launch_r<2>(a, num_sms, s);
+        case 3: return launch_r<3>(a, num_sms, s);
+        case 4: return launch_r<4>(a, num_sms, s);
+        case 5: return launch_r<5>(a, num_sms, s);
+        case 6: return launch_r<6>(a, num_sms, s);
+        case 7: return launch_r<7>(a, num_sms, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace opc

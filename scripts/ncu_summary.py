@@ -1,9 +1,11 @@
 #!/usr/bin/env python3
 """Summarise an ncu report (--set full) of the skew kernel into profiles/.
 
-usage: python scripts/ncu_summary.py <report.ncu-rep> <out-prefix> [kernel-regex]
+usage: python scripts/ncu_summary.py <report.ncu-rep> <out-prefix> [kernel-regex] [alg-bytes]
 writes <out-prefix>.md (human summary) and <out-prefix>.json (numbers, incl.
-dram bytes per launch that bench.py reports as roofline.traffic).
+dram bytes per launch that bench.py reports as roofline.traffic).  alg-bytes =
+the kernel's algorithmic bytes per launch (input + output it must move); the
+summary then states the traffic ratio dram bytes / algorithmic bytes.
 """
 from __future__ import annotations
 
@@ -79,10 +81,16 @@ def main() -> None:
         sys.exit("no matching kernel in report")
     d = out[0]
     d["dram_bytes_per_launch"] = d.get("dram_read", 0) + d.get("dram_write", 0)
+    if len(sys.argv) > 4:
+        d["algorithmic_bytes_per_launch"] = float(sys.argv[4])
+        d["traffic_ratio"] = round(d["dram_bytes_per_launch"] / float(sys.argv[4]), 3)
     with open(prefix + ".json", "w") as f:
         json.dump(d, f, indent=1)
-    lines = [f"# ncu summary: `{d['kernel'][:80]}`", "", f"source report: `{rep}`", "",
-             "| metric | value |", "|---|---|"]
+    lines = [f"# ncu summary: `{d['kernel'][:80]}`", "", f"source report: `{rep}`", ""]
+    if "traffic_ratio" in d:
+        lines += [f"traffic ratio: {d['traffic_ratio']} (DRAM {d['dram_bytes_per_launch']:.4g} B / "
+                  f"algorithmic {d['algorithmic_bytes_per_launch']:.4g} B per launch)", ""]
+    lines += ["| metric | value |", "|---|---|"]
     for k, v in d.items():
         if k in ("kernel", "stalls_per_issue"):
             continue

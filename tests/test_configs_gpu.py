@@ -74,3 +74,18 @@ def test_c4_band_split_and_sampled_window_extremes(gpu):
     want = oracle_lib.oracle_filter(strip, r, cfg.levels, 0, threads=8)
     assert np.array_equal(got, want)
     assert np.array_equal(got[r:-r, r:-r], whole[4000 + r:4000 + r + 40, 1000 + r:1000 + r + 300])
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c5"])
+@pytest.mark.parametrize("kernel", [2, 4, 5])  # skew, column, planes: every family taking r <= 7, L+1 <= 32
+def test_config_digest_forced_family(gpu, name, kernel):
+    """Every small-window family, forced, reproduces the reference digests at
+    full size (the planner picks one; the others must stay bit-exact)."""
+    cfg = gpu.CONFIGS[name]
+    d = DIGESTS[name]
+    frames = cfg.generate_all()
+    p = gpu.FilterParams(cfg.radius, cfg.levels)
+    c = gpu.CudaConfig(kernel=kernel)
+    out = gpu.apply_cuda_batch(frames, p, c) if cfg.frames > 1 else gpu.apply_cuda(frames[0], p, c)[None]
+    bad = [f for f in range(cfg.frames) if sha(out[f]) != d["outputs"]["copy_input"][f]]
+    assert not bad, f"{name} kernel {kernel}: frames {bad[:8]} differ from the reference"

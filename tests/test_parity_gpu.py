@@ -23,7 +23,7 @@ from test_oracle import load_cases, ppm_payload
 pytestmark = pytest.mark.gpu
 
 GOLDEN = Path(__file__).resolve().parent / "golden"
-AUTO, DIRECT, SKEW, SLIDE, COLUMN = 0, 1, 2, 3, 4
+AUTO, DIRECT, SKEW, SLIDE, COLUMN, PLANES = 0, 1, 2, 3, 4, 5
 
 
 def run(opc, img, r, L, border=0, kernel=AUTO, allow256=False):
@@ -43,6 +43,10 @@ def column_ok(r, L):
     return L + 1 <= 32 and r <= 7
 
 
+def planes_ok(r, L):
+    return L + 1 <= 32 and 1 <= r <= 7
+
+
 def test_reference_fixture_cases_all_kernels(gpu):
     n = 0
     for w, h, r, L, border, src, img, want in load_cases():
@@ -55,6 +59,8 @@ def test_reference_fixture_cases_all_kernels(gpu):
             assert np.array_equal(run(gpu, img, r, L, border, SLIDE, allow), want), (w, h, r, L)
         if column_ok(r, L):
             assert np.array_equal(run(gpu, img, r, L, border, COLUMN), want), (w, h, r, L, border)
+        if planes_ok(r, L):
+            assert np.array_equal(run(gpu, img, r, L, border, PLANES), want), (w, h, r, L, border)
         n += 1
     assert n == 296
 
@@ -62,7 +68,7 @@ def test_reference_fixture_cases_all_kernels(gpu):
 def test_golden_ppm(gpu):
     _, _, golden = ppm_payload(GOLDEN / "gradient8_r2_l20_zero.ppm")
     img = gpu.generate(gpu.Pattern.GRADIENT, 8, 8)
-    for k in (AUTO, DIRECT, SKEW, SLIDE, COLUMN):
+    for k in (AUTO, DIRECT, SKEW, SLIDE, COLUMN, PLANES):
         assert np.array_equal(run(gpu, img, 2, 20, 1, k), golden)
 
 
@@ -92,6 +98,24 @@ def test_criterion2_random_medium_vs_oracle(gpu):
             assert np.array_equal(run(gpu, img, r, L, b, SKEW), want), (i, w, h, r, L, b)
         if column_ok(r, L):
             assert np.array_equal(run(gpu, img, r, L, b, COLUMN), want), (i, w, h, r, L, b)
+        if planes_ok(r, L):
+            assert np.array_equal(run(gpu, img, r, L, b, PLANES), want), (i, w, h, r, L, b)
+
+
+@pytest.mark.parametrize("r", [1, 2, 3, 4, 5, 6, 7])
+@pytest.mark.parametrize("L", [1, 2, 15, 20, 23, 30, 31])
+def test_planes_radius_levels_grid(gpu, r, L):
+    """Bit-plane family: every radius it instantiates (the row loop is
+    unrolled by 2r+1), counts up to (2r+1)^2 in its bit planes, 2..32 bins,
+    ragged widths (partial 128-column blocks and 32-column warps) and heights
+    (partial row blocks)."""
+    rng = np.random.default_rng(r * 1000 + L + 7)
+    h = 2 * r + 1 + int(rng.integers(0, 300))
+    w = 2 * r + 1 + int(rng.integers(0, 400))
+    img = rng.integers(0, 256, (h, w, 3), dtype=np.uint8)
+    for b in (0, 1):
+        want = oracle_lib.oracle_filter(img, r, L, b, threads=4)
+        assert np.array_equal(run(gpu, img, r, L, b, PLANES), want), (r, L, b, w, h)
 
 
 @pytest.mark.parametrize("r", [0, 1, 2, 3, 5, 7])
@@ -165,6 +189,8 @@ def test_skew_tie_heavy_content(gpu, content):
         assert np.array_equal(run(gpu, img, r, L, 0, DIRECT), want), (content, r, L)
         if column_ok(r, L):
             assert np.array_equal(run(gpu, img, r, L, 0, COLUMN), want), (content, r, L)
+        if planes_ok(r, L):
+            assert np.array_equal(run(gpu, img, r, L, 0, PLANES), want), (content, r, L)
 
 
 @pytest.mark.parametrize("L", [23, 30, 31])
@@ -336,7 +362,7 @@ def test_launch_counter_advances(gpu):
     assert gpu.kernel_launches() >= before + 1  # direct tile kernel (border blocks fused)
 
 
-@pytest.mark.parametrize("kernel", [AUTO, DIRECT, SKEW, SLIDE, COLUMN])
+@pytest.mark.parametrize("kernel", [AUTO, DIRECT, SKEW, SLIDE, COLUMN, PLANES])
 @pytest.mark.parametrize("r", [3, 6])
 @pytest.mark.parametrize("in_off,out_off", [(0, 0), (1, 3), (5, 2), (16, 7)])
 def test_device_pointers_at_unaligned_offsets(gpu, kernel, r, in_off, out_off):
