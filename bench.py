@@ -511,8 +511,9 @@ def run_b200(args, wl) -> None:
         step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
     else:
         step_ms = [ev[i].elapsed_time(ev_end[i]) for i in range(args.steps)]
-    family = opc.plan_kernel(W, H, r, L)  # OPC_KERNEL_DIRECT/SKEW/SLIDE/COLUMN = 1-4
-    kid = {4: _lib.OPC_KID_COLUMN}.get(family, family)  # timing ids: 1-3 as the families, 6 column
+    family = opc.plan_kernel(W, H, r, L)  # OPC_KERNEL_DIRECT/SKEW/SLIDE/COLUMN/PLANES = 1-5
+    # timing ids: 1-3 as the families, 6 column, 7 planes
+    kid = {4: _lib.OPC_KID_COLUMN, 5: _lib.OPC_KID_PLANES}.get(family, family)
     kernel_total_ms, kernel_n = opc.kernel_timing_read(kid)
     pre_ms, _ = opc.kernel_timing_read(_lib.OPC_KID_PREPASS)
     border_ms, _ = opc.kernel_timing_read(_lib.OPC_KID_BORDER)
@@ -620,7 +621,7 @@ def run_b200(args, wl) -> None:
         "model": f"{model_label}; "
                  f"{num_sms} SMs x 4 x 32 x {sm_mhz:.0f} MHz ({peaks_kind} sm_max_mhz)",
         "algorithmic_ops_per_launch": ops_per_step * args.steps // max(1, kernel_n),
-        "kernel": {1: "direct", 2: "skew", 3: "slide", 4: "column"}.get(family, str(family)),
+        "kernel": {1: "direct", 2: "skew", 3: "slide", 4: "column", 5: "planes"}.get(family, str(family)),
         "kernel_ms": round(kernel_ms, 4),
         "kernel_launches": kernel_n,
         "step_share": {"kernel": round(kernel_total_ms / step_total_ms, 4),

@@ -450,6 +450,11 @@ int plan(int levels, int radius, int forced, long long interior_px) {
     if (forced == OPC_KERNEL_PLANES) {
         return opc::planes_supported(levels, radius) ? OPC_KERNEL_PLANES : -1;
     }
+    // r <= 7, L+1 <= 32: the bit-plane family, at every size (scripts/size_sweep.py
+    // on one B200, noise, L = 20 / 30, 640x480 .. 7680x4320: faster than the
+    // column and skew families everywhere; on config 5's smooth frames, where
+    // the skew family's bin window pays, within 1% of it).
+    if (forced == OPC_KERNEL_AUTO && opc::planes_supported(levels, radius)) return OPC_KERNEL_PLANES;
     // Small images: the column family, while its per-pixel cost (~ 2r+1
     // updates per pixel) stays below the skew family's fill-bound launch
     // (scripts/size_sweep.py on one B200, noise, L = 20: column wins up to

@@ -39,9 +39,22 @@
 // The border pixels of the launch ride on extra blocks (border.cuh).
 #include "kernels.cuh"
 #include "border.cuh"
+#include "tma.cuh"
 
 #include <algorithm>
 
+#ifndef OPC_PLANES_TMA
+#define OPC_PLANES_TMA 1  // TMA tile loads (raw RGB rows) where the row layout allows
+#endif
+#ifndef OPC_PLANES_BCS
+#define OPC_PLANES_BCS 2  // column sums: 0 per warp, 1 block-shared (block barriers), 2 by launch size
+#endif
+#ifndef OPC_PLANES_THMAX_BCS
+#define OPC_PLANES_THMAX_BCS 48  // rows per block of multi-round launches with block-shared sums
+#endif
+#ifndef OPC_PLANES_CNTCS
+#define OPC_PLANES_CNTCS 1  // window count from the column sums' hi words, not the plane walk
+#endif
 #ifndef OPC_PLANES_THMAX
 #define OPC_PLANES_THMAX 64  // rows per block when the image needs several rounds of blocks
 #endif
@@ -54,7 +67,8 @@ constexpr int kPlWarps = 4;
 constexpr int kPlThreads = 32 * kPlWarps;
 constexpr int kPlCols = 32 * kPlWarps;  // output columns per block
 constexpr int kPlMaxR = 7;
-constexpr int kPlPitch = 64;            // CS words per bin row: >= 32 + 2r, a multiple of 32
+constexpr int kPlPitch = 64;            // per-warp CS: uint2 per bin row, >= 32 + 2r, a multiple of 32
+constexpr int kPlBPitch = 160;          // block-shared CS: >= 128 + 2r, a multiple of 32
 
 struct PlGeom {
     int th;  // output rows per block
@@ -77,16 +91,16 @@ __host__ __device__ constexpr int pl_tile_cols() {
     return kPlCols + 2 * R;
 }
 
-template <int R>
-__host__ inline std::size_t pl_smem_bytes(const PlGeom& g) {
-    const std::size_t cs = static_cast<std::size_t>(kPlWarps) * g.nb * kPlPitch * 8;
-    const std::size_t tile = static_cast<std::size_t>(pl_tile_cols<R>()) * (g.th + 2 * R) * 4;
-    const std::size_t recip = static_cast<std::size_t>((2 * R + 1) * (2 * R + 1) + 1) * 4;
-    return cs + tile + ((recip + 15) & ~std::size_t(15));
-}
 
 // Tile entry of one pixel: bin | R << 8 | G << 16 | B << 24.
-__device__ __forceinline__ std::uint32_t pl_hi(std::uint32_t e) { return __byte_perm(e, 0u, 0x4441); }  // R
+// hi word R | 1 << 16: the column sums count their pixels in bits 16..23
+// (window counts <= 225; R sums < 2^16 never carry into them), so the
+// winner's count comes with its sums (OPC_PLANES_CNTCS); otherwise R alone
+#if OPC_PLANES_CNTCS
+__device__ __forceinline__ std::uint32_t pl_hi(std::uint32_t e) { return __byte_perm(e, 1u, 0x5451); }
+#else
+__device__ __forceinline__ std::uint32_t pl_hi(std::uint32_t e) { return __byte_perm(e, 0u, 0x4441); }
+#endif
 __device__ __forceinline__ std::uint32_t pl_lo(std::uint32_t e) { return __byte_perm(e, 0u, 0x4243); }  // G << 16 | B
 __device__ __forceinline__ std::uint32_t pl_mask(std::uint32_t e) { return 1u << (e & 31u); }
 
@@ -189,40 +203,97 @@ __device__ __forceinline__ void planes_sub(std::uint32_t (&w)[P], const std::uin
     }
 }
 
+// Raw RGB rows staged by TMA (the TMA variant): one box of 112 u32 words (448
+// bytes >= 3 (128 + 2r) + 15) x TR rows, starting at the 16-byte-aligned
+// word at or left of the tile's first byte; row pitch 448 bytes.
+constexpr int kPlRawWords = 112;
+
 template <int R>
-__global__ void __launch_bounds__(kPlThreads) planes_kernel(BandArgs a, PlGeom g) {
+__host__ inline std::size_t pl_region_bytes(const PlGeom& g, bool tma, bool bcs) {
+    const std::size_t cs = bcs ? static_cast<std::size_t>(g.nb) * kPlBPitch * 8
+                               : static_cast<std::size_t>(kPlWarps) * g.nb * kPlPitch * 8;
+    const std::size_t raw = tma ? static_cast<std::size_t>(kPlRawWords) * 4 * (g.th + 2 * R) : 0;
+    return cs > raw ? cs : raw;
+}
+
+template <int R>
+__host__ inline std::size_t pl_smem_total(const PlGeom& g, bool tma, bool bcs) {
+    const std::size_t tile = static_cast<std::size_t>(pl_tile_cols<R>()) * (g.th + 2 * R) * 4;
+    const std::size_t recip = static_cast<std::size_t>((2 * R + 1) * (2 * R + 1) + 1) * 4;
+    return pl_region_bytes<R>(g, tma, bcs) + tile + ((recip + 15) & ~std::size_t(15)) + 16;
+}
+
+// The launch's border pixels (border.cuh: 256-thread job blocks of the
+// frame) are shared out over the filter blocks of that frame, so no extra
+// blocks queue behind the filter blocks; each filter block runs its share
+// while its tile loads.
+__device__ __forceinline__ void border_share(const BandArgs& a, int tid) {
+    const int per_frame = gridDim.x * gridDim.y;
+    for (int b = blockIdx.y * gridDim.x + blockIdx.x; b < a.border.nblocks; b += per_frame) {
+        border_block(a, b, blockIdx.z, tid);
+        border_block(a, b, blockIdx.z, tid + kPlThreads);
+    }
+}
+
+// BCS: one block-shared column-sum array ([nb][160]: every tile column once,
+// the block's 4 warps step in lockstep with block barriers) instead of one
+// per warp ([warp][nb][64]: 2r halo columns per warp, warp barriers only).
+template <int R, bool TMA, bool BCS>
+__global__ void __launch_bounds__(kPlThreads)
+    planes_kernel(BandArgs a, PlGeom g, unsigned region_bytes, const __grid_constant__ CUtensorMap tin) {
     constexpr int W2 = 2 * R + 1;
     constexpr int P = pl_planes<R>();
     constexpr int TW = pl_tile_cols<R>();
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int main_rows = (a.y_hi - a.y_lo + g.th - 1) / g.th;
-    if (static_cast<int>(blockIdx.y) >= main_rows) {  // appended border blocks (256-thread jobs)
-        const int b = (blockIdx.y - main_rows) * gridDim.x + blockIdx.x;
-        if (b < a.border.nblocks) {
-            border_block(a, b, blockIdx.z, tid);
-            border_block(a, b, blockIdx.z, tid + kPlThreads);
-        }
-        return;
-    }
     const int nb = g.nb;
     const int TR = g.th + 2 * R;
-    uint2* cs_all = reinterpret_cast<uint2*>(smem);  // [warp][nb][64] (R, G << 16 | B)
-    std::uint32_t* tile = reinterpret_cast<std::uint32_t*>(cs_all + kPlWarps * nb * kPlPitch);  // [TR][TW]
+    constexpr int PITCH = BCS ? kPlBPitch : kPlPitch;
+    uint2* cs_all = reinterpret_cast<uint2*>(smem);  // [warp][nb][64] or [nb][160]: (R, G << 16 | B)
+    std::uint32_t* tile = reinterpret_cast<std::uint32_t*>(smem + region_bytes);  // [TR][TW]
     std::uint32_t* recip = tile + TR * TW;
     recip = reinterpret_cast<std::uint32_t*>((reinterpret_cast<std::uintptr_t>(recip) + 15) & ~std::uintptr_t(15));
+    constexpr int nrec = W2 * W2 + 1;
+    std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(recip + ((nrec + 3) & ~3));
 
     const int x0 = a.x_lo + blockIdx.x * kPlCols;  // first output column of the block
     const int y0 = a.y_lo + blockIdx.y * g.th;     // first output row of the block
     const int frame = blockIdx.z;
     const std::size_t stride = static_cast<std::size_t>(a.width) * 3;
-    const std::uint8_t* in = a.in + a.in_frame_stride * frame;
-    const int in_last = a.in_row0 + a.in_rows - 1;
 
-    // ---- tile: (TR rows) x (TW columns) entries, input rows y0-R .., columns
-    // x0-R ..; columns past the image and rows past the band are clamped (they
-    // only feed outputs that are not stored) ----
-    {
+    // ---- tile: (TR rows) x (TW columns) entries bin | R << 8 | G << 16 |
+    // B << 24 of input rows y0-R .., columns x0-R ..  Columns past the image
+    // and rows past the band only feed outputs that are not stored: the LDG
+    // path clamps them, TMA zero-fills them ----
+    if constexpr (TMA) {
+        const int xb = 3 * (x0 - R);
+        const int xw = (xb >> 4) << 2;  // 16-byte-aligned start word
+        const int delta = xb - 4 * xw;  // 0 .. 15
+        if (tid == 0) {
+            prefetch_tensor_map(&tin);
+            mbar_init(bar, 1);
+            fence_mbar_init();
+            mbar_arrive_expect_tx(bar, static_cast<unsigned>(kPlRawWords * 4 * TR));
+            tma_load_3d(smem, &tin, xw, y0 - R - a.in_row0, frame, bar);
+        }
+        for (int i = tid; i < nrec; i += kPlThreads) recip[i] = i ? 0x80000000u / static_cast<std::uint32_t>(i) + 1u : 0u;
+        border_share(a, tid);  // while the tile is in flight
+        __syncthreads();  // (barrier initialised before anyone waits on it)
+        mbar_wait(bar, 0);
+        const std::uint32_t* raw = reinterpret_cast<const std::uint32_t*>(smem);
+        const int n = TR * TW;
+        for (int i = tid; i < n; i += kPlThreads) {
+            const int ty = i / TW, tx = i - ty * TW;
+            const int bo = delta + 3 * tx;
+            const std::uint32_t* q = raw + ty * kPlRawWords + (bo >> 2);
+            const std::uint32_t v = __funnelshift_r(q[0], q[1], (bo & 3) * 8);  // R | G << 8 | B << 16 | x
+            tile[i] = __umulhi(__dp4a(v, 0x00010101u, 0u), a.bin_mul) | (v << 8);
+        }
+        __syncthreads();  // raw rows consumed: the region becomes the column sums
+    } else {
+        border_share(a, tid);
+        const std::uint8_t* in = a.in + a.in_frame_stride * frame;
+        const int in_last = a.in_row0 + a.in_rows - 1;
         constexpr int kBatch = 8;
         const int n = TR * TW;
         for (int i0 = tid; i0 < n; i0 += kBatch * kPlThreads) {
@@ -247,19 +318,26 @@ __global__ void __launch_bounds__(kPlThreads) planes_kernel(BandArgs a, PlGeom g
                 }
             }
         }
+        for (int i = tid; i < nrec; i += kPlThreads) recip[i] = i ? 0x80000000u / static_cast<std::uint32_t>(i) + 1u : 0u;
     }
-    constexpr int nrec = W2 * W2 + 1;
-    for (int i = tid; i < nrec; i += kPlThreads) recip[i] = i ? 0x80000000u / static_cast<std::uint32_t>(i) + 1u : 0u;
-    uint2* cs = cs_all + warp * nb * kPlPitch;
-    for (int i = lane; i < nb * kPlPitch; i += 32) cs[i] = make_uint2(0u, 0u);
+    uint2* cs = BCS ? cs_all : cs_all + warp * nb * kPlPitch;
+    if (BCS) {
+        for (int i = tid; i < nb * PITCH; i += kPlThreads) cs[i] = make_uint2(0u, 0u);
+    } else {
+        for (int i = lane; i < nb * PITCH; i += 32) cs[i] = make_uint2(0u, 0u);
+    }
     __syncthreads();
 
     const int nrows = min(g.th, a.y_hi - y0);  // warp-uniform
     if (nrows <= 0) return;
-    // lane's window: tile columns c0 .. c0 + 2R, its own CS column c0 (and the
-    // halo column c0 + 32 for lanes < 2R)
+    // lane's window: tile columns c0 .. c0 + 2R; its own CS column (c0 in
+    // the block's array, lane in the warp's) and its halo column, tile column
+    // c0 + HOFF (per-warp arrays: lanes < 2R, column lane + 32; block array:
+    // warp 0's lanes < 2R, column 128 + lane)
     const int c0 = warp * 32 + lane;
-    const bool halo = lane < 2 * R;
+    const bool halo = BCS ? (warp == 0 && lane < 2 * R) : lane < 2 * R;
+    constexpr int HOFF = BCS ? kPlCols : 32;
+    const int own = BCS ? c0 : lane;
     const std::uint32_t* trow = tile + c0;  // tile row 0, the lane's window start
 
     // ---- first window: tile rows 0 .. 2R ----
@@ -275,145 +353,196 @@ __global__ void __launch_bounds__(kPlThreads) planes_kernel(BandArgs a, PlGeom g
 #pragma unroll 1
     for (int i = 0; i < W2; ++i) {
         const std::uint32_t e = trow[i * TW];
-        uint2& v = cs[(e & 31u) * kPlPitch + lane];
+        uint2& v = cs[(e & 31u) * PITCH + own];
         v.x += pl_hi(e);
         v.y += pl_lo(e);
         if (halo) {
-            const std::uint32_t eh = trow[i * TW + 32];
-            uint2& vh = cs[(eh & 31u) * kPlPitch + lane + 32];
+            const std::uint32_t eh = trow[i * TW + HOFF];
+            uint2& vh = cs[(eh & 31u) * PITCH + own + HOFF];
             vh.x += pl_hi(eh);
             vh.y += pl_lo(eh);
         }
     }
-    __syncwarp();
+    if (BCS) {
+        __syncthreads();
+    } else {
+        __syncwarp();
+    }
 
     const int x = x0 + lane + warp * 32;
     const bool store = x < a.x_hi;
     std::uint8_t* o = a.out + a.out_frame_stride * frame +
                       static_cast<std::size_t>(y0 - a.out_row0) * stride + static_cast<std::size_t>(x) * 3;
-    const uint2* csl = cs + lane;
+    const uint2* csl = cs + own;
 
-    // output row k of the block from the current planes and column sums
-    auto emit = [&](int k) {
-        std::uint32_t cand = 0xFFFFFFFFu, cnt = 0u;
-#pragma unroll
-        for (int p = P - 1; p >= 0; --p) {
-            const std::uint32_t t = cand & w[p];
-            const bool nz = t != 0u;
-            cand = nz ? t : cand;
-            cnt = (cnt << 1) | (nz ? 1u : 0u);
-        }
-        const uint2* pb = csl + (__ffs(cand) - 1) * kPlPitch;
-        std::uint32_t sr = 0u, sgb = 0u;
-#pragma unroll
-        for (int j = 0; j < W2; ++j) {
-            const uint2 v = pb[j];
-            sr += v.x;
-            sgb += v.y;
-        }
-        const std::uint32_t m = recip[cnt];
-        if (store) {
-            std::uint8_t* q = o + static_cast<std::size_t>(k) * stride;
-            q[0] = static_cast<std::uint8_t>(__umulhi(sr << 1, m));
-            q[1] = static_cast<std::uint8_t>(__umulhi((sgb >> 16) << 1, m));
-            q[2] = static_cast<std::uint8_t>(__umulhi((sgb & 0xFFFFu) << 1, m));
-        }
-    };
-
-    emit(0);
-    if (nrows <= 1) return;
-    // ---- slide down: output row k's window is tile rows k .. k + 2R.  The
-    // entries of step k (entering row k + 2R: the lane's 2R+1 window columns
-    // and its halo column; leaving row k - 1: its own and halo column) are
-    // loaded one step ahead, before the step's warp syncs ----
+    // Entries the next slide needs (entering row e = k + 1 + 2R: the lane's
+    // 2R+1 window columns and its halo column; leaving row k: its own and halo
+    // column), loaded one row ahead.  Rows past the tile are clamped: the
+    // slide they feed is never emitted.
     std::uint32_t ent[W2], eh, el, elh;
-    {
-        const std::uint32_t* erow = trow + (1 + 2 * R) * TW;
+    auto fetch = [&](int k) {
+        const std::uint32_t* erow = trow + min(k + 1 + 2 * R, TR - 1) * TW;
+        const std::uint32_t* lrow = trow + min(k, TR - 1) * TW;
 #pragma unroll
         for (int j = 0; j < W2; ++j) ent[j] = erow[j];
-        eh = halo ? erow[32] : 0u;  // (column c0 + 32 exists for halo lanes only)
-        el = trow[0];
-        elh = halo ? trow[32] : 0u;
-    }
-    int k = 1;
+        eh = halo ? erow[HOFF] : 0u;  // (column c0 + HOFF exists for halo lanes only)
+        el = lrow[0];
+        elh = halo ? lrow[HOFF] : 0u;
+    };
+    fetch(0);
+
+    // ---- row loop.  Iteration k emits output row k (window = tile rows k ..
+    // k + 2R, column sums of those rows) and slides the planes and column sums
+    // to row k + 1.  The next window's counts are computed between issuing the
+    // winner's column-sum loads and using them.  Ring slot s holds the planes
+    // of tile row k (k == s mod W2), the row that leaves next. ----
+    int k = 0;
     for (;;) {
 #pragma unroll
-        for (int s = 0; s < W2; ++s) {  // ring slot s holds tile row k - 1 (k - 1 == s mod W2)
-            std::uint32_t rin[4];
-            {
-                std::uint32_t m[W2];
+        for (int s = 0; s < W2; ++s) {
+            // argmax of window k (filter.hpp:71-82): walk the planes down
+            std::uint32_t cand = 0xFFFFFFFFu;
+#if !OPC_PLANES_CNTCS
+            std::uint32_t cnt = 0u;
+#endif
 #pragma unroll
-                for (int j = 0; j < W2; ++j) m[j] = pl_mask(ent[j]);
-                Csa<W2, 0, 4>::run(m, rin);
+            for (int p = P - 1; p >= 0; --p) {
+                const std::uint32_t t = cand & w[p];
+                const bool nz = t != 0u;
+                cand = nz ? t : cand;
+#if !OPC_PLANES_CNTCS
+                cnt = (cnt << 1) | (nz ? 1u : 0u);
+#endif
             }
-            planes_update<P>(w, rin, ring[s]);
+            const uint2* pb = csl + (__ffs(cand) - 1) * PITCH;
+            uint2 v[W2];
 #pragma unroll
-            for (int p = 0; p < 4; ++p) ring[s][p] = rin[p];
+            for (int j = 0; j < W2; ++j) v[j] = pb[j];
+#if !OPC_PLANES_CNTCS
+            const std::uint32_t m = recip[cnt];
+#endif
+            // counts of window k + 1
+            {
+                std::uint32_t rin[4], mk[W2];
+#pragma unroll
+                for (int j = 0; j < W2; ++j) mk[j] = pl_mask(ent[j]);
+                Csa<W2, 0, 4>::run(mk, rin);
+                planes_update<P>(w, rin, ring[s]);
+#pragma unroll
+                for (int p = 0; p < 4; ++p) ring[s][p] = rin[p];
+            }
             const std::uint32_t ee = ent[0], ehe = eh, el0 = el, elh0 = elh;
-            const bool more = k + 1 < nrows;
-            if (more) {  // next step's entries
-                const std::uint32_t* erow = trow + (k + 1 + 2 * R) * TW;
+            fetch(k + 1);
+            // output row k (filter.cpp:41-43)
+            std::uint32_t sr = 0u, sgb = 0u;
 #pragma unroll
-                for (int j = 0; j < W2; ++j) ent[j] = erow[j];
-                eh = halo ? erow[32] : 0u;
-                el = trow[k * TW];
-                elh = halo ? trow[k * TW + 32] : 0u;
+            for (int j = 0; j < W2; ++j) {
+                sr += v[j].x;
+                sgb += v[j].y;
             }
-            __syncwarp();  // every lane has read the previous row's column sums
+#if OPC_PLANES_CNTCS
+            const std::uint32_t m = recip[sr >> 16];
+            sr &= 0xFFFFu;
+#endif
+            if (store) {
+                o[0] = static_cast<std::uint8_t>(__umulhi(sr << 1, m));
+                o[1] = static_cast<std::uint8_t>(__umulhi((sgb >> 16) << 1, m));
+                o[2] = static_cast<std::uint8_t>(__umulhi((sgb & 0xFFFFu) << 1, m));
+            }
+            o += stride;
+            if (++k >= nrows) return;
+            // every lane has read row k - 1's column sums
+            if (BCS) {
+                __syncthreads();
+            } else {
+                __syncwarp();
+            }
             {
-                uint2& vl = cs[(el0 & 31u) * kPlPitch + lane];
+                uint2& vl = cs[(el0 & 31u) * PITCH + own];
                 vl.x -= pl_hi(el0);
                 vl.y -= pl_lo(el0);
-                uint2& ve = cs[(ee & 31u) * kPlPitch + lane];
+                uint2& ve = cs[(ee & 31u) * PITCH + own];
                 ve.x += pl_hi(ee);
                 ve.y += pl_lo(ee);
                 if (halo) {
-                    uint2& hl = cs[(elh0 & 31u) * kPlPitch + lane + 32];
+                    uint2& hl = cs[(elh0 & 31u) * PITCH + own + HOFF];
                     hl.x -= pl_hi(elh0);
                     hl.y -= pl_lo(elh0);
-                    uint2& he = cs[(ehe & 31u) * kPlPitch + lane + 32];
+                    uint2& he = cs[(ehe & 31u) * PITCH + own + HOFF];
                     he.x += pl_hi(ehe);
                     he.y += pl_lo(ehe);
                 }
             }
-            __syncwarp();  // column sums of row k complete
-            emit(k);
-            ++k;
-            if (!more) return;
+            // column sums of row k complete
+            if (BCS) {
+                __syncthreads();
+            } else {
+                __syncwarp();
+            }
         }
     }
+}
+
+template <int R, bool TMA, bool BCS>
+cudaError_t launch_rt(const BandArgs& a, const PlGeom& g, const CUtensorMap& tin, cudaStream_t s) {
+    const std::size_t region = pl_region_bytes<R>(g, TMA, BCS);
+    const std::size_t smem = pl_smem_total<R>(g, TMA, BCS);
+    cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(planes_kernel<R, TMA, BCS>), static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    const unsigned gx = static_cast<unsigned>((a.x_hi - a.x_lo + kPlCols - 1) / kPlCols);
+    const dim3 grid(gx, static_cast<unsigned>((a.y_hi - a.y_lo + g.th - 1) / g.th), static_cast<unsigned>(a.frames));
+    timing_mark(kIdPlanes, 0, s);
+    planes_kernel<R, TMA, BCS><<<grid, kPlThreads, smem, s>>>(a, g, static_cast<unsigned>(region), tin);
+    timing_mark(kIdPlanes, 1, s);
+    return cudaGetLastError();
+}
+
+// Rows per block: one round of resident blocks when the image allows (the
+// first window's 2r+1 rows are amortised over as many rows as possible),
+// capped at thmax rows otherwise.  Returns true when the cap was hit (the
+// launch needs several rounds of blocks).
+template <int R>
+bool plan_rows(const BandArgs& a, int num_sms, bool tma, bool bcs, int thmax, PlGeom& g) {
+    const long long iw = a.x_hi - a.x_lo, ih = a.y_hi - a.y_lo;
+    const long long units = (iw + kPlCols - 1) / kPlCols * ih * a.frames;  // block-columns x rows
+    for (int bps = 4; bps >= 1; --bps) {
+        const long long want = static_cast<long long>(num_sms) * bps;
+        const long long th = (units + want - 1) / want;
+        g.th = static_cast<int>(std::max(4ll, std::min<long long>(thmax, th)));
+        if (bps == 1 || pl_smem_total<R>(g, tma, bcs) * bps + bps * 1024 <= 228u * 1024) return th > thmax;
+    }
+    return false;
 }
 
 template <int R>
 cudaError_t launch_r(const BandArgs& a, int num_sms, cudaStream_t s) {
     PlGeom g{};
     g.nb = a.levels + 1;
-    const long long iw = a.x_hi - a.x_lo, ih = a.y_hi - a.y_lo;
-    const long long bx = (iw + kPlCols - 1) / kPlCols;
-    // rows per block: one round of resident blocks when the image is small
-    // (the first window's (2r+1) rows are amortised over as many rows as
-    // possible), OPC_PLANES_THMAX rows per block otherwise
-    int bps = 4;
-    for (; bps > 1; --bps) {
-        long long th = (bx * ih * a.frames + static_cast<long long>(num_sms) * bps - 1) /
-                       (static_cast<long long>(num_sms) * bps);
-        g.th = static_cast<int>(std::max(4ll, std::min<long long>(OPC_PLANES_THMAX, th)));
-        if (pl_smem_bytes<R>(g) * bps + bps * 1024 <= 228u * 1024) break;
+    // TMA tile loads when the rows are 16-byte-aligned word arrays
+    const std::size_t row_bytes = static_cast<std::size_t>(a.width) * 3;
+    bool tma = OPC_PLANES_TMA && row_bytes % 16 == 0 && a.in_frame_stride % 16 == 0 &&
+               reinterpret_cast<std::uintptr_t>(a.in) % 16 == 0;
+    // Column sums: per warp for a launch that fits one round of blocks (no
+    // block barriers; C2 -6%), block-shared for launches of several rounds
+    // (smaller blocks, more of them resident: C5 -10%; measured, profiles/r02_notes.md)
+    bool bcs = OPC_PLANES_BCS == 1;
+    if (OPC_PLANES_BCS == 2) {
+        bcs = plan_rows<R>(a, num_sms, tma, false, OPC_PLANES_THMAX, g);
     }
-    if (bps == 1) {
-        long long th = (bx * ih * a.frames + num_sms - 1) / num_sms;
-        g.th = static_cast<int>(std::max(4ll, std::min<long long>(OPC_PLANES_THMAX, th)));
+    plan_rows<R>(a, num_sms, tma, bcs, bcs ? OPC_PLANES_THMAX_BCS : OPC_PLANES_THMAX, g);
+    CUtensorMap tin{};
+    if (tma) {
+        const cuuint64_t dims[3] = {static_cast<cuuint64_t>(row_bytes / 4), static_cast<cuuint64_t>(a.in_rows),
+                                    static_cast<cuuint64_t>(a.frames)};
+        const cuuint64_t strides[2] = {static_cast<cuuint64_t>(row_bytes),
+                                       static_cast<cuuint64_t>(a.in_frame_stride)};
+        const cuuint32_t box[3] = {static_cast<cuuint32_t>(kPlRawWords),
+                                   static_cast<cuuint32_t>(g.th + 2 * R), 1};
+        tma = encode_tensor_map(&tin, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<std::uint8_t*>(a.in), dims,
+                                strides, box) == 0;
     }
-    const std::size_t smem = pl_smem_bytes<R>(g);
-    cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(planes_kernel<R>), static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    const unsigned gx = static_cast<unsigned>(bx);
-    const dim3 grid(gx, static_cast<unsigned>((ih + g.th - 1) / g.th) + border_grid_rows(a, gx),
-                    static_cast<unsigned>(a.frames));
-    timing_mark(kIdPlanes, 0, s);
-    planes_kernel<R><<<grid, kPlThreads, smem, s>>>(a, g);
-    timing_mark(kIdPlanes, 1, s);
-    return cudaGetLastError();
+    if (tma) return bcs ? launch_rt<R, true, true>(a, g, tin, s) : launch_rt<R, true, false>(a, g, tin, s);
+    return bcs ? launch_rt<R, false, true>(a, g, tin, s) : launch_rt<R, false, false>(a, g, tin, s);
 }
 
 }  // namespace

@@ -102,14 +102,18 @@ def test_band_helpers():
 
 
 def test_kernel_planner():
-    assert opc.plan_kernel(640, 480, 2, 20) == _lib.OPC_KERNEL_COLUMN  # small image, small r
+    P = _lib.OPC_KERNEL_PLANES
+    assert opc.plan_kernel(640, 480, 2, 20) == P  # r <= 7, L+1 <= 32: bit-plane family at every size
+    assert opc.plan_kernel(640, 480, 0, 20) == _lib.OPC_KERNEL_COLUMN  # r = 0 (identity)
     assert opc.plan_kernel(640, 480, 2, 255) == _lib.OPC_KERNEL_DIRECT  # many bins, small r
-    assert opc.plan_kernel(4000, 4000, 2, 20) == _lib.OPC_KERNEL_SKEW
-    assert opc.plan_kernel(1920, 1080, 5, 20) == _lib.OPC_KERNEL_COLUMN
-    assert opc.plan_kernel(1920, 1080, 8, 20) == _lib.OPC_KERNEL_SKEW  # column family: r <= 7
-    assert opc.plan_kernel(2560, 1600, 7, 20) == _lib.OPC_KERNEL_SKEW
+    assert opc.plan_kernel(4000, 4000, 2, 20) == P
+    assert opc.plan_kernel(1920, 1080, 5, 20) == P
+    assert opc.plan_kernel(1920, 1080, 8, 20) == _lib.OPC_KERNEL_SKEW  # bit-plane family: r <= 7
+    assert opc.plan_kernel(2560, 1600, 7, 20) == P
     assert opc.plan_kernel(16384, 16384, 15, 20) == _lib.OPC_KERNEL_SKEW
-    assert opc.plan_kernel(3840, 2160, 7, 30) == _lib.OPC_KERNEL_SKEW
+    assert opc.plan_kernel(3840, 2160, 7, 30) == P
+    assert opc.plan_kernel(3840, 2160, 7, 31) == P  # 32 bins: one bit each in the plane words
+    assert opc.plan_kernel(3840, 2160, 7, 32) == _lib.OPC_KERNEL_SLIDE  # 33 bins
     assert opc.plan_kernel(4096, 4096, 10, 256) == _lib.OPC_KERNEL_SLIDE
     assert opc.plan_kernel(300, 300, 15, 100) == _lib.OPC_KERNEL_SLIDE
     assert opc.plan_kernel(100, 100, 16, 20) == _lib.OPC_KERNEL_DIRECT

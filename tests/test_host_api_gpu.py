@@ -119,16 +119,18 @@ def test_kernel_timing_records_each_launch(gpu):
     opc.kernel_timing(True)
     for _ in range(3):
         opc.apply_cuda(img, p, skew)
-    opc.apply_cuda(img, p)  # automatic choice for this size: the column family
+    opc.apply_cuda(img, p)  # automatic choice for this size: the bit-plane family
+    opc.apply_cuda(img, p, opc.CudaConfig(kernel=_lib.OPC_KERNEL_COLUMN))
     skew_ms, skew_n = opc.kernel_timing_read(_lib.OPC_KID_SKEW)
     pre_ms, pre_n = opc.kernel_timing_read(_lib.OPC_KID_PREPASS)
     bor_ms, bor_n = opc.kernel_timing_read(_lib.OPC_KID_BORDER)
     col_ms, col_n = opc.kernel_timing_read(_lib.OPC_KID_COLUMN)
+    pl_ms, pl_n = opc.kernel_timing_read(_lib.OPC_KID_PLANES)
     opc.kernel_timing(False)
-    # the border job rides on the shear pre-pass / the column kernel: no
-    # border launch of its own
-    assert (skew_n, pre_n, bor_n, col_n) == (3, 3, 0, 1)
-    assert skew_ms > 0 and pre_ms > 0 and bor_ms == 0 and col_ms > 0
+    # the border job rides on the shear pre-pass / the column and bit-plane
+    # kernels: no border launch of its own
+    assert (skew_n, pre_n, bor_n, col_n, pl_n) == (3, 3, 0, 1, 1)
+    assert skew_ms > 0 and pre_ms > 0 and bor_ms == 0 and col_ms > 0 and pl_ms > 0
     opc.apply_cuda(img, p, skew)  # timing off: nothing recorded
     assert opc.kernel_timing_read(_lib.OPC_KID_SKEW) == (0.0, 0)
 

@@ -386,3 +386,39 @@ def test_device_pointers_at_unaligned_offsets(gpu, kernel, r, in_off, out_off):
         got = dev_out.cpu().numpy()
         assert np.array_equal(got[out_off:out_off + n].reshape(h, w, 3), want), (b, kernel)
         assert (got[:out_off] == 0xCD).all() and (got[out_off + n:] == 0xCD).all()
+
+
+@pytest.mark.parametrize("r,L", [(1, 31), (4, 20), (7, 30)])
+def test_planes_multi_round_batch(gpu, r, L):
+    """A launch of several rounds of blocks takes the bit-plane family's
+    block-shared column sums (one array per block, block barriers per row):
+    a 48-frame batch against the oracle on sampled frames and the per-frame
+    calls on all of them; 16-column-multiple width (TMA tile loads) and a
+    ragged one (LDG tile loads)."""
+    rng = np.random.default_rng(r * 100 + L)
+    for w in (608, 601):
+        h, f = 301, 48
+        frames = rng.integers(0, 256, (f, h, w, 3), dtype=np.uint8)
+        p = gpu.FilterParams(r, L)
+        c = gpu.CudaConfig(kernel=PLANES)
+        out = gpu.apply_cuda_batch(frames, p, c)
+        for i in (0, 17, f - 1):
+            assert np.array_equal(out[i], oracle_lib.oracle_filter(frames[i], r, L, 0, threads=8)), (w, i)
+        for i in range(f):
+            assert np.array_equal(out[i], gpu.apply_cuda(frames[i], p, c)), (w, i)
+
+
+@pytest.mark.parametrize("y0,y1", [(0, 97), (40, 233), (230, 301)])
+def test_planes_bands(gpu, y0, y1):
+    """Row bands (the multi-GPU unit) through the bit-plane family: the band
+    input starts at in_row0 > 0 (the TMA box's row coordinate is relative to
+    it) and ends inside the image."""
+    rng = np.random.default_rng(y0 + y1)
+    img = rng.integers(0, 256, (301, 640, 3), dtype=np.uint8)
+    for r in (2, 5, 7):
+        p = gpu.FilterParams(r, 20)
+        c = gpu.CudaConfig(kernel=PLANES)
+        whole = oracle_lib.oracle_filter(img, r, 20, 0, threads=8)
+        lo, hi = gpu.band_input_rows(301, y0, y1, r)
+        band = gpu.apply_cuda_band(img[lo:hi], 301, y0, y1, p, c)
+        assert np.array_equal(band, whole[y0:y1]), (r, y0, y1)
