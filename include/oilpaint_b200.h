@@ -160,8 +160,12 @@ int opc_kernel_timing_read(int32_t kernel_id, double* ms_total, int64_t* launche
 int opc_op_counts(int32_t device, uint64_t* out, int32_t n, int32_t reset);
 
 /* Which kernel family OPC_KERNEL_AUTO would use for these parameters
- * (OPC_KERNEL_*), or -1 if invalid.  Host logic only. */
+ * (OPC_KERNEL_*), or -1 if invalid.  Host logic only.  _batch: for a call
+ * of `frames` frames (opc_filter_rgb8_batch; video batches may plan another
+ * family than single images). */
 int32_t opc_plan_kernel(int32_t width, int32_t height, int32_t radius, int32_t levels);
+int32_t opc_plan_kernel_batch(int32_t width, int32_t height, int32_t radius, int32_t levels,
+                              int32_t frames);
 
 /* Releases cached device buffers and streams. */
 void opc_release(void);

@@ -26,6 +26,7 @@ EXPORTS = (
     "opc_validate", "opc_filter_rgb8", "opc_filter_rgb8_batch", "opc_filter_rgb8_band",
     "opc_band_in_row0", "opc_band_in_rows", "opc_last_error", "opc_version",
     "opc_kernel_launches", "opc_device_count", "opc_synchronize", "opc_plan_kernel",
+    "opc_plan_kernel_batch",
     "opc_release", "opc_generate", "opc_filter_rgb8_multi", "opc_band_begin",
     "opc_generate_device", "opc_kernel_timing", "opc_kernel_timing_read", "opc_generate_rows",
     "opc_op_counts",
@@ -87,6 +88,8 @@ def _load() -> ctypes.CDLL:
     lib.opc_synchronize.restype = ctypes.c_int
     lib.opc_plan_kernel.argtypes = [i32, i32, i32, i32]
     lib.opc_plan_kernel.restype = i32
+    lib.opc_plan_kernel_batch.argtypes = [i32, i32, i32, i32, i32]
+    lib.opc_plan_kernel_batch.restype = i32
     lib.opc_release.argtypes = []
     lib.opc_release.restype = None
     lib.opc_generate.argtypes = [i32, ctypes.c_uint64, i32, i32, i32, u8p, i32]

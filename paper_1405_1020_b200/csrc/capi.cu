@@ -438,7 +438,7 @@ int ensure(void** p, std::size_t* cap, std::size_t need) {
 // (both r <= 15), direct otherwise -- and direct for small images with small
 // windows (r <= 3, <= 4 Mpx of interior), where the O(r^2) scan is cheap and
 // the sliding families cannot fill the GPU (measured: C1 0.026 vs 0.22 ms).
-int plan(int levels, int radius, int forced, long long interior_px) {
+int plan(int levels, int radius, int forced, long long interior_px, int frames) {
     if (forced == OPC_KERNEL_DIRECT) return OPC_KERNEL_DIRECT;
     if (forced == OPC_KERNEL_SKEW) return opc::skew_supported(levels, radius) ? OPC_KERNEL_SKEW : -1;
     if (forced == OPC_KERNEL_COLUMN) {
@@ -454,7 +454,14 @@ int plan(int levels, int radius, int forced, long long interior_px) {
     // on one B200, noise, L = 20 / 30, 640x480 .. 7680x4320: faster than the
     // column and skew families everywhere; on config 5's smooth frames, where
     // the skew family's bin window pays, within 1% of it).
-    if (forced == OPC_KERNEL_AUTO && opc::planes_supported(levels, radius)) return OPC_KERNEL_PLANES;
+    // Exception: batches of >= 8 frames with >= 24 bins, i.e. video, go to the
+    // skew family, whose per-pass 16-bin window pays on smooth frames
+    // (scripts/batch_families.py, 64 x 3840x2160, r = 7, L = 30: smooth skew
+    // 6.37 ms / planes 7.01; uniform noise skew 8.48 / planes 7.01).
+    if (forced == OPC_KERNEL_AUTO && opc::planes_supported(levels, radius)) {
+        if (levels + 1 >= 24 && frames >= 8 && opc::skew_supported(levels, radius)) return OPC_KERNEL_SKEW;
+        return OPC_KERNEL_PLANES;
+    }
     // Small images: the column family, while its per-pixel cost (~ 2r+1
     // updates per pixel) stays below the skew family's fill-bound launch
     // (scripts/size_sweep.py on one B200, noise, L = 20: column wins up to
@@ -563,7 +570,7 @@ int filter_core(const std::uint8_t* in, std::uint8_t* out, int frames, int w, in
     if (!in || !out) return set_error(OPC_EINVAL, "null image buffer");
     const long long iy = std::max(0, std::min(y_end, h - radius) - std::max(y_begin, radius));
     const long long interior = std::max(0, w - 2 * radius) * iy * frames;
-    int kernel = plan(levels, radius, cfg ? cfg->kernel : 0, interior);
+    int kernel = plan(levels, radius, cfg ? cfg->kernel : 0, interior / std::max(1, frames), frames);
     if (kernel < 0) {
         return set_error(OPC_EINVAL, "requested kernel family does not support L=" +
                                          std::to_string(levels) + " r=" + std::to_string(radius));
@@ -1051,7 +1058,17 @@ int32_t opc_plan_kernel(int32_t width, int32_t height, int32_t radius, int32_t l
         return -1;
     }
     return plan(levels, radius, 0,
-                static_cast<long long>(width - 2 * radius) * (height - 2 * radius));
+                static_cast<long long>(width - 2 * radius) * (height - 2 * radius), 1);
+}
+
+int32_t opc_plan_kernel_batch(int32_t width, int32_t height, int32_t radius, int32_t levels,
+                              int32_t frames) {
+    if (frames < 1 || validate_params(width, height, 3ull * width * height, radius, levels,
+                                      OPC_FLAG_ALLOW_LEVELS_256) != OPC_OK) {
+        return -1;
+    }
+    return plan(levels, radius, 0,
+                static_cast<long long>(width - 2 * radius) * (height - 2 * radius), frames);
 }
 
 void opc_release(void) {

@@ -185,8 +185,10 @@ def synchronize(cfg: Optional[CudaConfig] = None) -> None:
     _raise(LIB.opc_synchronize(ctypes.byref(c)))
 
 
-def plan_kernel(width: int, height: int, radius: int, levels: int) -> int:
-    return LIB.opc_plan_kernel(width, height, radius, levels)
+def plan_kernel(width: int, height: int, radius: int, levels: int, frames: int = 1) -> int:
+    if frames == 1:
+        return LIB.opc_plan_kernel(width, height, radius, levels)
+    return LIB.opc_plan_kernel_batch(width, height, radius, levels, frames)
 
 
 def kernel_launches() -> int:

@@ -112,6 +112,9 @@ def test_kernel_planner():
     assert opc.plan_kernel(2560, 1600, 7, 20) == P
     assert opc.plan_kernel(16384, 16384, 15, 20) == _lib.OPC_KERNEL_SKEW
     assert opc.plan_kernel(3840, 2160, 7, 30) == P
+    assert opc.plan_kernel(3840, 2160, 7, 30, frames=64) == _lib.OPC_KERNEL_SKEW  # video batch
+    assert opc.plan_kernel(3840, 2160, 7, 30, frames=4) == P
+    assert opc.plan_kernel(3840, 2160, 7, 20, frames=64) == P  # 21 bins: no bin window
     assert opc.plan_kernel(3840, 2160, 7, 31) == P  # 32 bins: one bit each in the plane words
     assert opc.plan_kernel(3840, 2160, 7, 32) == _lib.OPC_KERNEL_SLIDE  # 33 bins
     assert opc.plan_kernel(4096, 4096, 10, 256) == _lib.OPC_KERNEL_SLIDE
