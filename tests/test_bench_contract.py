@@ -100,3 +100,34 @@ def test_reference_inputs_match_product_generators(bench):
         got = eng.generate_rows(wl, 40)
         want = opc.CONFIGS[name].generate_rows(0, 40)
         assert np.array_equal(got, want), name
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("config", ["c2", "c5"])
+def test_bench_gpus2_relaunches_two_ranks(config):
+    """`bench.py --gpus 2` run plainly (as the driver's scaling run does)
+    relaunches itself as 2 ranks under torch.distributed.run.  On a 1-GPU box
+    the ranks share the device over gloo (OPC_BENCH_BACKEND=gloo: a plumbing
+    check, not a number): n_gpus 2, the row-band split of
+    proj/src/parallel.cpp:55-108 lifted to ranks (C2) or the frame split (C5),
+    and a cpu_baseline on the line."""
+    import json
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, OPC_BENCH_BACKEND="gloo")
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--config", config,
+                          "--steps", "3", "--warmup", "3", "--e2e-steps", "1", "--cpu-seconds", "1"],
+                         env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]  # rank 0 prints the one JSON line
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["cpu_baseline"]["value"] > 0
+    ranks = sorted(d["ranks"], key=lambda x: x["rank"])
+    assert [x["rank"] for x in ranks] == [0, 1]
+    if config == "c2":
+        assert ranks[0]["rows"] == [0, 540] and ranks[1]["rows"] == [540, 1080]
+        assert ranks[0]["input_rows"] == [0, 545] and ranks[1]["input_rows"] == [535, 1080]
+    else:
+        assert ranks[0]["frames"] == [0, 32] and ranks[1]["frames"] == [32, 64]
