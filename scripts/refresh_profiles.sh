@@ -13,13 +13,13 @@ python scripts/ncu_summary.py gpurun_out/prof_c4.ncu-rep profiles/${R}_c4_shear_
 python scripts/ncu_summary.py gpurun_out/prof_c3.ncu-rep profiles/${R}_c3_slide_ncu slide_kernel $((C3PX*6)) > /dev/null
 python scripts/ncu_summary.py gpurun_out/prof_c3.ncu-rep profiles/${R}_c3_transpose_ncu transpose $((C3PX*7)) > /dev/null
 python scripts/ncu_summary.py gpurun_out/prof_c5.ncu-rep profiles/${R}_c5_skew_ncu skew $((C5PX*6)) > /dev/null
-python scripts/ncu_summary.py gpurun_out/prof_c2.ncu-rep profiles/${R}_c2_column_ncu column $((C2PX*6)) > /dev/null
+python scripts/ncu_summary.py gpurun_out/prof_c2.ncu-rep profiles/${R}_c2_planes_ncu planes $((C2PX*6)) > /dev/null
 for c in c1 c2 c3 c4 c5; do [ -s gpurun_out/bench_$c.json ] && cp gpurun_out/bench_$c.json profiles/${R}_bench_$c.json; done
 for c in c1 c2 c3 c4 c5; do [ -s gpurun_out/bench_ref_$c.json ] && cp gpurun_out/bench_ref_$c.json profiles/${R}_bench_reference_$c.json; done
 R=$R python - <<'PY'
 import json, os
 R = os.environ["R"]
-for cfg, src in (("c2", "c2_column_ncu"), ("c3", "c3_slide_ncu"), ("c4", "c4_skew_ncu"), ("c5", "c5_skew_ncu")):
+for cfg, src in (("c2", "c2_planes_ncu"), ("c3", "c3_slide_ncu"), ("c4", "c4_skew_ncu"), ("c5", "c5_skew_ncu")):
     d = json.load(open(f'profiles/{R}_{src}.json'))
     json.dump({"kernel": d["kernel"], "dram_bytes_per_launch": d["dram_bytes_per_launch"],
                "traffic_ratio": d.get("traffic_ratio"),
