@@ -1,40 +1,62 @@
 #!/usr/bin/env python3
-"""Per-rank device time of the C4 row bands of an N-GPU split, measured on one
-GPU (rank k's band alone): predicts strong-scaling efficiency of bench.py
---gpus N (no collective on the data path, so ranks are independent).
-usage: python scripts/band_scaling.py [N ...]"""
+"""Per-rank device time of an N-GPU split, measured on one GPU (rank k's share
+alone): predicts the strong-scaling efficiency of bench.py --gpus N (no
+collective on the data path, so ranks are independent and the job time is the
+slowest share).  Single images split into row bands with r halo rows
+(parallel.cpp:55-108 lifted to devices), batches into frame ranges.  Shares
+under twice the L2 get the L2 flushed before every call, as bench.py does.
+usage: python scripts/band_scaling.py [--config c4] [N ...]"""
+import argparse
 import sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import numpy as np, torch
 import paper_1405_1020_b200 as opc
 
-cfg = opc.CONFIGS["c4"]
-W, H, r, L = cfg.width, cfg.height, cfg.radius, cfg.levels
-full = cfg.generate(0)
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c4")
+ap.add_argument("n", nargs="*", type=int)
+args = ap.parse_args()
+cfg = opc.CONFIGS[args.config]
+W, H, F, r, L = cfg.width, cfg.height, cfg.frames, cfg.radius, cfg.levels
+full = cfg.generate_all() if F > 1 else cfg.generate(0)[None]
 p = opc.FilterParams(r, L)
 s = torch.cuda.Stream()
-c = opc.CudaConfig(device=0, stream=s.cuda_stream)
+c = opc.CudaConfig(device=0, stream=s.cuda_stream, allow_levels_256=L == 256)
+flush = torch.empty(512 * 2**20, dtype=torch.uint8, device="cuda")
 base = None
-for n in [int(a) for a in sys.argv[1:]] or [1, 2, 4, 8]:
+for n in args.n or [1, 2, 4, 8]:
     worst = 0.0
     for k in sorted({0, n - 1, n // 2}):
-        y0, y1 = opc.band_begin(H, n, k), opc.band_begin(H, n, k + 1)
-        lo, hi = opc.band_input_rows(H, y0, y1, r)
-        din = torch.from_numpy(np.ascontiguousarray(full[lo:hi])).cuda()
-        dout = torch.empty((y1 - y0, W, 3), dtype=torch.uint8, device="cuda")
+        if F == 1:
+            y0, y1 = opc.band_begin(H, n, k), opc.band_begin(H, n, k + 1)
+            lo, hi = opc.band_input_rows(H, y0, y1, r)
+            din = torch.from_numpy(np.ascontiguousarray(full[0, lo:hi])).cuda()
+            dout = torch.empty((y1 - y0, W, 3), dtype=torch.uint8, device="cuda")
+            call = lambda: opc.apply_cuda_band_device(din.data_ptr(), dout.data_ptr(), W, H, y0, y1, p, c)
+        else:
+            f0, f1 = opc.band_begin(F, n, k), opc.band_begin(F, n, k + 1)
+            din = torch.from_numpy(np.ascontiguousarray(full[f0:f1])).cuda()
+            dout = torch.empty_like(din)
+            call = lambda: opc.apply_cuda_device(din.data_ptr(), dout.data_ptr(), W, H, p, c, frames=f1 - f0)
+        small = din.numel() < 2 * 126 * 2**20
         for _ in range(2):
-            opc.apply_cuda_band_device(din.data_ptr(), dout.data_ptr(), W, H, y0, y1, p, c)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(s):
-            e0.record(s)
-            for _ in range(10):
-                opc.apply_cuda_band_device(din.data_ptr(), dout.data_ptr(), W, H, y0, y1, p, c)
-            e1.record(s)
-        s.synchronize()
-        worst = max(worst, e0.elapsed_time(e1) / 10)
+            call()
+        ms = []
+        for _ in range(10):
+            with torch.cuda.stream(s):
+                if small:
+                    flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(s)
+                call()
+                e1.record(s)
+            s.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        worst = max(worst, sorted(ms)[len(ms) // 2])
         del din, dout
     if base is None:
         base = worst * n
-    mp = W * H / (worst / 1e3) / 1e6
-    print(f"N={n}: slowest band {worst:.3f} ms -> {mp:,.0f} MP/s job, efficiency {base / (worst * n):.3f}", flush=True)
+    mp = F * W * H / (worst / 1e3) / 1e6
+    print(f"{args.config} N={n}: slowest share {worst:.4f} ms -> {mp:,.0f} MP/s job, "
+          f"efficiency {base / (worst * n):.3f}", flush=True)
