@@ -36,7 +36,12 @@
 //    block, written as one coalesced 96-byte run.
 #include "kernels.cuh"
 #include "border.cuh"
+#include "tma.cuh"
 #include "worksplit.cuh"
+
+#ifndef OPC_SHEAR_TMA
+#define OPC_SHEAR_TMA 1  // TMA interior tiles in the shear pre-pass (A/B: profiles/r02_notes.md)
+#endif
 
 namespace opc {
 
@@ -96,8 +101,13 @@ __device__ __forceinline__ std::uint32_t entry_from_brg(std::uint32_t t, std::ui
 // Interior tiles: each thread loads 3 words (4 pixels) per row straight from
 // global memory and splits them with byte permutes; row stride 132 words keeps
 // both the 16-byte tile stores and the diagonal reads conflict-free.
+// TMA (OPC_SHEAR_TMA, A/B in profiles/r02_notes.md): interior tiles arrive as
+// one cp.async.bulk.tensor box of 96 words x 32 rows and are split from shared
+// memory instead of by 12 __ldg per thread.
+template <bool TMA>
 __global__ void __launch_bounds__(256)
-    shear_kernel(BandArgs a, std::uint32_t* S, ShearGeom g, int vec_ok, int key, std::uint32_t* bmask) {
+    shear_kernel(BandArgs a, std::uint32_t* S, ShearGeom g, int vec_ok, int key, std::uint32_t* bmask,
+                 const __grid_constant__ CUtensorMap tin) {
     __shared__ __align__(16) std::uint32_t tile[kShearRows * kShearStride];
     if (static_cast<int>(blockIdx.y) >= g.Hs / kShearRows) {  // appended border blocks
         const int b = (blockIdx.y - g.Hs / kShearRows) * gridDim.x + blockIdx.x;
@@ -114,13 +124,31 @@ __global__ void __launch_bounds__(256)
     const int in_hi = a.in_row0 + a.in_rows;
     if (vec_ok && x0 + kShearCols <= a.width && y0 + kShearRows <= in_hi) {
         std::uint32_t w[kShearRows / 8][3];
+        if constexpr (TMA) {
+            __shared__ __align__(128) std::uint32_t raw[kShearRows * kShearCols * 3 / 4];
+            __shared__ std::uint64_t bar;
+            if (threadIdx.x == 0) {
+                mbar_init(&bar, 1);
+                fence_mbar_init();
+                mbar_arrive_expect_tx(&bar, sizeof(raw));
+                tma_load_3d(raw, &tin, x0 * 3 / 4, y0 - a.in_row0, frame, &bar);
+            }
+            __syncthreads();
+            mbar_wait(&bar, 0);
 #pragma unroll
-        for (int k = 0; k < kShearRows / 8; ++k) {
-            const std::uint32_t* src = reinterpret_cast<const std::uint32_t*>(
-                in + static_cast<std::size_t>(y0 + warp + 8 * k - a.in_row0) * stride +
-                static_cast<std::size_t>(x0) * 3) + 3 * lane;
+            for (int k = 0; k < kShearRows / 8; ++k) {
 #pragma unroll
-            for (int q = 0; q < 3; ++q) w[k][q] = __ldg(src + q);
+                for (int q = 0; q < 3; ++q) w[k][q] = raw[(warp + 8 * k) * (kShearCols * 3 / 4) + 3 * lane + q];
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < kShearRows / 8; ++k) {
+                const std::uint32_t* src = reinterpret_cast<const std::uint32_t*>(
+                    in + static_cast<std::size_t>(y0 + warp + 8 * k - a.in_row0) * stride +
+                    static_cast<std::size_t>(x0) * 3) + 3 * lane;
+#pragma unroll
+                for (int q = 0; q < 3; ++q) w[k][q] = __ldg(src + q);
+            }
         }
 #pragma unroll
         for (int k = 0; k < kShearRows / 8; ++k) {
@@ -878,8 +906,27 @@ cudaError_t launch_nbs(const BandArgs& a, int* counter, void* scratch, int num_s
         const int vec_ok = (reinterpret_cast<std::uintptr_t>(a.in) % 4 == 0) &&
                            ((static_cast<std::size_t>(a.width) * 3) % 4 == 0) &&
                            (a.in_frame_stride % 4 == 0);
+        // TMA interior tiles: rows and frames 16-byte aligned
+        const std::size_t row_bytes = static_cast<std::size_t>(a.width) * 3;
+        CUtensorMap tin{};
+        bool tma = OPC_SHEAR_TMA && row_bytes % 16 == 0 && a.in_frame_stride % 16 == 0 &&
+                   reinterpret_cast<std::uintptr_t>(a.in) % 16 == 0;
+        if (tma) {
+            const cuuint64_t dims[3] = {static_cast<cuuint64_t>(row_bytes / 4),
+                                        static_cast<cuuint64_t>(a.in_rows), static_cast<cuuint64_t>(a.frames)};
+            const cuuint64_t strides[2] = {static_cast<cuuint64_t>(row_bytes),
+                                           static_cast<cuuint64_t>(a.in_frame_stride)};
+            const cuuint32_t box[3] = {kShearCols * 3 / 4, kShearRows, 1};
+            tma = encode_tensor_map(&tin, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<std::uint8_t*>(a.in),
+                                    dims, strides, box) == 0;
+        }
+        const int key = (SPARSE && OPC_SKEW_KEY) ? 1 : 0;
         timing_mark(kIdPrePass, 0, s);
-        shear_kernel<<<grid, 256, 0, s>>>(a, S, sg, vec_ok, (SPARSE && OPC_SKEW_KEY) ? 1 : 0, bmask);
+        if (tma) {
+            shear_kernel<true><<<grid, 256, 0, s>>>(a, S, sg, vec_ok, key, bmask, tin);
+        } else {
+            shear_kernel<false><<<grid, 256, 0, s>>>(a, S, sg, vec_ok, key, bmask, tin);
+        }
         timing_mark(kIdPrePass, 1, s);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;

@@ -52,7 +52,7 @@ def main() -> None:
     s.synchronize()
     if args.kt:
         from paper_1405_1020_b200 import _lib
-        for name in ("DIRECT", "SKEW", "SLIDE", "COLUMN", "PREPASS", "BORDER"):
+        for name in ("DIRECT", "SKEW", "SLIDE", "COLUMN", "PLANES", "PREPASS", "BORDER"):
             t, n = opc.kernel_timing_read(getattr(_lib, "OPC_KID_" + name))
             if n:
                 print(f"  {name.lower()}: {t / n * 1e3:.1f} us x {n}")
