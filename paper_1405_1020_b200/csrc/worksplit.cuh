@@ -104,6 +104,32 @@ inline WorkSplit make_split(int frames, int nbands, int iw, long long resident, 
     return g;
 }
 
+// Band-aligned split: every band cut into the same number of equal segments,
+// at most one segment per resident warp, so no chunk crosses a band end and no
+// warp takes a second pass.  For launches whose per-warp share is small (the
+// bands of a multi-GPU split): there a pass's fixed cost (the skew kernel's
+// 2(2r+1) + 32 steps of init lead, warm-up and fill / drain) is a large part of
+// a share, and a dynamic remainder chunk is a whole extra pass for the warps
+// that take it.  Returns false (g untouched) when the bands outnumber the warps.
+inline bool make_aligned_split(int frames, int nbands, int iw, long long resident, int min_seg,
+                               WorkSplit& g) {
+    const long long per_band = static_cast<long long>(frames) * nbands;
+    if (per_band > resident) return false;
+    long long nsegs = resident / per_band;
+    nsegs = std::max(1ll, std::min(nsegs, static_cast<long long>(iw) / std::max(1, min_seg)));
+    WorkSplit w{};
+    w.nbands = nbands;
+    w.iw = iw;
+    w.s2 = (iw + nsegs - 1) / nsegs;
+    w.pitch = static_cast<int>(w.s2 * nsegs);
+    w.nstatic = 0;
+    w.s1 = 0;
+    w.units = per_band * w.pitch;
+    w.nchunks = static_cast<int>(per_band * nsegs);
+    g = w;
+    return true;
+}
+
 #ifdef __CUDACC__
 #define OPC_HD __host__ __device__
 #else

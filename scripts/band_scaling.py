@@ -16,6 +16,7 @@ import paper_1405_1020_b200 as opc
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c4")
 ap.add_argument("n", nargs="*", type=int)
+ap.add_argument("--kt", action="store_true", help="per-kernel times of every share (event hook)")
 args = ap.parse_args()
 cfg = opc.CONFIGS[args.config]
 W, H, F, r, L = cfg.width, cfg.height, cfg.frames, cfg.radius, cfg.levels
@@ -54,6 +55,19 @@ for n in args.n or [1, 2, 4, 8]:
             s.synchronize()
             ms.append(e0.elapsed_time(e1))
         worst = max(worst, sorted(ms)[len(ms) // 2])
+        if args.kt:
+            from paper_1405_1020_b200 import _lib
+            opc.kernel_timing(True)
+            for _ in range(5):
+                call()
+            s.synchronize()
+            parts = []
+            for name in ("SKEW", "SLIDE", "PLANES", "PREPASS", "BORDER"):
+                t, cnt = opc.kernel_timing_read(getattr(_lib, "OPC_KID_" + name))
+                if cnt:
+                    parts.append(f"{name.lower()} {t / cnt * 1e3:.1f} us")
+            opc.kernel_timing(False)
+            print(f"    N={n} share {k}: {sorted(ms)[len(ms) // 2]:.4f} ms ({', '.join(parts)})", flush=True)
         del din, dout
     if base is None:
         base = worst * n

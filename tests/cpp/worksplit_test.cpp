@@ -8,9 +8,28 @@
 
 #include "worksplit.cuh"
 
+static int check_split(const opc::WorkSplit& g, int frames, int nbands, int iw, long long max_chunks,
+                       bool one_pass);
+
 static int check(int frames, int nbands, int iw, long long blocks, int wpb, int pct, long long minc,
                  int dyn, int guided) {
     const opc::WorkSplit g = opc::make_split(frames, nbands, iw, blocks * wpb, pct, minc, dyn, guided);
+    int fails = check_split(g, frames, nbands, iw, -1, false);
+    // the band-aligned split of small shares: every unit once, at most one
+    // chunk per resident warp, every chunk a single pass
+    opc::WorkSplit a = g;
+    if (opc::make_aligned_split(frames, nbands, iw, blocks * wpb, static_cast<int>(minc), a)) {
+        fails += check_split(a, frames, nbands, iw, blocks * wpb, true);
+    }
+    return fails;
+}
+
+static int check_split(const opc::WorkSplit& g, int frames, int nbands, int iw, long long max_chunks,
+                       bool one_pass) {
+    if (max_chunks >= 0 && g.nchunks > max_chunks) {
+        std::printf("aligned split: %d chunks for %lld warps\n", g.nchunks, max_chunks);
+        return 1;
+    }
     std::vector<unsigned char> seen(static_cast<std::size_t>(frames) * nbands * iw, 0);
     long long passes = 0;
     // chunks as the kernels claim them: indexed chunks, then (guided mode)
@@ -33,8 +52,13 @@ static int check(int frames, int nbands, int iw, long long blocks, int wpb, int 
     }
     for (auto [u, u_end] : chunks) {
         int f, kb, x0, x1;
+        int chunk_passes = 0;
         while (opc::pass_in_chunk(g, u, u_end, f, kb, x0, x1)) {
             ++passes;
+            if (one_pass && ++chunk_passes > 1) {
+                std::printf("aligned split: a chunk of two passes, shape %d/%d/%d\n", frames, nbands, iw);
+                return 1;
+            }
             if (f < 0 || f >= frames || kb < 0 || kb >= nbands || x0 < 0 || x1 > iw || x0 >= x1) {
                 std::printf("bad pass f=%d kb=%d [%d,%d) shape %d/%d/%d\n", f, kb, x0, x1, frames,
                             nbands, iw);
