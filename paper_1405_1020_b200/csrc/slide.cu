@@ -22,6 +22,7 @@
 // chunk, completion on an mbarrier), two chunks ahead of the slide.  Finished
 // 16-column output blocks leave through a TMA store (the rows' 48 bytes each,
 // clipped by the hardware at the interior end and the band end).
+#include <cmath>
 #include <cstdio>
 
 #include "kernels.cuh"
@@ -63,6 +64,12 @@ namespace {
 #endif
 #ifndef OPC_SLIDE_PLAN_CPW
 #define OPC_SLIDE_PLAN_CPW 4  // planned chunks per resident warp
+#endif
+#ifndef OPC_SLIDE_PLAN_K
+#define OPC_SLIDE_PLAN_K 1  // > 0: decreasing chunk sizes (remaining / (K x warps)), see TGeom
+#endif
+#ifndef OPC_SLIDE_PLAN_M
+#define OPC_SLIDE_PLAN_M 16  // smallest chunk of the decreasing plan: total / (M x warps)
 #endif
 #ifndef OPC_SLIDE_COST_K
 #define OPC_SLIDE_COST_K 24  // cost of a window-changing step in flat steps (work plan)
@@ -129,6 +136,15 @@ struct TGeom {
                            // 32 blk + x changes the window (not flat)
     std::uint32_t* bc;     // [frame][nband][nblk]: cost of the block's columns
     int* cs;               // [nch + 1]: first block of each chunk
+    // Decreasing chunk sizes (OPC_SLIDE_PLAN_K > 0): chunk j covers the cost
+    // fractions [1 - q^j, 1 - q^(j+1)) with q = 1 - 1 / (K x resident) -- each
+    // the remaining cost / (K x resident), guided self-scheduling precomputed --
+    // until chunks would shrink below 1 / (M x resident) of the total, then
+    // equal chunks of that size (from fraction xJ on, chunk J on).
+    float lnq;  // ln q (0: equal-cost chunks)
+    float xJ;   // 1 - q^J
+    float rm;   // M x resident
+    int J;
 };
 
 __host__ inline int plan_chunks(long long blocks, long long resident);
@@ -144,6 +160,19 @@ __host__ inline TGeom tgeom(const BandArgs& a, void* scratch = nullptr, long lon
     g.nblk = (a.x_hi - a.x_lo + 31) / 32;
     const long long blocks = static_cast<long long>(a.frames) * g.nbands * g.nblk;
     g.nch = plan_chunks(blocks, resident);
+    if (OPC_SLIDE_PLAN_K > 0 && resident > 0) {
+        const double R = static_cast<double>(resident), K = OPC_SLIDE_PLAN_K, M = OPC_SLIDE_PLAN_M;
+        const double lnq = std::log1p(-1.0 / (K * R));
+        const int J = static_cast<int>(std::ceil(std::log(K / M) / lnq));
+        const double xJ = 1.0 - std::exp(J * lnq);
+        g.lnq = static_cast<float>(lnq);
+        g.J = J;
+        g.xJ = static_cast<float>(xJ);
+        g.rm = static_cast<float>(M * R);
+        long long n = J + static_cast<long long>(std::ceil((1.0 - xJ) * M * R)) + 2;
+        if (n > blocks) n = blocks;  // (the mapping is clamped to nch - 1)
+        g.nch = static_cast<int>(std::max(1ll, n));
+    }
     if (scratch) {
         std::uint32_t* p = static_cast<std::uint32_t*>(scratch) + g.frame_elems * a.frames;
         g.dmask = p;
@@ -372,7 +401,14 @@ __global__ void __launch_bounds__(kPlanThreads) slide_plan_kernel(BandArgs a, TG
     const std::uint32_t total = static_cast<std::uint32_t>(s_total_);
     if (total == 0) return;
     const float scale = static_cast<float>(g.nch) / static_cast<float>(total);
-    auto chunk_of = [&](std::uint32_t e) { return static_cast<int>(static_cast<float>(e) * scale); };
+    const float inv_total = 1.0f / static_cast<float>(total);
+    auto chunk_of = [&](std::uint32_t e) {
+        if (g.lnq == 0.0f) return static_cast<int>(static_cast<float>(e) * scale);
+        const float x = static_cast<float>(e) * inv_total;  // cost fraction before the block
+        const int j = x < g.xJ ? static_cast<int>(log1pf(-x) / g.lnq)
+                               : g.J + static_cast<int>((x - g.xJ) * g.rm);
+        return min(j, g.nch - 1);
+    };
     std::uint32_t e_b = wsum[w] + incl - mine;  // cost before b0
     int prev = b0 == 0 ? -1 : chunk_of(e_b - cost(b0 - 1));
     for (long long b = b0; b < b1; ++b) {
