@@ -21,6 +21,13 @@
 #include "../../include/oilpaint_b200_patterns.h"
 #include "kernels.cuh"
 
+#ifndef OPC_HOST_SMALL_CHUNKS
+#define OPC_HOST_SMALL_CHUNKS 16  // most chunks of a host-pointer image below four 48 MB chunks
+#endif
+#ifndef OPC_HOST_SMALL_MIN_KB
+#define OPC_HOST_SMALL_MIN_KB 6144  // smallest such chunk (per-chunk launch gaps: 2-4 MB chunks measured slower)
+#endif
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -655,7 +662,16 @@ int filter_core(const std::uint8_t* in, std::uint8_t* out, int frames, int w, in
             }
             sizes.insert(sizes.end(), ramp.rbegin(), ramp.rend());
         } else {
+            // Smaller images: up to OPC_HOST_SMALL_CHUNKS chunks of >= 6 MB, so
+            // the H2D of chunk k+1 and the D2H of chunk k overlap even when the
+            // image is below one 48 MB chunk (C2: one 6 MB transfer each way
+            // plus the kernel, end to end, was fully serial).
             int n = static_cast<int>((rows + chunk_rows - 1) / chunk_rows);
+            const long long bytes = static_cast<long long>(rows) * static_cast<long long>(row_bytes);
+            const int small = static_cast<int>(std::min<long long>(
+                OPC_HOST_SMALL_CHUNKS, bytes / static_cast<long long>(OPC_HOST_SMALL_MIN_KB * 1024)));
+            n = std::max(n, small);
+            n = std::min(n, std::max(1, rows / std::max(1, 2 * radius + 1)));  // chunks >= 2r+1 rows
             n = n < 1 ? 1 : n;
             for (int k = 0; k < n; ++k) {
                 sizes.push_back(static_cast<int>(static_cast<long long>(rows) * (k + 1) / n -

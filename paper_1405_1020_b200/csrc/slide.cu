@@ -165,13 +165,16 @@ __host__ inline TGeom tgeom(const BandArgs& a, void* scratch = nullptr, long lon
         const double lnq = std::log1p(-1.0 / (K * R));
         const int J = static_cast<int>(std::ceil(std::log(K / M) / lnq));
         const double xJ = 1.0 - std::exp(J * lnq);
-        g.lnq = static_cast<float>(lnq);
-        g.J = J;
-        g.xJ = static_cast<float>(xJ);
-        g.rm = static_cast<float>(M * R);
-        long long n = J + static_cast<long long>(std::ceil((1.0 - xJ) * M * R)) + 2;
-        if (n > blocks) n = blocks;  // (the mapping is clamped to nch - 1)
-        g.nch = static_cast<int>(std::max(1ll, n));
+        const long long n = J + static_cast<long long>(std::ceil((1.0 - xJ) * M * R)) + 2;
+        // (a launch with fewer 32-column blocks than that keeps equal chunks:
+        // clamping the guided map would pile its tail onto the last chunk)
+        if (n <= blocks) {
+            g.lnq = static_cast<float>(lnq);
+            g.J = J;
+            g.xJ = static_cast<float>(xJ);
+            g.rm = static_cast<float>(M * R);
+            g.nch = static_cast<int>(n);
+        }
     }
     if (scratch) {
         std::uint32_t* p = static_cast<std::uint32_t*>(scratch) + g.frame_elems * a.frames;
