@@ -89,3 +89,37 @@ def test_config_digest_forced_family(gpu, name, kernel):
     out = gpu.apply_cuda_batch(frames, p, c) if cfg.frames > 1 else gpu.apply_cuda(frames[0], p, c)[None]
     bad = [f for f in range(cfg.frames) if sha(out[f]) != d["outputs"]["copy_input"][f]]
     assert not bad, f"{name} kernel {kernel}: frames {bad[:8]} differ from the reference"
+
+
+@pytest.mark.parametrize("name", ["c3", "c4"])
+def test_band_of_8way_split_not_slower_than_whole_image(gpu, name):
+    """Guard for the work plans of the persistent kernels on small launches:
+    one band of an 8-way split (the multi-GPU unit) must take less device time
+    than the whole image (an earlier slide plan piled a band's work onto one
+    chunk: 5x the whole image's time)."""
+    torch = pytest.importorskip("torch")
+    cfg = gpu.CONFIGS[name]
+    W, H, r, L = cfg.width, cfg.height, cfg.radius, cfg.levels
+    img = cfg.generate()
+    s = torch.cuda.Stream()
+    c = gpu.CudaConfig(device=0, stream=s.cuda_stream, allow_levels_256=L == 256)
+    p = gpu.FilterParams(r, L)
+
+    def timed(din, dout, y0, y1):
+        for _ in range(2):
+            gpu.apply_cuda_band_device(din.data_ptr(), dout.data_ptr(), W, H, y0, y1, p, c)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):
+            e0.record(s)
+            for _ in range(3):
+                gpu.apply_cuda_band_device(din.data_ptr(), dout.data_ptr(), W, H, y0, y1, p, c)
+            e1.record(s)
+        s.synchronize()
+        return e0.elapsed_time(e1) / 3
+
+    whole = timed(torch.from_numpy(img).cuda(), torch.empty((H, W, 3), dtype=torch.uint8, device="cuda"), 0, H)
+    y0, y1 = gpu.band_begin(H, 8, 3), gpu.band_begin(H, 8, 4)
+    lo, hi = gpu.band_input_rows(H, y0, y1, r)
+    band = timed(torch.from_numpy(np.ascontiguousarray(img[lo:hi])).cuda(),
+                 torch.empty((y1 - y0, W, 3), dtype=torch.uint8, device="cuda"), y0, y1)
+    assert band < whole, (name, band, whole)
