@@ -55,6 +55,9 @@
 #ifndef OPC_PLANES_CNTCS
 #define OPC_PLANES_CNTCS 1  // window count from the column sums' hi words, not the plane walk
 #endif
+#ifndef OPC_PLANES_BPS_MAX
+#define OPC_PLANES_BPS_MAX 4  // most blocks per SM the row planning aims for
+#endif
 #ifndef OPC_PLANES_THMAX
 #define OPC_PLANES_THMAX 64  // rows per block when the image needs several rounds of blocks
 #endif
@@ -505,7 +508,7 @@ template <int R>
 bool plan_rows(const BandArgs& a, int num_sms, bool tma, bool bcs, int thmax, PlGeom& g) {
     const long long iw = a.x_hi - a.x_lo, ih = a.y_hi - a.y_lo;
     const long long units = (iw + kPlCols - 1) / kPlCols * ih * a.frames;  // block-columns x rows
-    for (int bps = 4; bps >= 1; --bps) {
+    for (int bps = OPC_PLANES_BPS_MAX; bps >= 1; --bps) {
         const long long want = static_cast<long long>(num_sms) * bps;
         const long long th = (units + want - 1) / want;
         g.th = static_cast<int>(std::max(4ll, std::min<long long>(thmax, th)));
