@@ -422,3 +422,18 @@ def test_planes_bands(gpu, y0, y1):
         lo, hi = gpu.band_input_rows(301, y0, y1, r)
         band = gpu.apply_cuda_band(img[lo:hi], 301, y0, y1, p, c)
         assert np.array_equal(band, whole[y0:y1]), (r, y0, y1)
+
+
+@pytest.mark.parametrize("w,h", [(16, 16), (16, 300), (32, 7), (48, 129), (160, 15), (2048, 31)])
+def test_planes_tma_edge_shapes(gpu, w, h):
+    """Widths that are multiples of 16 take the TMA tile path: boxes wider
+    and taller than the tensor (zero-filled), a single 128-column block, and
+    images only 2r+1 rows high."""
+    rng = np.random.default_rng(w * 1000 + h)
+    img = rng.integers(0, 256, (h, w, 3), dtype=np.uint8)
+    for r in (1, 3, 7):
+        if min(w, h) < 2 * r + 1:
+            continue
+        for L in (20, 31):
+            want = oracle_lib.oracle_filter(img, r, L, 0, threads=4)
+            assert np.array_equal(run(gpu, img, r, L, 0, PLANES), want), (w, h, r, L)
