@@ -324,10 +324,18 @@ __global__ void __launch_bounds__(kPlThreads)
         for (int i = tid; i < nrec; i += kPlThreads) recip[i] = i ? 0x80000000u / static_cast<std::uint32_t>(i) + 1u : 0u;
     }
     uint2* cs = BCS ? cs_all : cs_all + warp * nb * kPlPitch;
-    if (BCS) {
-        for (int i = tid; i < nb * PITCH; i += kPlThreads) cs[i] = make_uint2(0u, 0u);
-    } else {
-        for (int i = lane; i < nb * PITCH; i += 32) cs[i] = make_uint2(0u, 0u);
+    // zero the column sums of the columns in use only (the block's TW = 128 +
+    // 2R or the warp's 32 + 2R of each bin row; the pitch pads them to a bank
+    // multiple): thread (or lane) c zeroes column c and the halo thread its
+    // halo column, of every bin
+    {
+        const int c = BCS ? tid : lane;
+        const bool zh = BCS ? tid < 2 * R : lane < 2 * R;
+        constexpr int ZH = BCS ? kPlCols : 32;
+        for (int b = 0; b < nb; ++b) {
+            cs[b * PITCH + c] = make_uint2(0u, 0u);
+            if (zh) cs[b * PITCH + c + ZH] = make_uint2(0u, 0u);
+        }
     }
     __syncthreads();
 
