@@ -441,10 +441,12 @@ int ensure(void** p, std::size_t* cap, std::size_t need) {
     return OPC_OK;
 }
 
-// Kernel family for a call.  Auto: skew for L+1 <= 32, slide for more bins
-// (both r <= 15), direct otherwise -- and direct for small images with small
-// windows (r <= 3, <= 4 Mpx of interior), where the O(r^2) scan is cheap and
-// the sliding families cannot fill the GPU (measured: C1 0.026 vs 0.22 ms).
+// Kernel family for a call.  Auto: the bit-plane
+// family for r <= 7 and L+1 <= 32 (video batches with >= 24 bins: skew);
+// r = 0 (identity) the column family on small images; direct for r <= 3 with
+// many bins on small images, where the O(r^2) scan is cheap and the sliding
+// families cannot fill the GPU; then skew for L+1 <= 32, slide for more bins
+// (both r <= 15), direct otherwise.  interior_px is per frame.
 int plan(int levels, int radius, int forced, long long interior_px, int frames) {
     if (forced == OPC_KERNEL_DIRECT) return OPC_KERNEL_DIRECT;
     if (forced == OPC_KERNEL_SKEW) return opc::skew_supported(levels, radius) ? OPC_KERNEL_SKEW : -1;
@@ -459,8 +461,7 @@ int plan(int levels, int radius, int forced, long long interior_px, int frames) 
     }
     // r <= 7, L+1 <= 32: the bit-plane family, at every size (scripts/size_sweep.py
     // on one B200, noise, L = 20 / 30, 640x480 .. 7680x4320: faster than the
-    // column and skew families everywhere; on config 5's smooth frames, where
-    // the skew family's bin window pays, within 1% of it).
+    // column and skew families everywhere).
     // Exception: batches of >= 8 frames with >= 24 bins, i.e. video, go to the
     // skew family, whose per-pass 16-bin window pays on smooth frames
     // (scripts/batch_families.py, 64 x 3840x2160, r = 7, L = 30: smooth skew
@@ -469,11 +470,9 @@ int plan(int levels, int radius, int forced, long long interior_px, int frames) 
         if (levels + 1 >= 24 && frames >= 8 && opc::skew_supported(levels, radius)) return OPC_KERNEL_SKEW;
         return OPC_KERNEL_PLANES;
     }
-    // Small images: the column family, while its per-pixel cost (~ 2r+1
-    // updates per pixel) stays below the skew family's fill-bound launch
-    // (scripts/size_sweep.py on one B200, noise, L = 20: column wins up to
-    // interior * (2r+1) ~ 50M, e.g. 1920x1080 r <= 7, 2560x1600 r <= 5,
-    // 4096^2 r <= 2; the skew family beyond).
+    // (only r = 0 is left here) small images: the column family, while its
+    // per-pixel cost stays below the skew family's fill-bound launch
+    // (round 1, scripts/size_sweep.py: interior * (2r+1) ~ 50M).
     if (forced == OPC_KERNEL_AUTO && opc::column_supported(levels, radius) &&
         interior_px * (2 * radius + 1) <= 50ll * 1000 * 1000) {
         return OPC_KERNEL_COLUMN;
