@@ -21,6 +21,9 @@
 #include "../../include/oilpaint_b200_patterns.h"
 #include "kernels.cuh"
 
+#ifndef OPC_HOST_CHUNK_MB
+#define OPC_HOST_CHUNK_MB 48  // row chunks of the host-pointer pipeline (single images)
+#endif
 #ifndef OPC_HOST_SMALL_CHUNKS
 #define OPC_HOST_SMALL_CHUNKS 16  // most chunks of a host-pointer image below four 48 MB chunks
 #endif
@@ -644,7 +647,7 @@ int filter_core(const std::uint8_t* in, std::uint8_t* out, int frames, int w, in
         // at both ends: only the first chunk's H2D and the last chunk's kernels
         // and D2H are not overlapped with transfers in the other direction.
         const long long chunk_rows =
-            std::max<long long>(1, static_cast<long long>((48ull << 20) / row_bytes));
+            std::max<long long>(1, static_cast<long long>((static_cast<unsigned long long>(OPC_HOST_CHUNK_MB) << 20) / row_bytes));
         std::vector<int> sizes;
         if (rows > 4 * chunk_rows) {
             std::vector<int> ramp;

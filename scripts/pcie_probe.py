@@ -21,3 +21,20 @@ def both():
     with torch.cuda.stream(s2): h_out.copy_(d_out, non_blocking=True)
 bb = t(both)
 print(f"H2D {n/h2d/1e9:.1f} GB/s  D2H {n/d2h/1e9:.1f} GB/s  both {2*n/bb/1e9:.1f} GB/s total ({bb*1e3:.1f} ms)")
+
+# two streams per direction (halves), to see whether one copy engine per
+# direction is the limit
+s3, s4 = torch.cuda.Stream(), torch.cuda.Stream()
+half = n // 2
+def both4():
+    with torch.cuda.stream(s1): d_in[:half].copy_(h_in[:half], non_blocking=True)
+    with torch.cuda.stream(s3): d_in[half:].copy_(h_in[half:], non_blocking=True)
+    with torch.cuda.stream(s2): h_out[:half].copy_(d_out[:half], non_blocking=True)
+    with torch.cuda.stream(s4): h_out[half:].copy_(d_out[half:], non_blocking=True)
+b4 = min(t(both4) for _ in range(3))
+def h2d2():
+    with torch.cuda.stream(s1): d_in[:half].copy_(h_in[:half], non_blocking=True)
+    with torch.cuda.stream(s3): d_in[half:].copy_(h_in[half:], non_blocking=True)
+h2 = min(t(h2d2) for _ in range(3))
+bb = min(t(both) for _ in range(3))
+print(f"both, 1 stream each way {bb*1e3:.1f} ms; 2 streams each way {b4*1e3:.1f} ms; H2D on 2 streams {n/h2/1e9:.1f} GB/s")
