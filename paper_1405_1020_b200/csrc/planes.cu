@@ -40,6 +40,7 @@
 #include "kernels.cuh"
 #include "border.cuh"
 #include "tma.cuh"
+#include "bitplanes.cuh"
 
 #include <algorithm>
 
@@ -51,9 +52,6 @@
 #endif
 #ifndef OPC_PLANES_THMAX_BCS
 #define OPC_PLANES_THMAX_BCS 48  // rows per block of multi-round launches with block-shared sums
-#endif
-#ifndef OPC_PLANES_CNTCS
-#define OPC_PLANES_CNTCS 1  // window count from the column sums' hi words, not the plane walk
 #endif
 #ifndef OPC_PLANES_BPS_MAX
 #define OPC_PLANES_BPS_MAX 4  // most blocks per SM the row planning aims for
@@ -98,57 +96,10 @@ __host__ __device__ constexpr int pl_tile_cols() {
 // Tile entry of one pixel: bin | R << 8 | G << 16 | B << 24.
 // hi word R | 1 << 16: the column sums count their pixels in bits 16..23
 // (window counts <= 225; R sums < 2^16 never carry into them), so the
-// winner's count comes with its sums (OPC_PLANES_CNTCS); otherwise R alone
-#if OPC_PLANES_CNTCS
+// winner's count comes with its sums (A/B against spelling it from the plane
+// walk: C2 -6%, C5 -3%, profiles/r02_notes.md)
 __device__ __forceinline__ std::uint32_t pl_hi(std::uint32_t e) { return __byte_perm(e, 1u, 0x5451); }
-#else
-__device__ __forceinline__ std::uint32_t pl_hi(std::uint32_t e) { return __byte_perm(e, 0u, 0x4441); }
-#endif
 __device__ __forceinline__ std::uint32_t pl_lo(std::uint32_t e) { return __byte_perm(e, 0u, 0x4243); }  // G << 16 | B
-__device__ __forceinline__ std::uint32_t pl_mask(std::uint32_t e) { return 1u << (e & 31u); }
-
-__device__ __forceinline__ std::uint32_t maj3(std::uint32_t a, std::uint32_t b, std::uint32_t c) {
-    return (a & b) | (a & c) | (b & c);
-}
-
-// Carry-save adder tree: N signals of weight 2^K (bit-sliced one-hot masks or
-// carries) reduced into plane K of q and N/2 carries of weight 2^(K+1).
-template <int N, int K, int NP>
-struct Csa {
-    __device__ __forceinline__ static void run(const std::uint32_t* in, std::uint32_t (&q)[NP]) {
-        constexpr int NC = N / 2;
-        std::uint32_t c[NC];
-        std::uint32_t s = in[0];
-#pragma unroll
-        for (int i = 1, k = 0; i < N; i += 2, ++k) {
-            if (i + 1 < N) {  // full adder
-                const std::uint32_t x = in[i], y = in[i + 1];
-                c[k] = maj3(s, x, y);
-                s = s ^ x ^ y;
-            } else {  // half adder
-                c[k] = s & in[i];
-                s ^= in[i];
-            }
-        }
-        q[K] = s;
-        Csa<NC, K + 1, NP>::run(c, q);
-    }
-};
-template <int K, int NP>
-struct Csa<1, K, NP> {
-    __device__ __forceinline__ static void run(const std::uint32_t* in, std::uint32_t (&q)[NP]) {
-        q[K] = in[0];
-#pragma unroll
-        for (int k = K + 1; k < NP; ++k) q[k] = 0u;
-    }
-};
-template <int K, int NP>
-struct Csa<0, K, NP> {
-    __device__ __forceinline__ static void run(const std::uint32_t*, std::uint32_t (&q)[NP]) {
-#pragma unroll
-        for (int k = K; k < NP; ++k) q[k] = 0u;
-    }
-};
 
 // Row histogram (4 planes: counts <= 15) of the 2R+1 entries at row[0 .. 2R].
 template <int R>
@@ -156,54 +107,8 @@ __device__ __forceinline__ void row_planes(const std::uint32_t* row, std::uint32
     constexpr int W2 = 2 * R + 1;
     std::uint32_t m[W2];
 #pragma unroll
-    for (int j = 0; j < W2; ++j) m[j] = pl_mask(row[j]);
+    for (int j = 0; j < W2; ++j) m[j] = bin_mask(row[j]);
     Csa<W2, 0, 4>::run(m, q);
-}
-
-// w += d (d: 4 planes), modulo 2^P per bin.
-template <int P>
-__device__ __forceinline__ void planes_add(std::uint32_t (&w)[P], const std::uint32_t (&d)[4]) {
-    std::uint32_t c = 0u;
-#pragma unroll
-    for (int k = 0; k < P; ++k) {
-        const std::uint32_t x = k < 4 ? d[k] : 0u, a = w[k];
-        w[k] = a ^ x ^ c;
-        c = maj3(a, x, c);
-    }
-}
-
-// w += a - d in one pass: w + a + ~d + 1, a carry-save layer (planes >= 4
-// of a are 0 and of ~d are 1: sum ~w, carry w) and one ripple with carry-in 1.
-template <int P>
-__device__ __forceinline__ void planes_update(std::uint32_t (&w)[P], const std::uint32_t (&a)[4],
-                                              const std::uint32_t (&d)[4]) {
-    std::uint32_t s[P], c[P + 1];
-    c[0] = 0u;
-#pragma unroll
-    for (int k = 0; k < P; ++k) {
-        const std::uint32_t x = w[k], y = k < 4 ? a[k] : 0u, z = k < 4 ? ~d[k] : 0xFFFFFFFFu;
-        s[k] = x ^ y ^ z;
-        c[k + 1] = maj3(x, y, z);
-    }
-    std::uint32_t cin = 0xFFFFFFFFu;
-#pragma unroll
-    for (int k = 0; k < P; ++k) {
-        const std::uint32_t x = s[k], y = c[k];
-        w[k] = x ^ y ^ cin;
-        cin = maj3(x, y, cin);
-    }
-}
-
-// w -= d: w + ~d + 1.
-template <int P>
-__device__ __forceinline__ void planes_sub(std::uint32_t (&w)[P], const std::uint32_t (&d)[4]) {
-    std::uint32_t c = 0xFFFFFFFFu;
-#pragma unroll
-    for (int k = 0; k < P; ++k) {
-        const std::uint32_t x = k < 4 ? ~d[k] : 0xFFFFFFFFu, a = w[k];
-        w[k] = a ^ x ^ c;
-        c = maj3(a, x, c);
-    }
 }
 
 // Raw RGB rows staged by TMA (the TMA variant): one box of 112 u32 words (448
@@ -411,32 +316,17 @@ __global__ void __launch_bounds__(kPlThreads)
     for (;;) {
 #pragma unroll
         for (int s = 0; s < W2; ++s) {
-            // argmax of window k (filter.hpp:71-82): walk the planes down
-            std::uint32_t cand = 0xFFFFFFFFu;
-#if !OPC_PLANES_CNTCS
-            std::uint32_t cnt = 0u;
-#endif
-#pragma unroll
-            for (int p = P - 1; p >= 0; --p) {
-                const std::uint32_t t = cand & w[p];
-                const bool nz = t != 0u;
-                cand = nz ? t : cand;
-#if !OPC_PLANES_CNTCS
-                cnt = (cnt << 1) | (nz ? 1u : 0u);
-#endif
-            }
-            const uint2* pb = csl + (__ffs(cand) - 1) * PITCH;
+            // argmax of window k (filter.hpp:71-82): the lowest of the bins
+            // holding the largest count (plane walk, bitplanes.cuh)
+            const uint2* pb = csl + (__ffs(plane_max_bins<P>(w)) - 1) * PITCH;
             uint2 v[W2];
 #pragma unroll
             for (int j = 0; j < W2; ++j) v[j] = pb[j];
-#if !OPC_PLANES_CNTCS
-            const std::uint32_t m = recip[cnt];
-#endif
             // counts of window k + 1
             {
                 std::uint32_t rin[4], mk[W2];
 #pragma unroll
-                for (int j = 0; j < W2; ++j) mk[j] = pl_mask(ent[j]);
+                for (int j = 0; j < W2; ++j) mk[j] = bin_mask(ent[j]);
                 Csa<W2, 0, 4>::run(mk, rin);
                 planes_update<P>(w, rin, ring[s]);
 #pragma unroll
@@ -451,10 +341,8 @@ __global__ void __launch_bounds__(kPlThreads)
                 sr += v[j].x;
                 sgb += v[j].y;
             }
-#if OPC_PLANES_CNTCS
-            const std::uint32_t m = recip[sr >> 16];
+            const std::uint32_t m = recip[sr >> 16];  // the winner's count rides in the hi words
             sr &= 0xFFFFu;
-#endif
             if (store) {
                 o[0] = static_cast<std::uint8_t>(__umulhi(sr << 1, m));
                 o[1] = static_cast<std::uint8_t>(__umulhi((sgb >> 16) << 1, m));
