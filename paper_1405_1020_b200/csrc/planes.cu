@@ -1,14 +1,16 @@
 // planes.cu -- the bit-plane column family (L+1 <= 32, r <= 7): window counts
-// as bit planes in registers, channel sums from per-warp column histograms.
+// as bit planes in registers, the winner's channel sums from column-sum
+// histograms in shared memory.  DESIGN.md section 3.0.
 //
 // The column family (column.cu) keeps every thread's window histogram in
 // shared memory and pays two 32-bit read-modify-writes per updated pixel
 // (2(2r+1) per output row): ~166 shared-memory wavefronts per 32 pixels on
 // config 2, which bounds it at the L1 data pipe (profiles/r01_c2_column_ncu.md).
-// Here the same vertical slide is split in two:
+// Here a 128-thread block owns 128 output columns x TH rows, each lane one
+// column, and the vertical slide is split in two:
 //
-//  * COUNTS, bit-sliced in registers.  Bit k of plane word Wk holds bit k of
-//    the count of bin b at bit position b (<= 32 bins, one bit each).  The
+//  * COUNTS, bit-sliced in registers (bitplanes.cuh).  Bit b of plane word
+//    Wk holds bit k of bin b's window count (<= 32 bins, one bit each).  The
 //    row histogram of the entering window row (2r+1 one-hot masks 1 << bin)
 //    is a carry-save adder tree (XOR3 / MAJ, one LOP3 each: 16 for 11 masks);
 //    the window counts advance by W += RH(y+r+1) - RH(y-r) with the leaving
@@ -16,27 +18,32 @@
 //    unrolled by 2r+1).  The lowest-index bin with the largest count
 //    (filter.hpp:71-82) falls out of a walk down the planes from the top:
 //    keep the candidates that have bit k set if any does -- the survivors are
-//    the bins with the maximum count, the lowest one is __ffs, and the taken
-//    branches spell the count.  No shared memory, no dynamic indexing.
+//    the bins with the maximum count, the lowest one is __ffs.  No shared
+//    memory, no dynamic indexing.
 //
-//  * SUMS of the winning bin only, from column histograms.  Each warp owns 32
-//    output columns; its 32 + 2r input columns keep per-bin channel sums over
-//    the current 2r+1 window rows, CS[bin][column] = (R, G << 16 | B) in two
-//    [bin][64] u32 arrays (r <= 7: column sums < 2^12, window sums < 2^16).
-//    Per output row a lane updates its column (and one halo column if lane <
-//    2r): minus the leaving pixel, plus the entering one -- and then reads
-//    the winner's 2r+1 column sums CS[best][x .. x+2r]: with a 64-word bin
-//    pitch lane l always reads bank (l + j) mod 32, conflict-free whatever
-//    the bins of the lanes.
+//  * SUMS of the winning bin only, from column histograms.  For every tile
+//    column, CS[bin][column] = (R | count << 16, G << 16 | B) over the
+//    current 2r+1 window rows (r <= 7: column sums < 2^12, window sums and
+//    counts fit their 16-bit fields).  Per output row each lane subtracts
+//    the leaving and adds the entering pixel of its column (lanes < 2r also
+//    of one halo column), then sums CS[best][x .. x+2r] -- 2r+1 LDS.64 with a
+//    bin pitch that is a multiple of 32 words, so lane l reads bank (l + j)
+//    mod 32 whatever the lanes' bins -- and the hi-word sum carries the
+//    winner's count.  One-round launches keep one CS array per warp ([warp]
+//    [nb][64], warp barriers); multi-round launches one per block ([nb][160],
+//    block barriers, three blocks per SM).
 //
-// Per output pixel (r = 5): 11 mask loads, 22 column-sum loads, ~8 shared
-// RMW words, ~150 ALU ops; against ~166 wavefronts and ~520 instructions per
-// pixel of the column kernel (profiles/r01_c2_column_ncu.md).
+//  * Tile by TMA: one box of raw RGB rows per block, converted in shared
+//    memory to entries bin | R << 8 | G << 16 | B << 24 (byte loads where
+//    the rows are not 16-byte aligned).
+//
+// Per row step (r = 5): ~177 SASS instructions, ~45 shared-memory wavefronts
+// per 32 pixels.
 //
 // Truncating quotient per channel (filter.cpp:41-43): umulhi(2*sum, m_c),
 // m_c = floor(2^31/c) + 1 (exact for c <= 1023, sum <= 255c; checked
 // exhaustively by tests/test_oracle.py::test_reciprocal_division_exact).
-// The border pixels of the launch ride on extra blocks (border.cuh).
+// The launch's border pixels are shared out over the filter blocks (border.cuh).
 #include "kernels.cuh"
 #include "border.cuh"
 #include "tma.cuh"
