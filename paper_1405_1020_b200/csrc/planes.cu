@@ -30,7 +30,7 @@
 //    bin pitch that is a multiple of 32 words, so lane l reads bank (l + j)
 //    mod 32 whatever the lanes' bins -- and the hi-word sum carries the
 //    winner's count.  One-round launches keep one CS array per warp ([warp]
-//    [nb][64], warp barriers); multi-round launches one per block ([nb][160],
+//    [nb][48], warp barriers); multi-round launches one per block ([nb][144],
 //    block barriers, three blocks per SM).
 //
 //  * Tile by TMA: one box of raw RGB rows per block, converted in shared
@@ -51,6 +51,12 @@
 
 #include <algorithm>
 
+#ifndef OPC_PLANES_PITCH_W
+#define OPC_PLANES_PITCH_W 48  // uint2 entries per bin row of a warp's column sums (>= 32 + 2r, multiple of 16)
+#endif
+#ifndef OPC_PLANES_PITCH_B
+#define OPC_PLANES_PITCH_B 144  // ... of a block's (>= 128 + 2r, multiple of 16)
+#endif
 #ifndef OPC_PLANES_TMA
 #define OPC_PLANES_TMA 1  // TMA tile loads (raw RGB rows) where the row layout allows
 #endif
@@ -75,8 +81,8 @@ constexpr int kPlWarps = 4;
 constexpr int kPlThreads = 32 * kPlWarps;
 constexpr int kPlCols = 32 * kPlWarps;  // output columns per block
 constexpr int kPlMaxR = 7;
-constexpr int kPlPitch = 64;            // per-warp CS: uint2 per bin row, >= 32 + 2r, a multiple of 32
-constexpr int kPlBPitch = 160;          // block-shared CS: >= 128 + 2r, a multiple of 32
+constexpr int kPlPitch = OPC_PLANES_PITCH_W;  // per-warp CS: uint2 per bin row, >= 32 + 2r, a multiple of 16 (2 words each)
+constexpr int kPlBPitch = OPC_PLANES_PITCH_B;  // block-shared CS: >= 128 + 2r, a multiple of 16
 
 struct PlGeom {
     int th;  // output rows per block
@@ -150,9 +156,9 @@ __device__ __forceinline__ void border_share(const BandArgs& a, int tid) {
     }
 }
 
-// BCS: one block-shared column-sum array ([nb][160]: every tile column once,
+// BCS: one block-shared column-sum array ([nb][144]: every tile column once,
 // the block's 4 warps step in lockstep with block barriers) instead of one
-// per warp ([warp][nb][64]: 2r halo columns per warp, warp barriers only).
+// per warp ([warp][nb][48]: 2r halo columns per warp, warp barriers only).
 template <int R, bool TMA, bool BCS>
 __global__ void __launch_bounds__(kPlThreads)
     planes_kernel(BandArgs a, PlGeom g, unsigned region_bytes, const __grid_constant__ CUtensorMap tin) {
@@ -164,7 +170,7 @@ __global__ void __launch_bounds__(kPlThreads)
     const int nb = g.nb;
     const int TR = g.th + 2 * R;
     constexpr int PITCH = BCS ? kPlBPitch : kPlPitch;
-    uint2* cs_all = reinterpret_cast<uint2*>(smem);  // [warp][nb][64] or [nb][160]: (R, G << 16 | B)
+    uint2* cs_all = reinterpret_cast<uint2*>(smem);  // [warp][nb][48] or [nb][144]: (R | count << 16, G << 16 | B)
     std::uint32_t* tile = reinterpret_cast<std::uint32_t*>(smem + region_bytes);  // [TR][TW]
     std::uint32_t* recip = tile + TR * TW;
     recip = reinterpret_cast<std::uint32_t*>((reinterpret_cast<std::uintptr_t>(recip) + 15) & ~std::uintptr_t(15));
