@@ -57,6 +57,9 @@
 #ifndef OPC_PLANES_PITCH_B
 #define OPC_PLANES_PITCH_B 144  // ... of a block's (>= 128 + 2r, multiple of 16)
 #endif
+#ifndef OPC_PLANES_HALO_BRANCHLESS
+#define OPC_PLANES_HALO_BRANCHLESS 1  // per-warp sums: halo column updates without a divergent block
+#endif
 #ifndef OPC_PLANES_TMA
 #define OPC_PLANES_TMA 1  // TMA tile loads (raw RGB rows) where the row layout allows
 #endif
@@ -376,6 +379,22 @@ __global__ void __launch_bounds__(kPlThreads)
                 uint2& ve = cs[(ee & 31u) * PITCH + own];
                 ve.x += pl_hi(ee);
                 ve.y += pl_lo(ee);
+#if OPC_PLANES_HALO_BRANCHLESS
+                if (!BCS) {
+                    // Branch-free halo update (per-warp sums, where every warp
+                    // has halo lanes): the other lanes add zero to bin 0 of
+                    // their own column (elh0 = ehe = 0 for them), which only
+                    // they write -- conflict-free, no divergent block.
+                    const int hc = halo ? own + HOFF : own;
+                    const std::uint32_t hm = halo ? 0xFFFFFFFFu : 0u;
+                    uint2& hl = cs[(elh0 & 31u) * PITCH + hc];
+                    hl.x -= pl_hi(elh0) & hm;
+                    hl.y -= pl_lo(elh0);
+                    uint2& he = cs[(ehe & 31u) * PITCH + hc];
+                    he.x += pl_hi(ehe) & hm;
+                    he.y += pl_lo(ehe);
+                } else
+#endif
                 if (halo) {
                     uint2& hl = cs[(elh0 & 31u) * PITCH + own + HOFF];
                     hl.x -= pl_hi(elh0);
