@@ -234,6 +234,7 @@ __global__ void __launch_bounds__(256)
 // into shifts on the ALU pipe, which is the kernel's binding resource.
 struct Mul {
     std::uint32_t m16, negm16, four, one;  // 16, -16, 4, 1
+    std::uint32_t r1k;  // entry_r1's constant operand (0x00040000; KEY: 0x01000000)
 };
 
 // Packed histogram words.  Default layout (any r <= 15):
@@ -246,10 +247,16 @@ template <bool KEY = false>
 __device__ __forceinline__ std::uint32_t entry_lo(std::uint32_t e) {
     return KEY ? __byte_perm(e, 0u, 0x4240) : e & 0x03FC00FFu;  // KEY: B | G << 16
 }
+#ifndef OPC_SKEW_R1K_ARG
+#define OPC_SKEW_R1K_ARG 1
+#endif
+// (the constant operand comes from the kernel argument M.r1k: the selector is
+// then PRMT's immediate and no per-use register copy of a constant is needed)
 template <bool KEY = false>
-__device__ __forceinline__ std::uint32_t entry_r1(std::uint32_t e) {
+__device__ __forceinline__ std::uint32_t entry_r1(std::uint32_t e, std::uint32_t r1k) {
     // default: R + 2^18 (x16 = R << 4 | 1 << 22); KEY: R | 1 << 24 (x1)
-    return KEY ? __byte_perm(e, 0x01000000u, 0x7541) : __byte_perm(e, 0x00040000u, 0x7641);
+    if (!OPC_SKEW_R1K_ARG) r1k = KEY ? 0x01000000u : 0x00040000u;
+    return KEY ? __byte_perm(e, r1k, 0x7541) : __byte_perm(e, r1k, 0x7641);
 }
 template <bool KEY = false>
 __device__ __forceinline__ std::uint32_t entry_bin(std::uint32_t e) { return KEY ? e >> 24 : e >> 26; }
@@ -289,11 +296,11 @@ __device__ __forceinline__ void packed_sub(unsigned long long* p, std::uint32_t 
 // E[bin(e)][slot] += / -= packed(e).  Es = E + slot, SL slots per bin row.
 template <int SL, bool KEY = false>
 __device__ __forceinline__ void rmw_add(unsigned long long* Es, std::uint32_t e, const Mul& M) {
-    packed_add(Es + entry_bin<KEY>(e) * SL, entry_lo<KEY>(e), entry_r1<KEY>(e), M.m16);
+    packed_add(Es + entry_bin<KEY>(e) * SL, entry_lo<KEY>(e), entry_r1<KEY>(e, M.r1k), M.m16);
 }
 template <int SL, bool KEY = false>
 __device__ __forceinline__ void rmw_sub(unsigned long long* Es, std::uint32_t e, const Mul& M) {
-    packed_sub(Es + entry_bin<KEY>(e) * SL, entry_lo<KEY>(e), entry_r1<KEY>(e), M.negm16);
+    packed_sub(Es + entry_bin<KEY>(e) * SL, entry_lo<KEY>(e), entry_r1<KEY>(e, M.r1k), M.negm16);
 }
 
 // Masked forms (all lanes execute; lanes with mask 0 add zero): lo & mask,
@@ -301,12 +308,12 @@ __device__ __forceinline__ void rmw_sub(unsigned long long* Es, std::uint32_t e,
 template <int SL, bool KEY = false>
 __device__ __forceinline__ void rmw_add_m(unsigned long long* Es, std::uint32_t e, std::uint32_t mask,
                                           std::uint32_t m16, const Mul& M) {
-    packed_add(Es + entry_bin<KEY>(e) * SL, entry_lo<KEY>(e) & mask, entry_r1<KEY>(e), m16);
+    packed_add(Es + entry_bin<KEY>(e) * SL, entry_lo<KEY>(e) & mask, entry_r1<KEY>(e, M.r1k), m16);
 }
 template <int SL, bool KEY = false>
 __device__ __forceinline__ void rmw_sub_m(unsigned long long* Es, std::uint32_t e, std::uint32_t mask,
                                           std::uint32_t nm16, const Mul& M) {
-    packed_sub(Es + entry_bin<KEY>(e) * SL, entry_lo<KEY>(e) & mask, entry_r1<KEY>(e), nm16);
+    packed_sub(Es + entry_bin<KEY>(e) * SL, entry_lo<KEY>(e) & mask, entry_r1<KEY>(e, M.r1k), nm16);
 }
 
 // Lowest-index bin with the largest count (filter.hpp:71-82) and its truncated
@@ -471,6 +478,7 @@ struct Task {
     int NV, X0, w2, lane;
     int y_rows;               // valid rows in the band (<= 32)
     std::size_t stride;
+    std::uint32_t stride32;   // row stride in bytes (32 rows of it fit 32 bits)
     std::uint32_t gm;         // bin groups (8 bins each) the current phase touches (GROUPED steps)
     int base;                 // windowed passes: bin of win[0]
 };
@@ -490,23 +498,36 @@ struct Task {
 #define OPC_SKEW_GROUP_BINS 8  // bins per group (4, 8 or 16)
 #endif
 
-// 32-bit element offset from a 64-bit base: one IMAD.WIDE (FMA pipe; the
-// runtime multiplier four = 4 keeps ptxas from turning it into ALU LEAs).
+#ifndef OPC_SKEW_LDOFF_IMM
+#define OPC_SKEW_LDOFF_IMM 1  // r > 7 launches (C4 -1.1%); the SPARSE launches keep the runtime multiplier (C5 +0.8% with it)
+#endif
+// 32-bit element offset from a 64-bit base.  IMM: immediate multiplier 4
+// (ptxas emits LEA + LEA.HI.X); otherwise the runtime multiplier four = 4
+// (IMAD.WIDE + IADD3 + IADD3.X: one op more, but one of them on the FMA pipe).
+template <bool IMM>
 __device__ __forceinline__ std::uint32_t ld_off(const std::uint32_t* base, std::uint32_t off,
                                                 std::uint32_t four) {
     std::uint32_t v;
-    asm volatile(
-        "{\n\t.reg .u64 a;\n\tmad.wide.u32 a, %1, %2, %3;\n\tld.global.nc.u32 %0, [a];\n\t}"
-        : "=r"(v)
-        : "r"(off), "r"(four), "l"(base));
+    if constexpr (IMM) {
+        asm volatile(
+            "{\n\t.reg .u64 a;\n\tmad.wide.u32 a, %1, 4, %2;\n\tld.global.nc.u32 %0, [a];\n\t}"
+            : "=r"(v)
+            : "r"(off), "l"(base));
+    } else {
+        asm volatile(
+            "{\n\t.reg .u64 a;\n\tmad.wide.u32 a, %1, %2, %3;\n\tld.global.nc.u32 %0, [a];\n\t}"
+            : "=r"(v)
+            : "r"(off), "r"(four), "l"(base));
+    }
     return v;
 }
 
 // Loads of step s.  Ring column c, ring row rho live at offset
 // o0 + (c + rho) * Hs + rho, so every access of a step is on diagonal D0 + s
 // (+ a step-independent shift), 32 consecutive rows per access.
-template <bool EDGE>
+template <bool EDGE, bool SPARSE>
 __device__ __forceinline__ Loads fetch(const Task& T, int s) {
+    constexpr bool IMM = OPC_SKEW_LDOFF_IMM && !SPARSE;
     Loads L;
     const int t = T.lane;
     const int w2 = T.w2;
@@ -515,18 +536,18 @@ __device__ __forceinline__ Loads fetch(const Task& T, int s) {
     const int v = s - t;
     L.a = L.b = L.c = L.d = 0;
     if (!EDGE || (v >= 0 && v < T.NV)) {
-        L.a = ld_off(T.Sf, ob + T.dA, four);  // new row t+w2, entering column
-        L.b = ld_off(T.Sf, ob, four);         // old row t, entering column
+        L.a = ld_off<IMM>(T.Sf, ob + T.dA, four);  // new row t+w2, entering column
+        L.b = ld_off<IMM>(T.Sf, ob, four);         // old row t, entering column
         if (!EDGE || v >= w2) {
-            L.c = ld_off(T.Sf, ob + w2, four);     // new row, leaving column
-            L.d = ld_off(T.Sf, ob - T.dD, four);   // old row, leaving column
+            L.c = ld_off<IMM>(T.Sf, ob + w2, four);     // new row, leaving column
+            L.d = ld_off<IMM>(T.Sf, ob - T.dD, four);   // old row, leaving column
         }
     }
     // Init (lanes t < w2): row t of column vi = s - t + w2, i.e. diagonal
     // s + w2, row t; its leaving pixel (column vi - w2 = v, row t) is b.
     const int vi = s - t + w2;
     L.i1 = 0;
-    if (!EDGE || (t < w2 && vi >= 0 && vi < T.NV)) L.i1 = ld_off(T.Sf, ob + T.dI, four);
+    if (!EDGE || (t < w2 && vi >= 0 && vi < T.NV)) L.i1 = ld_off<IMM>(T.Sf, ob + T.dI, four);
     return L;
 }
 
@@ -618,10 +639,10 @@ __device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
     {  // one row of the from-scratch build of E(vi, band top): lane t adds row t
         if (kHoist) {
             const unsigned long long n1 =
-                packed_plus(iold1, entry_lo<KEY>(cur.i1), entry_r1<KEY>(cur.i1), T.M.m16);
+                packed_plus(iold1, entry_lo<KEY>(cur.i1), entry_r1<KEY>(cur.i1, T.M.r1k), T.M.m16);
             // (both in one bin: one word, the second update applies to n1)
             const unsigned long long n2 =
-                packed_minus(ip1 == ip2 ? n1 : iold2, entry_lo<KEY>(cur.b), entry_r1<KEY>(cur.b), T.M.negm16);
+                packed_minus(ip1 == ip2 ? n1 : iold2, entry_lo<KEY>(cur.b), entry_r1<KEY>(cur.b, T.M.r1k), T.M.negm16);
             if (t < w2) {
                 *ip1 = n1;
                 *ip2 = n2;
@@ -647,8 +668,11 @@ __device__ __forceinline__ void step(const Task& T, int s, const Loads& cur,
     const int vv = s - fr - 31 + t;
     if (fr < T.y_rows && (!EDGE || (vv >= w2 && vv < T.NV))) {
         const std::uint32_t rgb = stage[fr * kStageStride + t];
-        std::uint8_t* o = T.out_row0 + static_cast<std::size_t>(fr) * T.stride +
-                          static_cast<std::size_t>(T.X0 + vv) * 3;
+        // 32-bit byte offset within the band's 32 rows (skew_fits(): W < 2^25,
+        // so 32 rows x 3W bytes < 2^32)
+        const std::uint32_t ob = static_cast<std::uint32_t>(fr) * T.stride32 +
+                                 static_cast<std::uint32_t>(T.X0 + vv) * 3u;
+        std::uint8_t* o = T.out_row0 + ob;
         o[0] = static_cast<std::uint8_t>(rgb);
         o[1] = static_cast<std::uint8_t>(rgb >> 8);
         o[2] = static_cast<std::uint8_t>(rgb >> 16);
@@ -727,7 +751,7 @@ __device__ __forceinline__ void run_pass(Task& T, const BandArgs& a, const Shear
     const int p_steady_lo = (T.w2 + 32 + 31) >> 5;
     // The first init row (column 0, lane 0) is added at step -w2: phase -1
     // starts there.  (Slots the skipped steps would clear are still zero.)
-    Loads cur = fetch<true>(T, -T.w2);
+    Loads cur = fetch<true, SPARSE>(T, -T.w2);
     for (int p = -1; p < nphases; ++p) {
         if constexpr (WIN) {
             // keep the phase's bins inside the window [base, base + NW): the
@@ -767,27 +791,27 @@ __device__ __forceinline__ void run_pass(Task& T, const BandArgs& a, const Shear
             // Global loads run kLook steps ahead of their use (3 for NB <= 21:
             // 1% faster on C4; 2 for more bins, where the registers run out).
             constexpr int kLook = NB <= OPC_SKEW_LOOK3_MAXNB ? OPC_SKEW_LOOKAHEAD : 2;
-            Loads n1 = fetch<false>(T, 32 * p + 1);
+            Loads n1 = fetch<false, SPARSE>(T, 32 * p + 1);
             Loads n2{};
-            if constexpr (kLook >= 3) n2 = fetch<false>(T, 32 * p + 2);
+            if constexpr (kLook >= 3) n2 = fetch<false, SPARSE>(T, 32 * p + 2);
 #pragma unroll 1
             for (int ss = 0; ss < 32; ss += 2) {
                 const int s = 32 * p + ss;
                 if (OPC_SKEW_PF_DIST > 0) prefetch_l2(T, s + OPC_SKEW_PF_DIST);
                 if constexpr (kLook >= 3) {
-                    const Loads n3 = fetch<false>(T, s + 3);
+                    const Loads n3 = fetch<false, SPARSE>(T, s + 3);
                     step<NB, SL, SPARSE, false, NW>(T, s, cur, win, E, stage, recip);
                     if (OPC_SKEW_PF_DIST > 0) prefetch_l2(T, s + OPC_SKEW_PF_DIST + 1);
-                    const Loads n4 = fetch<false>(T, s + 4);
+                    const Loads n4 = fetch<false, SPARSE>(T, s + 4);
                     step<NB, SL, SPARSE, false, NW>(T, s + 1, n1, win, E, stage, recip);
                     cur = n2;
                     n1 = n3;
                     n2 = n4;
                 } else {
-                    const Loads m2 = fetch<false>(T, s + 2);
+                    const Loads m2 = fetch<false, SPARSE>(T, s + 2);
                     step<NB, SL, SPARSE, false, NW>(T, s, cur, win, E, stage, recip);
                     if (OPC_SKEW_PF_DIST > 0) prefetch_l2(T, s + OPC_SKEW_PF_DIST + 1);
-                    const Loads m3 = fetch<false>(T, s + 3);
+                    const Loads m3 = fetch<false, SPARSE>(T, s + 3);
                     step<NB, SL, SPARSE, false, NW>(T, s + 1, n1, win, E, stage, recip);
                     cur = m2;
                     n1 = m3;
@@ -797,7 +821,7 @@ __device__ __forceinline__ void run_pass(Task& T, const BandArgs& a, const Shear
 #pragma unroll 1
             for (int ss = p < 0 ? 32 - T.w2 : 0; ss < 32; ++ss) {
                 const int s = 32 * p + ss;
-                const Loads nxt = fetch<true>(T, s + 1);
+                const Loads nxt = fetch<true, SPARSE>(T, s + 1);
                 step<NB, SL, SPARSE, true, NW>(T, s, cur, win, E, stage, recip);
                 cur = nxt;
             }
@@ -832,6 +856,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
     T.dI = T.w2 * T.Hs;
     T.lane = lane;
     T.stride = static_cast<std::size_t>(a.width) * 3;
+    T.stride32 = static_cast<std::uint32_t>(T.stride);
     T.imask = lane < T.w2 ? ~0u : 0u;
     T.im16 = T.imask & M.m16;
     T.inm16 = T.imask & M.negm16;
@@ -969,7 +994,7 @@ cudaError_t launch_nbs(const BandArgs& a, int* counter, void* scratch, int num_s
 
     e = cudaMemsetAsync(counter, 0, 4 * sizeof(int), s);
     if (e != cudaSuccess) return e;
-    const Mul M = (SPARSE && OPC_SKEW_KEY) ? Mul{1u, 0xFFFFFFFFu, 4u, 1u} : Mul{16u, 0xFFFFFFF0u, 4u, 1u};
+    const Mul M = (SPARSE && OPC_SKEW_KEY) ? Mul{1u, 0xFFFFFFFFu, 4u, 1u, 0x01000000u} : Mul{16u, 0xFFFFFFF0u, 4u, 1u, 0x00040000u};
     timing_mark(kIdSkew, 0, s);
     skew_kernel<NB, SL, SPARSE><<<static_cast<unsigned>(blocks), warps * 32, smem, s>>>(a, S, sg, counter, g, M,
                                                                                       bmask);
