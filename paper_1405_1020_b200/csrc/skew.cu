@@ -187,7 +187,6 @@ __global__ void __launch_bounds__(256)
         __shared__ std::uint32_t wm[8];
         const int j = warp >> 1;
         std::uint32_t m = 0;
-#pragma unroll
         // (pixels of the pad columns and of rows past the input are not in
         // any output window: left out)
         const bool col_ok = x0 + 32 * j + lane < a.width;
