@@ -47,7 +47,9 @@ namespace opc {
 
 namespace {
 
-constexpr int kStageStride = 34;  // == 2 (mod 32): skewed (row t, column s-t) writes hit distinct banks
+// == 2 (mod 32): skewed (row t, column s-t) writes hit distinct banks (stride 32 is conflict-free
+// too -- bank (s - t) & 31 -- and measured the same: profiles/r02_notes.md)
+constexpr int kStageStride = 34;
 constexpr int kRecipBytes = 1024 * 4;
 constexpr int kShearRows = 32;
 constexpr int kShearCols = 128;
