@@ -551,19 +551,24 @@ def run_b200(args, wl) -> None:
                                            H, r, L, 0, _ct.byref(c_e2e))
         assert rc == 0, LIB.opc_last_error()
 
-    def time_e2e(src, dst) -> float:
+    e2e_step_ms: list[float] = []  # this rank's wall time of every timed pinned-buffer call
+
+    def time_e2e(src, dst, record=None) -> float:
         step_e2e(src, dst)
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
+            t1 = time.perf_counter()
             step_e2e(src, dst)
+            if record is not None:
+                record.append(round((time.perf_counter() - t1) * 1e3, 4))
         dt = time.perf_counter() - t0
         te = torch.tensor([dt], dtype=torch.float64, device=red_dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         return job_pixels * args.e2e_steps / float(te.item()) / 1e6
 
-    e2e_value = time_e2e(host_in.numpy(), host_out.numpy())
+    e2e_value = time_e2e(host_in.numpy(), host_out.numpy(), e2e_step_ms)
     # the e2e output must equal the device-resident output
     assert torch.equal(host_out, dev_out.cpu()), "e2e output differs from device output"
     # the same call from pageable buffers (a std::vector Image / numpy array):
@@ -669,6 +674,7 @@ def run_b200(args, wl) -> None:
                 "d2h_bytes_per_step": int(host_out.numel()) * world,
                 "path": "opc_filter_rgb8_band / _batch (host pointers, pinned), "
                         f"{args.e2e_steps} steps, wall clock, max over ranks",
+                "step_ms": e2e_step_ms,  # rank 0's calls one by one (a busy host shows as spread)
                 "pageable": {"value": round(e2e_pageable, 2), "unit": "MP/s",
                              "path": "the same call from pageable numpy buffers (staged through "
                                      "the library's pinned ring)"}},
