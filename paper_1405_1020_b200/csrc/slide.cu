@@ -59,6 +59,12 @@ namespace {
 #ifndef OPC_SLIDE_UNROLL_CHANGE
 #define OPC_SLIDE_UNROLL_CHANGE 7  // winner-change column sums: loads in flight per lane
 #endif
+#ifndef OPC_SLIDE_PACKED_SUMS
+#define OPC_SLIDE_PACKED_SUMS 1  // step updates: packed winner-sum differences, PRMT keys, 32-bit shared addresses (C3 slide 252 -> 213 us)
+#endif
+#ifndef OPC_SLIDE_UNROLL_UPDATE
+#define OPC_SLIDE_UNROLL_UPDATE 7  // rows of a step's update loop in flight (A/B on C3: 1 / 3 / 7 / 11 / 21 rows -> 235 / 225 / 213 / 221 / 214 us)
+#endif
 #ifndef OPC_SLIDE_PLAN
 #define OPC_SLIDE_PLAN 1  // equal-cost chunks from the column-change masks (0: static + dynamic split)
 #endif
@@ -93,6 +99,7 @@ constexpr int kRingCols = kChunk * kSlots;
 constexpr int kUnrollScan = OPC_SLIDE_UNROLL_SCAN;
 constexpr int kUnrollSums = OPC_SLIDE_UNROLL_SUMS;
 constexpr int kUnrollChange = OPC_SLIDE_UNROLL_CHANGE;
+constexpr int kUnrollUpdate = OPC_SLIDE_UNROLL_UPDATE;
 constexpr int kStageCols = 16;   // output columns staged per flush (== kChunk)
 constexpr int kStageStride = 17;
 constexpr int kRecipBytes = 1024 * 4;
@@ -430,6 +437,13 @@ __global__ void __launch_bounds__(kPlanThreads) slide_plan_kernel(BandArgs a, TG
 #endif
 }
 
+// c + sum of (unsigned bytes of a) x (signed bytes of b)
+__device__ __forceinline__ std::int32_t dp4a_us(std::uint32_t a, std::uint32_t b, std::int32_t c) {
+    std::int32_t d;
+    asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
 __device__ __forceinline__ std::uint32_t bin_of(std::uint32_t e, std::uint32_t bin_mul) {
     const std::uint32_t s = __dp4a(e, 0x00010101u, 0u);  // R + G + B
     return __umulhi(s, bin_mul);                          // filter.hpp:31-35
@@ -740,6 +754,58 @@ __global__ void __launch_bounds__(kWarps * 32)
                         // its key, so no borrow crosses into the other lane's half)
                         std::uint32_t* const cw32 = reinterpret_cast<std::uint32_t*>(cnt) + (lane >> 1);
                         const unsigned csh = (lane & 1) * 16;
+#if OPC_SLIDE_PACKED_SUMS
+                        // The winner's channel sums change by the masked entering
+                        // minus leaving pixels.  They are accumulated packed: R and
+                        // B as the 16-bit fields of one word, G (times 256) in a
+                        // second -- plain 32-bit adds; every field total is within
+                        // +-31 * 255, so the low field is the sign-extended low
+                        // half and the high field what is left.
+                        const unsigned incs = inc << csh;
+                        // (32-bit shared-window addresses: one multiply-add per
+                        // count word instead of a 64-bit generic address)
+                        const std::uint32_t cw_s = static_cast<std::uint32_t>(__cvta_generic_to_shared(cw32));
+                        const std::uint32_t half = csh ? 0x4432u : 0x4410u;  // PRMT: this lane's u16 half
+                        std::uint32_t dall = 0;  // R + 256 G + 65536 B differences, summed
+                        std::int32_t dg = 0;     // the G differences alone
+                        std::uint32_t cand_k = 0;  // largest post-increment key of another bin
+#pragma unroll kUnrollUpdate
+                        for (int k = 0; k < w2; ++k) {
+                            const std::uint32_t ei = cin[k], eo = cout[k];
+                            const std::uint32_t bi = bin_of(ei, bm), bo = bin_of(eo, bm);
+                            const unsigned d = bi != bo ? incs : 0u;
+                            std::uint32_t old;
+                            asm volatile("atom.shared.add.u32 %0, [%1], %2;"
+                                         : "=r"(old)
+                                         : "r"(cw_s + bi * 64u), "r"(d)
+                                         : "memory");
+                            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(cw_s + bo * 64u), "r"(0u - d)
+                                         : "memory");
+                            // this lane's key of bin bi after the update (a count
+                            // never overflows its half: no carry to drop; keys
+                            // order like their counts).  A bin whose count did
+                            // not move (d = 0) is already bounded by ub, so it
+                            // may join the candidates.
+                            const std::uint32_t key = __byte_perm(old + d, 0u, half);
+                            cand_k = max(cand_k, bi != static_cast<std::uint32_t>(best0) ? key : 0u);
+                            const std::uint32_t a = bi == static_cast<std::uint32_t>(best0) ? ei : 0u;
+                            const std::uint32_t b = bo == static_cast<std::uint32_t>(best0) ? eo : 0u;
+                            dall += a - b;                           // (plane words: top byte 0)
+                            dg = dp4a_us(a, 0x00000100u, dg);  // + G(a)
+                            dg = dp4a_us(b, 0x0000FF00u, dg);  // - G(b): byte 1 of the multiplier = -1
+                        }
+                        cand_c = static_cast<int>(cand_k >> kb_);  // (0 when no other bin was touched: ub >= 0)
+                        {
+                            // dall - 256 dg = dR + 65536 dB with |dR|, |dB| <= 31 * 255:
+                            // dR is the sign-extended low half, dB what is left.
+                            const std::uint32_t drb = dall - (static_cast<std::uint32_t>(dg) << 8);
+                            const std::int32_t dr = static_cast<std::int16_t>(drb & 0xFFFFu);
+                            sr += static_cast<std::uint32_t>(dr);
+                            sb += static_cast<std::uint32_t>(
+                                static_cast<std::int32_t>(drb - static_cast<std::uint32_t>(dr)) >> 16);
+                            sg += static_cast<std::uint32_t>(dg);
+                        }
+#else
                         for (int k = 0; k < w2; ++k) {
                             const std::uint32_t ei = cin[k], eo = cout[k];
                             const int bi = bin_of(ei, bm), bo = bin_of(eo, bm);
@@ -763,6 +829,7 @@ __global__ void __launch_bounds__(kWarps * 32)
                             sg += ((ei & mi) >> 8 & 0xFFu) - ((eo & mo) >> 8 & 0xFFu);
                             sb += ((ei & mi) >> 16 & 0xFFu) - ((eo & mo) >> 16 & 0xFFu);
                         }
+#endif
                         // Resolve the winner (filter.hpp:71-82): it stays while its
                         // count is above every other bin's (bounded by ub);
                         // otherwise a rescan finds the lowest-index maximum.
