@@ -698,6 +698,7 @@ __global__ void __launch_bounds__(kWarps * 32)
         // nonflat bits of this band (work plan): bit x of word j = the step at
         // interior column 32 j + x changes the window
         const std::uint32_t* nfb = tg.nf + (static_cast<std::size_t>(f) * tg.nbands + kb) * tg.nblk;
+        int flat_from = xs;  // image column from which every output so far equals rgb
         for (int p = 0; kStageCols * p < n; ++p) {
             std::uint32_t nfm;  // bit i: the step at pass column 16p + i is not flat
             {
@@ -722,250 +723,314 @@ __global__ void __launch_bounds__(kWarps * 32)
                 }
             }
             const int xend = min(n, kStageCols * p + kStageCols);
-            for (int x = kStageCols * p; x < xend; ++x) {
-                if (x > 0) {
-                    tally(kOpSteps, 1);
-                    // Slide: add ring column x + 2r (image x + r), remove x - 1 (image x - r - 1).
-                    // Warp-wide flat check: the lanes' windows cover ring rows
-                    // 0 .. 31 + 2r, two rows per lane.
-                    bool nonflat;
-                    if (OPC_SLIDE_PLAN) {
-                        nonflat = (nfm >> (x - kStageCols * p)) & 1u;
-                    } else {
-                        const std::uint32_t* cinb = cin - lane;
-                        const std::uint32_t* coutb = cout - lane;
-                        bool diff = cinb[lane] != coutb[lane];
-                        if (lane < 2 * r) diff |= cinb[lane + 32] != coutb[lane + 32];
-                        nonflat = __any_sync(FULL, diff);
+            // A block of 16 columns of one colour (a flat run covering a whole
+            // output block): every row of the out tile is the 3-word pattern of
+            // rgb repeated -- packed from the register, no staging.
+            auto flush_flat = [&](const int xb) {
+                if (lane == 0) bulk_wait_read0();  // the previous store has read the tile
+                __syncwarp();
+                const std::uint32_t w0 = rgb | (rgb << 24), w1 = (rgb >> 8) | (rgb << 16),
+                                    w2_ = (rgb >> 16) | (rgb << 8);
+                uint4* orow = reinterpret_cast<uint4*>(otile + lane * 48);
+                orow[0] = make_uint4(w0, w1, w2_, w0);
+                orow[1] = make_uint4(w1, w2_, w0, w1);
+                orow[2] = make_uint4(w2_, w0, w1, w2_);
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_3d(&tout, otile, 3 * xb, yb - a.out_row0, f);
+                    bulk_commit();
+                }
+                __syncwarp();
+            };
+            // Flush of the output block holding image column xa, its last
+            // staged column (x = the pass column of xa).  Output blocks are 16
+            // image columns [16m, 16m + 15] (a TMA store box must start 16-byte
+            // aligned: 48m bytes); the partial blocks at the ends of a pass are
+            // written with byte stores.
+            auto flush = [&](const int xa) {
+                const int xb = xa & ~(kStageCols - 1);      // image column of stage column 0
+                if (TMA_OUT && xa - xb == kStageCols - 1 && flat_from <= xb && xb >= xs) {
+                    flush_flat(xb);  // no step changed the window since the block began
+                    return;
+                }
+                __syncwarp();
+                const int c_lo = max(xs, xb) - xb;          // valid stage columns [c_lo, c_hi]
+                const int c_hi = xa - xb;
+                if (TMA_OUT && c_lo == 0 && c_hi == kStageCols - 1) {
+                    // lane t packs row t's 16 pixels into 48 bytes of the out
+                    // tile; one TMA store writes the 32 x 48-byte box (rows
+                    // past the band end are clipped by the tensor map)
+                    if (lane == 0) bulk_wait_read0();  // the previous store has read the tile
+                    __syncwarp();
+                    const std::uint32_t* srow = stage + lane * kStageStride;
+                    std::uint32_t wv[12];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {  // pixels 4j .. 4j+3 -> words 3j .. 3j+2
+                        const std::uint32_t p0 = srow[4 * j], p1 = srow[4 * j + 1],
+                                            p2 = srow[4 * j + 2], p3 = srow[4 * j + 3];
+                        wv[3 * j] = p0 | (p1 << 24);
+                        wv[3 * j + 1] = (p1 >> 8) | (p2 << 16);
+                        wv[3 * j + 2] = (p2 >> 16) | (p3 << 8);
                     }
-                    if (nonflat) {
-                        tally(kOpUpdates, 2ull * w2);
-                        if (lane == 0) tally(kOpNonFlatSteps, 1);
-                        const int best0 = best;
-                        int cand_c = -1;  // the largest post-increment count of another bin
-                        // Branch-free form: every row pays two count updates (of
-                        // zero when the pixel does not change bin), so lanes whose
-                        // changes sit at different rows do not diverge.
-                        // (atomics: the two updates of a row are shared-memory
-                        // atomics on the 32-bit word holding this lane's u16 count,
-                        // so the rows' updates are in flight together instead of
-                        // one read-modify-write chain; same-address atomics of a
-                        // thread apply in order, and a count never drops below
-                        // its key, so no borrow crosses into the other lane's half)
-                        std::uint32_t* const cw32 = reinterpret_cast<std::uint32_t*>(cnt) + (lane >> 1);
-                        const unsigned csh = (lane & 1) * 16;
-#if OPC_SLIDE_PACKED_SUMS
-                        // The winner's channel sums change by the masked entering
-                        // minus leaving pixels.  They are accumulated packed: R and
-                        // B as the 16-bit fields of one word, G (times 256) in a
-                        // second -- plain 32-bit adds; every field total is within
-                        // +-31 * 255, so the low field is the sign-extended low
-                        // half and the high field what is left.
-                        const unsigned incs = inc << csh;
-                        // (32-bit shared-window addresses: one multiply-add per
-                        // count word instead of a 64-bit generic address)
-                        const std::uint32_t cw_s = static_cast<std::uint32_t>(__cvta_generic_to_shared(cw32));
-                        const std::uint32_t half = csh ? 0x4432u : 0x4410u;  // PRMT: this lane's u16 half
-                        std::uint32_t dall = 0;  // R + 256 G + 65536 B differences, summed
-                        std::int32_t dg = 0;     // the G differences alone
-                        std::uint32_t cand_k = 0;  // largest post-increment key of another bin
-#pragma unroll kUnrollUpdate
-                        for (int k = 0; k < w2; ++k) {
-                            const std::uint32_t ei = cin[k], eo = cout[k];
-                            const std::uint32_t bi = bin_of(ei, bm), bo = bin_of(eo, bm);
-                            const unsigned d = bi != bo ? incs : 0u;
-                            std::uint32_t old;
-                            asm volatile("atom.shared.add.u32 %0, [%1], %2;"
-                                         : "=r"(old)
-                                         : "r"(cw_s + bi * 64u), "r"(d)
-                                         : "memory");
-                            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(cw_s + bo * 64u), "r"(0u - d)
-                                         : "memory");
-                            // this lane's key of bin bi after the update (a count
-                            // never overflows its half: no carry to drop; keys
-                            // order like their counts).  A bin whose count did
-                            // not move (d = 0) is already bounded by ub, so it
-                            // may join the candidates.
-                            const std::uint32_t key = __byte_perm(old + d, 0u, half);
-                            cand_k = max(cand_k, bi != static_cast<std::uint32_t>(best0) ? key : 0u);
-                            const std::uint32_t a = bi == static_cast<std::uint32_t>(best0) ? ei : 0u;
-                            const std::uint32_t b = bo == static_cast<std::uint32_t>(best0) ? eo : 0u;
-                            dall += a - b;                           // (plane words: top byte 0)
-                            dg = dp4a_us(a, 0x00000100u, dg);  // + G(a)
-                            dg = dp4a_us(b, 0x0000FF00u, dg);  // - G(b): byte 1 of the multiplier = -1
+                    uint4* orow = reinterpret_cast<uint4*>(otile + lane * 48);
+                    orow[0] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                    orow[1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
+                    orow[2] = make_uint4(wv[8], wv[9], wv[10], wv[11]);
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_3d(&tout, otile, 3 * xb, yb - a.out_row0, f);
+                        bulk_commit();
+                    }
+                } else {
+                    const int c = lane & (kStageCols - 1);
+                    for (int f0 = 0; f0 < 32; f0 += 32 / kStageCols) {  // 2 rows per store
+                        const int fr = f0 + lane / kStageCols;
+                        if (yb + f0 >= a.y_hi) break;
+                        if (c >= c_lo && c <= c_hi && yb + fr < a.y_hi) {
+                            const std::uint32_t v = stage[fr * kStageStride + c];
+                            std::uint8_t* o = out +
+                                              static_cast<std::size_t>(yb + fr - a.out_row0) * stride +
+                                              static_cast<std::size_t>(xb + c) * 3;
+                            o[0] = static_cast<std::uint8_t>(v);
+                            o[1] = static_cast<std::uint8_t>(v >> 8);
+                            o[2] = static_cast<std::uint8_t>(v >> 16);
                         }
-                        cand_c = static_cast<int>(cand_k >> kb_);  // (0 when no other bin was touched: ub >= 0)
-                        {
-                            // dall - 256 dg = dR + 65536 dB with |dR|, |dB| <= 31 * 255:
-                            // dR is the sign-extended low half, dB what is left.
-                            const std::uint32_t drb = dall - (static_cast<std::uint32_t>(dg) << 8);
-                            const std::int32_t dr = static_cast<std::int16_t>(drb & 0xFFFFu);
-                            sr += static_cast<std::uint32_t>(dr);
-                            sb += static_cast<std::uint32_t>(
-                                static_cast<std::int32_t>(drb - static_cast<std::uint32_t>(dr)) >> 16);
-                            sg += static_cast<std::uint32_t>(dg);
-                        }
-#else
-                        for (int k = 0; k < w2; ++k) {
-                            const std::uint32_t ei = cin[k], eo = cout[k];
-                            const int bi = bin_of(ei, bm), bo = bin_of(eo, bm);
-                            const bool mv = bi != bo;
-                            const unsigned d = mv ? inc : 0u;
-                            unsigned ki;
-                            if (OPC_SLIDE_ATOMICS) {
-                                const unsigned old = atomicAdd(cw32 + bi * 16, d << csh);
-                                atomicSub(cw32 + bo * 16, d << csh);
-                                ki = ((old >> csh) & 0xFFFFu) + d;
-                            } else {
-                                ki = cnt[bi * 32 + lane] + d;
-                                cnt[bi * 32 + lane] = static_cast<std::uint16_t>(ki);
-                                cnt[bo * 32 + lane] = static_cast<std::uint16_t>(cnt[bo * 32 + lane] - d);
-                            }
-                            const int ci = static_cast<int>(ki >> kb_);
-                            cand_c = (mv && bi != best0) ? max(cand_c, ci) : cand_c;
-                            const std::uint32_t mi = bi == best0 ? 0xFFFFFFFFu : 0u;
-                            const std::uint32_t mo = bo == best0 ? 0xFFFFFFFFu : 0u;
-                            sr += (ei & mi & 0xFFu) - (eo & mo & 0xFFu);
-                            sg += ((ei & mi) >> 8 & 0xFFu) - ((eo & mo) >> 8 & 0xFFu);
-                            sb += ((ei & mi) >> 16 & 0xFFu) - ((eo & mo) >> 16 & 0xFFu);
-                        }
-#endif
-                        // Resolve the winner (filter.hpp:71-82): it stays while its
-                        // count is above every other bin's (bounded by ub);
-                        // otherwise a rescan finds the lowest-index maximum.
-                        ub = max(ub, cand_c);
-                        const int bcf = cnt[best0 * 32 + lane] >> kb_;
-                        bool changed = false;
-                        const bool need = bcf <= ub;
-                        if (!need) bc = bcf;
-                        if (__any_sync(FULL, need)) {
-                            int nb, nc, nu;
-                            rescan(nb, nc, nu);
-                            if (need) {
-                                best = nb;
-                                bc = nc;
-                                ub = nu;
-                                changed = best != best0;
-                            }
-                        }
-                        if (changed) {
-                            tally(kOpSumPixels, static_cast<unsigned long long>(w2) * w2);
-                            tally(kOpWinnerChanges, 1);
-                        }
-                        // Winner changed: the new winner's window sums, one lane's
-                        // window at a time with lane c < 2r+1 summing its column c
-                        // (2r+1 loads per lane instead of (2r+1)^2 on one lane
-                        // while the others wait).
-                        const unsigned chg = __ballot_sync(FULL, changed);
-                        if (__popc(chg) >= OPC_SLIDE_PAR_SUMS) {
-                            // many lanes changed at once (an edge crossing all
-                            // rows): each sums its own window, in parallel
-                            if (changed) {
-                                std::uint32_t cr = 0, cg = 0, cbb = 0;
-                                for (int c = 0; c < w2; ++c) {
-                                    const std::uint32_t* col = ringp(x + c);
-#pragma unroll kUnrollSums
-                                    for (int k = 0; k < w2; ++k) {
-                                        const std::uint32_t e = col[k];
-                                        if (static_cast<int>(bin_of(e, bm)) == best) {
-                                            cr += e & 0xFFu;
-                                            cg += (e >> 8) & 0xFFu;
-                                            cbb += (e >> 16) & 0xFFu;
-                                        }
-                                    }
-                                }
-                                sr = cr;
-                                sg = cg;
-                                sb = cbb;
-                            }
-                        }
-                        for (unsigned todo = __popc(chg) >= OPC_SLIDE_PAR_SUMS ? 0u : chg; todo; todo &= todo - 1) {
-                            const int j = __ffs(todo) - 1;
-                            const int bj = __shfl_sync(FULL, best, j);
-                            std::uint32_t cr = 0, cg = 0, cbb = 0;
-                            if (lane < w2) {
-                                const std::uint32_t* col = ringp(x + lane) - lane + j;
-#pragma unroll kUnrollChange
-                                for (int k = 0; k < w2; ++k) {
-                                    const std::uint32_t e = col[k];
-                                    if (static_cast<int>(bin_of(e, bm)) == bj) {
-                                        cr += e & 0xFFu;
-                                        cg += (e >> 8) & 0xFFu;
-                                        cbb += (e >> 16) & 0xFFu;
-                                    }
-                                }
-                            }
-                            cr = __reduce_add_sync(FULL, cr);
-                            cg = __reduce_add_sync(FULL, cg);
-                            cbb = __reduce_add_sync(FULL, cbb);
-                            if (lane == j) {
-                                sr = cr;
-                                sg = cg;
-                                sb = cbb;
-                            }
-                        }
-                        rgb = quotient();
                     }
                 }
-                if (row_ok) tally(kOpPixels, 1);
-                // Output blocks are 16 image columns [16m, 16m + 15] (a TMA
-                // store box must start 16-byte aligned: 48m bytes); the partial
-                // blocks at the ends of a pass are written with byte stores.
-                const int xa = xs + x;
-                stage[lane * kStageStride + (xa & (kStageCols - 1))] = rgb;
-                if ((xa & (kStageCols - 1)) == kStageCols - 1 || x == n - 1) {  // flush the block
-                    __syncwarp();
-                    const int xb = xa & ~(kStageCols - 1);      // image column of stage column 0
-                    const int c_lo = max(xs, xb) - xb;          // valid stage columns [c_lo, c_hi]
-                    const int c_hi = xa - xb;
-                    if (TMA_OUT && c_lo == 0 && c_hi == kStageCols - 1) {
-                        // lane t packs row t's 16 pixels into 48 bytes of the out
-                        // tile; one TMA store writes the 32 x 48-byte box (rows
-                        // past the band end are clipped by the tensor map)
-                        if (lane == 0) bulk_wait_read0();  // the previous store has read the tile
-                        __syncwarp();
-                        const std::uint32_t* srow = stage + lane * kStageStride;
-                        std::uint32_t wv[12];
+                __syncwarp();
+            };
+            int x = kStageCols * p;
+            while (x < xend) {
+                // Flat steps ahead of x (the work plan's nonflat bits; step 0
+                // of a pass is no step): their outputs repeat rgb, so the run
+                // is emitted at once -- stage stores per 16-column output
+                // block, no per-step loop.
+                int run;
+                if (OPC_SLIDE_PLAN) {
+                    std::uint32_t bits = nfm >> (x - kStageCols * p);
+                    if (x == 0) bits &= ~1u;
+                    run = min(bits ? __ffs(bits) - 1 : 32, xend - x);
+                } else {
+                    bool diff = false;
+                    if (x > 0) {
+                        const std::uint32_t* cinb = cin - lane;
+                        const std::uint32_t* coutb = cout - lane;
+                        diff = cinb[lane] != coutb[lane];
+                        if (lane < 2 * r) diff |= cinb[lane + 32] != coutb[lane + 32];
+                    }
+                    run = __any_sync(FULL, diff) ? 0 : 1;
+                }
+                if (run > 0) {
+                    tally(kOpSteps, static_cast<unsigned long long>(run - (x == 0 ? 1 : 0)));
+                    if (row_ok) tally(kOpPixels, static_cast<unsigned long long>(run));
+                    for (int done = 0; done < run;) {  // at most two output blocks
+                        const int xa = xs + x + done;
+                        const int c0 = xa & (kStageCols - 1);
+                        const int seg = min(run - done, kStageCols - c0);
+                        if (TMA_OUT && seg == kStageCols) {
+                            flush_flat(xa);
+                        } else {
+                            std::uint32_t* sp = stage + lane * kStageStride + c0;
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {  // pixels 4j .. 4j+3 -> words 3j .. 3j+2
-                            const std::uint32_t p0 = srow[4 * j], p1 = srow[4 * j + 1],
-                                                p2 = srow[4 * j + 2], p3 = srow[4 * j + 3];
-                            wv[3 * j] = p0 | (p1 << 24);
-                            wv[3 * j + 1] = (p1 >> 8) | (p2 << 16);
-                            wv[3 * j + 2] = (p2 >> 16) | (p3 << 8);
+                            for (int i = 0; i < kStageCols; ++i) {
+                                if (i < seg) sp[i] = rgb;
+                            }
+                            if (c0 + seg == kStageCols || x + done + seg == n) flush(xa + seg - 1);
                         }
-                        uint4* orow = reinterpret_cast<uint4*>(otile + lane * 48);
-                        orow[0] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-                        orow[1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
-                        orow[2] = make_uint4(wv[8], wv[9], wv[10], wv[11]);
-                        fence_proxy_async_smem();
-                        __syncwarp();
-                        if (lane == 0) {
-                            tma_store_3d(&tout, otile, 3 * xb, yb - a.out_row0, f);
-                            bulk_commit();
-                        }
+                        done += seg;
+                    }
+                    cin += run * RR;
+                    cout += run * RR;
+                    if (cout >= ring_end) cout -= kRingCols * RR;
+                    if (cin >= ring_end) cin -= kRingCols * RR;
+                    x += run;
+                    continue;
+                }
+                // A step that changes the window (x > 0).
+                // Slide: add ring column x + 2r (image x + r), remove x - 1 (image x - r - 1).
+                tally(kOpSteps, 1);
+                {
+                tally(kOpUpdates, 2ull * w2);
+                if (lane == 0) tally(kOpNonFlatSteps, 1);
+                const int best0 = best;
+                int cand_c = -1;  // the largest post-increment count of another bin
+                // Branch-free form: every row pays two count updates (of
+                // zero when the pixel does not change bin), so lanes whose
+                // changes sit at different rows do not diverge.
+                // (atomics: the two updates of a row are shared-memory
+                // atomics on the 32-bit word holding this lane's u16 count,
+                // so the rows' updates are in flight together instead of
+                // one read-modify-write chain; same-address atomics of a
+                // thread apply in order, and a count never drops below
+                // its key, so no borrow crosses into the other lane's half)
+                std::uint32_t* const cw32 = reinterpret_cast<std::uint32_t*>(cnt) + (lane >> 1);
+                const unsigned csh = (lane & 1) * 16;
+#if OPC_SLIDE_PACKED_SUMS
+                // The winner's channel sums change by the masked entering
+                // minus leaving pixels.  They are accumulated packed: R and
+                // B as the 16-bit fields of one word, G (times 256) in a
+                // second -- plain 32-bit adds; every field total is within
+                // +-31 * 255, so the low field is the sign-extended low
+                // half and the high field what is left.
+                const unsigned incs = inc << csh;
+                // (32-bit shared-window addresses: one multiply-add per
+                // count word instead of a 64-bit generic address)
+                const std::uint32_t cw_s = static_cast<std::uint32_t>(__cvta_generic_to_shared(cw32));
+                const std::uint32_t half = csh ? 0x4432u : 0x4410u;  // PRMT: this lane's u16 half
+                std::uint32_t dall = 0;  // R + 256 G + 65536 B differences, summed
+                std::int32_t dg = 0;     // the G differences alone
+                std::uint32_t cand_k = 0;  // largest post-increment key of another bin
+#pragma unroll kUnrollUpdate
+                for (int k = 0; k < w2; ++k) {
+                    const std::uint32_t ei = cin[k], eo = cout[k];
+                    const std::uint32_t bi = bin_of(ei, bm), bo = bin_of(eo, bm);
+                    const unsigned d = bi != bo ? incs : 0u;
+                    std::uint32_t old;
+                    asm volatile("atom.shared.add.u32 %0, [%1], %2;"
+                                 : "=r"(old)
+                                 : "r"(cw_s + bi * 64u), "r"(d)
+                                 : "memory");
+                    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(cw_s + bo * 64u), "r"(0u - d)
+                                 : "memory");
+                    // this lane's key of bin bi after the update (a count
+                    // never overflows its half: no carry to drop; keys
+                    // order like their counts).  A bin whose count did
+                    // not move (d = 0) is already bounded by ub, so it
+                    // may join the candidates.
+                    const std::uint32_t key = __byte_perm(old + d, 0u, half);
+                    cand_k = max(cand_k, bi != static_cast<std::uint32_t>(best0) ? key : 0u);
+                    const std::uint32_t a = bi == static_cast<std::uint32_t>(best0) ? ei : 0u;
+                    const std::uint32_t b = bo == static_cast<std::uint32_t>(best0) ? eo : 0u;
+                    dall += a - b;                           // (plane words: top byte 0)
+                    dg = dp4a_us(a, 0x00000100u, dg);  // + G(a)
+                    dg = dp4a_us(b, 0x0000FF00u, dg);  // - G(b): byte 1 of the multiplier = -1
+                }
+                cand_c = static_cast<int>(cand_k >> kb_);  // (0 when no other bin was touched: ub >= 0)
+                {
+                    // dall - 256 dg = dR + 65536 dB with |dR|, |dB| <= 31 * 255:
+                    // dR is the sign-extended low half, dB what is left.
+                    const std::uint32_t drb = dall - (static_cast<std::uint32_t>(dg) << 8);
+                    const std::int32_t dr = static_cast<std::int16_t>(drb & 0xFFFFu);
+                    sr += static_cast<std::uint32_t>(dr);
+                    sb += static_cast<std::uint32_t>(
+                        static_cast<std::int32_t>(drb - static_cast<std::uint32_t>(dr)) >> 16);
+                    sg += static_cast<std::uint32_t>(dg);
+                }
+#else
+                for (int k = 0; k < w2; ++k) {
+                    const std::uint32_t ei = cin[k], eo = cout[k];
+                    const int bi = bin_of(ei, bm), bo = bin_of(eo, bm);
+                    const bool mv = bi != bo;
+                    const unsigned d = mv ? inc : 0u;
+                    unsigned ki;
+                    if (OPC_SLIDE_ATOMICS) {
+                        const unsigned old = atomicAdd(cw32 + bi * 16, d << csh);
+                        atomicSub(cw32 + bo * 16, d << csh);
+                        ki = ((old >> csh) & 0xFFFFu) + d;
                     } else {
-                        const int c = lane & (kStageCols - 1);
-                        for (int f0 = 0; f0 < 32; f0 += 32 / kStageCols) {  // 2 rows per store
-                            const int fr = f0 + lane / kStageCols;
-                            if (yb + f0 >= a.y_hi) break;
-                            if (c >= c_lo && c <= c_hi && yb + fr < a.y_hi) {
-                                const std::uint32_t v = stage[fr * kStageStride + c];
-                                std::uint8_t* o = out +
-                                                  static_cast<std::size_t>(yb + fr - a.out_row0) * stride +
-                                                  static_cast<std::size_t>(xb + c) * 3;
-                                o[0] = static_cast<std::uint8_t>(v);
-                                o[1] = static_cast<std::uint8_t>(v >> 8);
-                                o[2] = static_cast<std::uint8_t>(v >> 16);
+                        ki = cnt[bi * 32 + lane] + d;
+                        cnt[bi * 32 + lane] = static_cast<std::uint16_t>(ki);
+                        cnt[bo * 32 + lane] = static_cast<std::uint16_t>(cnt[bo * 32 + lane] - d);
+                    }
+                    const int ci = static_cast<int>(ki >> kb_);
+                    cand_c = (mv && bi != best0) ? max(cand_c, ci) : cand_c;
+                    const std::uint32_t mi = bi == best0 ? 0xFFFFFFFFu : 0u;
+                    const std::uint32_t mo = bo == best0 ? 0xFFFFFFFFu : 0u;
+                    sr += (ei & mi & 0xFFu) - (eo & mo & 0xFFu);
+                    sg += ((ei & mi) >> 8 & 0xFFu) - ((eo & mo) >> 8 & 0xFFu);
+                    sb += ((ei & mi) >> 16 & 0xFFu) - ((eo & mo) >> 16 & 0xFFu);
+                }
+#endif
+                // Resolve the winner (filter.hpp:71-82): it stays while its
+                // count is above every other bin's (bounded by ub);
+                // otherwise a rescan finds the lowest-index maximum.
+                ub = max(ub, cand_c);
+                const int bcf = cnt[best0 * 32 + lane] >> kb_;
+                bool changed = false;
+                const bool need = bcf <= ub;
+                if (!need) bc = bcf;
+                if (__any_sync(FULL, need)) {
+                    int nb, nc, nu;
+                    rescan(nb, nc, nu);
+                    if (need) {
+                        best = nb;
+                        bc = nc;
+                        ub = nu;
+                        changed = best != best0;
+                    }
+                }
+                if (changed) {
+                    tally(kOpSumPixels, static_cast<unsigned long long>(w2) * w2);
+                    tally(kOpWinnerChanges, 1);
+                }
+                // Winner changed: the new winner's window sums, one lane's
+                // window at a time with lane c < 2r+1 summing its column c
+                // (2r+1 loads per lane instead of (2r+1)^2 on one lane
+                // while the others wait).
+                const unsigned chg = __ballot_sync(FULL, changed);
+                if (__popc(chg) >= OPC_SLIDE_PAR_SUMS) {
+                    // many lanes changed at once (an edge crossing all
+                    // rows): each sums its own window, in parallel
+                    if (changed) {
+                        std::uint32_t cr = 0, cg = 0, cbb = 0;
+                        for (int c = 0; c < w2; ++c) {
+                            const std::uint32_t* col = ringp(x + c);
+#pragma unroll kUnrollSums
+                            for (int k = 0; k < w2; ++k) {
+                                const std::uint32_t e = col[k];
+                                if (static_cast<int>(bin_of(e, bm)) == best) {
+                                    cr += e & 0xFFu;
+                                    cg += (e >> 8) & 0xFFu;
+                                    cbb += (e >> 16) & 0xFFu;
+                                }
+                            }
+                        }
+                        sr = cr;
+                        sg = cg;
+                        sb = cbb;
+                    }
+                }
+                for (unsigned todo = __popc(chg) >= OPC_SLIDE_PAR_SUMS ? 0u : chg; todo; todo &= todo - 1) {
+                    const int j = __ffs(todo) - 1;
+                    const int bj = __shfl_sync(FULL, best, j);
+                    std::uint32_t cr = 0, cg = 0, cbb = 0;
+                    if (lane < w2) {
+                        const std::uint32_t* col = ringp(x + lane) - lane + j;
+#pragma unroll kUnrollChange
+                        for (int k = 0; k < w2; ++k) {
+                            const std::uint32_t e = col[k];
+                            if (static_cast<int>(bin_of(e, bm)) == bj) {
+                                cr += e & 0xFFu;
+                                cg += (e >> 8) & 0xFFu;
+                                cbb += (e >> 16) & 0xFFu;
                             }
                         }
                     }
-                    __syncwarp();
+                    cr = __reduce_add_sync(FULL, cr);
+                    cg = __reduce_add_sync(FULL, cg);
+                    cbb = __reduce_add_sync(FULL, cbb);
+                    if (lane == j) {
+                        sr = cr;
+                        sg = cg;
+                        sb = cbb;
+                    }
+                }
+                rgb = quotient();
+                }
+                if (row_ok) tally(kOpPixels, 1);
+                {
+                    const int xa = xs + x;
+                    flat_from = xa;
+                    stage[lane * kStageStride + (xa & (kStageCols - 1))] = rgb;
+                    if ((xa & (kStageCols - 1)) == kStageCols - 1 || x == n - 1) flush(xa);
                 }
                 cin += RR;
                 cout += RR;
                 if (cout >= ring_end) cout -= kRingCols * RR;
                 if (cin >= ring_end) cin -= kRingCols * RR;
+                ++x;
             }
         }
         // chunks requested but not consumed: wait, so no TMA write lands in

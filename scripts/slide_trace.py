@@ -41,3 +41,14 @@ for i in late:
 # per-band total time
 bt = np.bincount(kb, weights=dur)
 print("band time us (top 8):", [(int(b), round(bt[b]/1e3, 1)) for b in np.argsort(-bt)[:8]], "mean", round(bt.mean()/1e3, 1))
+# warp-time accounting: busy warp-time vs resident warp-time over the kernel span
+span = t1.max()
+nsm = len(np.unique(sm))
+print(f"busy warp-time {dur.sum()/1e3:.0f} us = {dur.sum()/span:.1f} warps busy on average over the span "
+      f"({nsm} SMs); cost per column-step by pass: p10 {np.percentile(dur/(x1-x0),10):.0f} ns "
+      f"p50 {np.percentile(dur/(x1-x0),50):.0f} p90 {np.percentile(dur/(x1-x0),90):.0f} max {(dur/(x1-x0)).max():.0f}")
+tl = np.linspace(0, span, 25)
+act = [int(((t0 <= a) & (t1 > a)).sum()) for a in tl[:-1]]
+print("passes in flight at 24 sample times:", act)
+if len(sys.argv) > 1:  # per-pass table for offline cost-model fits
+    np.savez_compressed(sys.argv[1], sm=sm, kb=kb, x0=x0, x1=x1, t0=t0, t1=t1)
