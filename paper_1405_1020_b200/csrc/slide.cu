@@ -62,6 +62,21 @@ namespace {
 #ifndef OPC_SLIDE_PACKED_SUMS
 #define OPC_SLIDE_PACKED_SUMS 1  // step updates: packed winner-sum differences, PRMT keys, 32-bit shared addresses (C3 slide 252 -> 213 us)
 #endif
+#ifndef OPC_SLIDE_RUNS
+#define OPC_SLIDE_RUNS 1  // steps whose rows form at most two runs of one (entering, leaving) bin pair: two weighted count updates
+#endif
+#ifndef OPC_SLIDE_BAND_ORDER
+#define OPC_SLIDE_BAND_ORDER 1  // the work plan takes the bands costliest first
+#endif
+#ifndef OPC_SLIDE_ROW_SUMS
+#define OPC_SLIDE_ROW_SUMS 1  // winner changes of several lanes to one bin: shared row sums + prefix differences
+#endif
+#ifndef OPC_SLIDE_JUMP
+#define OPC_SLIDE_JUMP 1  // flat stretches of kJumpMin phases or more: no ring loads, the stretch is emitted at once
+#endif
+#ifndef OPC_SLIDE_JUMP_MIN
+#define OPC_SLIDE_JUMP_MIN 4
+#endif
 #ifndef OPC_SLIDE_UNROLL_UPDATE
 #define OPC_SLIDE_UNROLL_UPDATE 7  // rows of a step's update loop in flight (A/B on C3: 1 / 3 / 7 / 11 / 21 rows -> 235 / 225 / 213 / 221 / 214 us)
 #endif
@@ -75,10 +90,10 @@ namespace {
 #define OPC_SLIDE_PLAN_K 1  // > 0: decreasing chunk sizes (remaining / (K x warps)), see TGeom
 #endif
 #ifndef OPC_SLIDE_PLAN_M
-#define OPC_SLIDE_PLAN_M 16  // smallest chunk of the decreasing plan: total / (M x warps)
+#define OPC_SLIDE_PLAN_M 4  // smallest chunk of the decreasing plan: total / (M x warps) (a pass start costs ~10 us: 16 -> 4 with the flat-stretch jumps, C3 -3%)
 #endif
 #ifndef OPC_SLIDE_COST_K
-#define OPC_SLIDE_COST_K 24  // cost of a window-changing step in flat steps (work plan)
+#define OPC_SLIDE_COST_K 200  // cost of a window-changing step in flat columns (work plan; fitted on per-pass traces: ~1.9 us against ~9 ns once flat stretches are jumped)
 #endif
 #ifndef OPC_SLIDE_PAR_SUMS
 #define OPC_SLIDE_PAR_SUMS 4  // winner changes in one step from which lanes sum their windows in parallel
@@ -91,7 +106,7 @@ constexpr int kWarps = 8;  // upper bound; the launcher fits as many as 227 KB a
 // Ring of entry columns, filled by TMA in chunks of kChunk columns: kSlots
 // chunks, i.e. the window (2r+1 <= 31 columns) + the phase being slid + two
 // chunks in flight.  Column c of a pass (image column xs - r + c) lives in
-// chunk k = (c - B) / kChunk with B = 2r - kChunk * K0, K0 = ceil(2r / kChunk):
+// chunk k = (c - B) / kChunk with B = 2r - kChunk * K0, K0 = ceil((2r + 1) / kChunk):
 // phase p (output columns 16p .. 16p+15) enters exactly chunk p + K0.
 constexpr int kChunk = 16;
 constexpr int kSlots = 5;
@@ -100,6 +115,7 @@ constexpr int kUnrollScan = OPC_SLIDE_UNROLL_SCAN;
 constexpr int kUnrollSums = OPC_SLIDE_UNROLL_SUMS;
 constexpr int kUnrollChange = OPC_SLIDE_UNROLL_CHANGE;
 constexpr int kUnrollUpdate = OPC_SLIDE_UNROLL_UPDATE;
+constexpr int kJumpMin = OPC_SLIDE_JUMP_MIN;
 constexpr int kStageCols = 16;   // output columns staged per flush (== kChunk)
 constexpr int kStageStride = 17;
 constexpr int kRecipBytes = 1024 * 4;
@@ -107,7 +123,9 @@ constexpr int kTRows = 32;
 constexpr int kTCols = 128;
 
 __host__ __device__ inline int ring_rows(int r) { return (32 + 2 * r + 3) & ~3; }  // 16-B rows
-__host__ __device__ inline int chunk_k0(int r) { return (2 * r + kChunk - 1) / kChunk; }
+// chunks spanned by a window's 2r + 1 columns (so the column a step removes, x - 1,
+// is in chunk p of phase p, never in the slot being refilled)
+__host__ __device__ inline int chunk_k0(int r) { return (2 * r + kChunk) / kChunk; }
 
 // Per-warp shared memory, 128-byte aligned pieces (TMA boxes):
 //   ring  kRingCols x ring_rows u32 | out tile 32 rows x 48 bytes |
@@ -143,6 +161,7 @@ struct TGeom {
                            // 32 blk + x changes the window (not flat)
     std::uint32_t* bc;     // [frame][nband][nblk]: cost of the block's columns
     int* cs;               // [nch + 1]: first block of each chunk
+    int* perm;             // [frames x nbands]: the plan's band order (position -> band), costliest first
     // Decreasing chunk sizes (OPC_SLIDE_PLAN_K > 0): chunk j covers the cost
     // fractions [1 - q^j, 1 - q^(j+1)) with q = 1 - 1 / (K x resident) -- each
     // the remaining cost / (K x resident), guided self-scheduling precomputed --
@@ -192,6 +211,7 @@ __host__ inline TGeom tgeom(const BandArgs& a, void* scratch = nullptr, long lon
         g.bc = p;
         p += blocks;
         g.cs = reinterpret_cast<int*>(p);
+        g.perm = g.cs + blocks + 2;
     }
     return g;
 }
@@ -201,7 +221,8 @@ __host__ inline std::size_t tgeom_bytes(const BandArgs& a) {
     const long long blocks = static_cast<long long>(a.frames) * g.nbands * g.nblk;
     // plan_chunks never exceeds the block count (+1 for the end marker)
     return (g.frame_elems * a.frames + static_cast<std::size_t>(a.frames) * g.ntr * g.ncols +
-            2 * static_cast<std::size_t>(blocks) + static_cast<std::size_t>(blocks) + 2) *
+            2 * static_cast<std::size_t>(blocks) + static_cast<std::size_t>(blocks) + 2 +
+            static_cast<std::size_t>(a.frames) * g.nbands) *
            sizeof(std::uint32_t);
 }
 
@@ -364,16 +385,54 @@ __global__ void __launch_bounds__(kPlanThreads) slide_plan_kernel(BandArgs a, TG
     // coalesced copy through L2 -- other CTAs wrote them).
     const int t = threadIdx.x;
     if (t == 0) *done = 0u;  // every CTA has arrived: ready for the next launch
+    // Band order of the plan: costliest bands first.  The estimates are worst
+    // where the content is busiest (rescans, winner changes and non-flat pass
+    // starts are not in them), and the guided plan's chunks shrink along the
+    // order: the busy bands get the early, large chunks and the tail is flat,
+    // predictable work.  (Up to kPlanThreads bands; more keep their order.)
+    const int nb = a.frames * g.nbands;
+    __shared__ std::uint32_t band_cost[kPlanThreads];
+    __shared__ int band_at[kPlanThreads];  // position -> band
+    const bool ordered = OPC_SLIDE_BAND_ORDER && nb <= kPlanThreads;
+    if (ordered) {
+        if (t < nb) {
+            std::uint32_t c = 0;
+            for (int j = 0; j < g.nblk; ++j) c += __ldcg(g.bc + static_cast<long long>(t) * g.nblk + j);
+            band_cost[t] = c;
+        }
+        __syncthreads();
+        if (t < nb) {
+            const std::uint32_t c = band_cost[t];
+            int rank = 0;
+            for (int j = 0; j < nb; ++j) {
+                const std::uint32_t o = band_cost[j];
+                rank += (o > c || (o == c && j < t)) ? 1 : 0;
+            }
+            band_at[rank] = t;
+            g.perm[rank] = t;
+        }
+        __syncthreads();
+    } else {
+        for (int i = t; i < nb; i += kPlanThreads) g.perm[i] = i;
+    }
+    // block at position i of the plan's order
+    auto block_at = [&](long long i) -> long long {
+        if (!ordered) return i;
+        const long long pos = i / g.nblk;
+        return static_cast<long long>(band_at[pos]) * g.nblk + (i - pos * g.nblk);
+    };
     const bool staged = nblocks <= smem_cap;
     if (staged) {
         // (padded: entry b at b + b / 16, so 16 consecutive blocks per lane
         // read conflict-free)
-        for (long long i = t; i < nblocks; i += kPlanThreads) sbc[i + (i >> 4)] = __ldcg(g.bc + i);
+        for (long long i = t; i < nblocks; i += kPlanThreads) sbc[i + (i >> 4)] = __ldcg(g.bc + block_at(i));
     }
     for (int i = t; i <= g.nch; i += kPlanThreads) g.cs[i] = static_cast<int>(nblocks);
     __syncthreads();
     PLAN_TICK(1);
-    auto cost = [&](long long b) -> std::uint32_t { return staged ? sbc[b + (b >> 4)] : __ldcg(g.bc + b); };
+    auto cost = [&](long long b) -> std::uint32_t {
+        return staged ? sbc[b + (b >> 4)] : __ldcg(g.bc + block_at(b));
+    };
     // Thread t owns a contiguous run of blocks [t * per, (t + 1) * per): the
     // run sums, one CTA scan of the 1024 sums (warp shuffles + the 32 warp
     // totals), then each thread walks its run in registers to get every
@@ -449,11 +508,23 @@ __device__ __forceinline__ std::uint32_t bin_of(std::uint32_t e, std::uint32_t b
     return __umulhi(s, bin_mul);                          // filter.hpp:31-35
 }
 
+#if !OPC_SLIDE_TRACE
+#define SEC_ADD(i, t0) do { } while (0)
+#define SEC_NOW() 0ll
+#endif
 #if OPC_SLIDE_TRACE
 // Debug trace of the passes (OPC_SLIDE_TRACE builds only): per pass
 // {smid << 48 | kb << 24 | x0, x1, start ns, end ns}.
 __device__ unsigned long long g_trace[1 << 16][4];
 __device__ int g_trace_n;
+// Section clocks (lane 0 of every warp, summed): 0 pass start (claim to first
+// output), 1 step walk (bins, sums, change points), 2 count updates, 3 winner
+// resolution (rescans), 4 winner-change sums, 5 flat emission, 6 jumps,
+// 7 single-column emit + flush, 8 phase top (ring waits / requests).
+__device__ unsigned long long g_sec[16];
+#define SEC_T0() const long long sec_t0_ = clock64()
+#define SEC_ADD(i, t0) do { if (lane == 0) sec_acc[i] += clock64() - (t0); } while (0)
+#define SEC_NOW() clock64()
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -471,6 +542,7 @@ __global__ void __launch_bounds__(kWarps * 32)
     slide_kernel(BandArgs a, TGeom tg, int* task_counter, WorkSplit g,
                  const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout) {
     unsigned long long opc_n[kOpCountN] = {};
+    [[maybe_unused]] long long sec_acc[16] = {};
     auto tally = [&](int k, unsigned long long v) {
         if constexpr (COUNT) opc_n[k] += v;
     };
@@ -519,6 +591,11 @@ __global__ void __launch_bounds__(kWarps * 32)
     int f, kb, x0, x1;
     while (next_pass<(OPC_SLIDE_GUIDED_K > 0), (OPC_SLIDE_PLAN != 0)>(g, task_counter, lane, u, u_end, f, kb,
                                                                        x0, x1)) {
+        if (OPC_SLIDE_PLAN) {  // the plan's band order (position -> band)
+            const int band = __ldg(tg.perm + f * tg.nbands + kb);
+            f = band / tg.nbands;
+            kb = band - f * tg.nbands;
+        }
 #if OPC_SLIDE_TRACE
         int pass_cols = x1 - x0;
         const unsigned long long t_start = gtime();
@@ -542,6 +619,7 @@ __global__ void __launch_bounds__(kWarps * 32)
             }
         } trace_guard{kb, x0, pass_cols, lane, 0, t_start};
 #endif
+        [[maybe_unused]] const long long t_pass = SEC_NOW();
         const int yb = a.y_lo + 32 * kb;
         const int xs = a.x_lo + x0;
         const int xe = a.x_lo + x1;
@@ -553,7 +631,7 @@ __global__ void __launch_bounds__(kWarps * 32)
         const int kmax = (n - 1 + 2 * r - B) / kChunk;
         // ring position (u32 offset) of pass column c: chunk (c - B) / 16 in
         // slot (q0 + chunk) % kSlots -- i.e. (16 * (q0 % kSlots) + c - B) mod 80
-        const int pos0 = kChunk * static_cast<int>(q0 % kSlots) - B;
+        int pos0 = kChunk * static_cast<int>(q0 % kSlots) - B;  // (re-based by a jump over flat phases)
         auto ringp = [&](int c) { return ring + ((pos0 + c) % kRingCols) * RR + lane; };
         auto issue = [&](int k) {  // lane 0: chunk k of the pass
             const unsigned q = q0 + static_cast<unsigned>(k);
@@ -690,6 +768,7 @@ __global__ void __launch_bounds__(kWarps * 32)
             return __umulhi(sr << 1, m) | (__umulhi(sg << 1, m) << 8) | (__umulhi(sb << 1, m) << 16);
         };
         std::uint32_t rgb = quotient();
+        SEC_ADD(0, t_pass);
 
         // entering column x + 2r and leaving column x - 1 of step x, as ring
         // pointers advanced by one column per step (the leaving pointer wraps)
@@ -699,15 +778,174 @@ __global__ void __launch_bounds__(kWarps * 32)
         // interior column 32 j + x changes the window
         const std::uint32_t* nfb = tg.nf + (static_cast<std::size_t>(f) * tg.nbands + kb) * tg.nblk;
         int flat_from = xs;  // image column from which every output so far equals rgb
-        for (int p = 0; kStageCols * p < n; ++p) {
-            std::uint32_t nfm;  // bit i: the step at pass column 16p + i is not flat
-            {
-                const int xi = x0 + kStageCols * p;
-                const int j = xi >> 5;
-                const std::uint32_t lo = nfb[j];
-                const std::uint32_t hi = j + 1 < tg.nblk ? nfb[j + 1] : 0u;
-                nfm = __funnelshift_r(lo, hi, xi & 31);
+        // A block of 16 columns of one colour (a flat run covering a whole
+        // output block): every row of the out tile is the 3-word pattern of
+        // rgb repeated -- packed from the register, no staging.
+        auto flush_flat = [&](const int xb) {
+            if (lane == 0) bulk_wait_read0();  // the previous store has read the tile
+            __syncwarp();
+            const std::uint32_t w0 = rgb | (rgb << 24), w1 = (rgb >> 8) | (rgb << 16),
+                                w2_ = (rgb >> 16) | (rgb << 8);
+            uint4* orow = reinterpret_cast<uint4*>(otile + lane * 48);
+            orow[0] = make_uint4(w0, w1, w2_, w0);
+            orow[1] = make_uint4(w1, w2_, w0, w1);
+            orow[2] = make_uint4(w2_, w0, w1, w2_);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+                tma_store_3d(&tout, otile, 3 * xb, yb - a.out_row0, f);
+                bulk_commit();
             }
+            __syncwarp();
+        };
+        // Flush of the output block holding image column xa, its last
+        // staged column (x = the pass column of xa).  Output blocks are 16
+        // image columns [16m, 16m + 15] (a TMA store box must start 16-byte
+        // aligned: 48m bytes); the partial blocks at the ends of a pass are
+        // written with byte stores.
+        auto flush = [&](const int xa) {
+            const int xb = xa & ~(kStageCols - 1);      // image column of stage column 0
+            if (TMA_OUT && xa - xb == kStageCols - 1 && flat_from <= xb && xb >= xs) {
+                flush_flat(xb);  // no step changed the window since the block began
+                return;
+            }
+            __syncwarp();
+            const int c_lo = max(xs, xb) - xb;          // valid stage columns [c_lo, c_hi]
+            const int c_hi = xa - xb;
+            if (TMA_OUT && c_lo == 0 && c_hi == kStageCols - 1) {
+                // lane t packs row t's 16 pixels into 48 bytes of the out
+                // tile; one TMA store writes the 32 x 48-byte box (rows
+                // past the band end are clipped by the tensor map)
+                if (lane == 0) bulk_wait_read0();  // the previous store has read the tile
+                __syncwarp();
+                const std::uint32_t* srow = stage + lane * kStageStride;
+                std::uint32_t wv[12];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {  // pixels 4j .. 4j+3 -> words 3j .. 3j+2
+                    const std::uint32_t p0 = srow[4 * j], p1 = srow[4 * j + 1],
+                                        p2 = srow[4 * j + 2], p3 = srow[4 * j + 3];
+                    wv[3 * j] = p0 | (p1 << 24);
+                    wv[3 * j + 1] = (p1 >> 8) | (p2 << 16);
+                    wv[3 * j + 2] = (p2 >> 16) | (p3 << 8);
+                }
+                uint4* orow = reinterpret_cast<uint4*>(otile + lane * 48);
+                orow[0] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                orow[1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
+                orow[2] = make_uint4(wv[8], wv[9], wv[10], wv[11]);
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_3d(&tout, otile, 3 * xb, yb - a.out_row0, f);
+                    bulk_commit();
+                }
+            } else {
+                const int c = lane & (kStageCols - 1);
+                for (int f0 = 0; f0 < 32; f0 += 32 / kStageCols) {  // 2 rows per store
+                    const int fr = f0 + lane / kStageCols;
+                    if (yb + f0 >= a.y_hi) break;
+                    if (c >= c_lo && c <= c_hi && yb + fr < a.y_hi) {
+                        const std::uint32_t v = stage[fr * kStageStride + c];
+                        std::uint8_t* o = out +
+                                          static_cast<std::size_t>(yb + fr - a.out_row0) * stride +
+                                          static_cast<std::size_t>(xb + c) * 3;
+                        o[0] = static_cast<std::uint8_t>(v);
+                        o[1] = static_cast<std::uint8_t>(v >> 8);
+                        o[2] = static_cast<std::uint8_t>(v >> 16);
+                    }
+                }
+            }
+            __syncwarp();
+        };
+        // Columns xf .. xf + cnt - 1 of the pass, all equal to rgb (flat steps).
+        auto emit_flat = [&](const int xf, const int cnt) {
+            tally(kOpSteps, static_cast<unsigned long long>(cnt - (xf == 0 ? 1 : 0)));
+            if (row_ok) tally(kOpPixels, static_cast<unsigned long long>(cnt));
+            for (int done = 0; done < cnt;) {
+                const int xa = xs + xf + done;
+                const int c0 = xa & (kStageCols - 1);
+                const int seg = min(cnt - done, kStageCols - c0);
+                if (TMA_OUT && seg == kStageCols) {
+                    flush_flat(xa);
+                } else {
+                    std::uint32_t* sp = stage + lane * kStageStride + c0;
+#pragma unroll
+                    for (int i = 0; i < kStageCols; ++i) {
+                        if (i < seg) sp[i] = rgb;
+                    }
+                    if (c0 + seg == kStageCols || xf + done + seg == n) flush(xa + seg - 1);
+                }
+                done += seg;
+            }
+        };
+        // (the words of the next phase are loaded a phase ahead: an L2 round
+        // trip per 16 columns would otherwise be most of a flat phase)
+        std::uint32_t nf_lo, nf_hi;
+        auto nf_load = [&](const int p) {
+            const int j = (x0 + kStageCols * p) >> 5;
+            nf_lo = j < tg.nblk ? __ldg(nfb + j) : 0u;
+            nf_hi = j + 1 < tg.nblk ? __ldg(nfb + j + 1) : 0u;
+        };
+        nf_load(0);
+        for (int p = 0; kStageCols * p < n; ++p) {
+            // bit i: the step at pass column 16p + i is not flat
+            const std::uint32_t nfm = __funnelshift_r(nf_lo, nf_hi, (x0 + kStageCols * p) & 31);
+            nf_load(p + 1);
+#if OPC_SLIDE_JUMP
+            // Flat stretches: flat steps read no pixels, so the ring need not
+            // follow them.  When this phase and the next hold no window-
+            // changing step, look for the next one (one coalesced load of the
+            // coming 32 nonflat words); if it is kJumpMin phases or more away,
+            // emit the stretch at once and restart the ring at that step's
+            // phase (the counts, the winner and its sums are unchanged).
+            if (OPC_SLIDE_PLAN && p > 0 && nfm == 0u && kStageCols * (p + kJumpMin) < n + kStageCols) {
+                const int xi = x0 + kStageCols * p;
+                const int j = xi >> 5, jl = (x0 + n - 1) >> 5;
+                std::uint32_t w = j + lane <= jl ? __ldg(nfb + j + lane) : 0u;
+                if (lane == 0) w &= 0xFFFFFFFFu << (xi & 31);
+                const unsigned any = __ballot_sync(FULL, w != 0u);
+                int xn;  // pass column of the next window-changing step (or past the words looked at)
+                if (any) {
+                    const int l = __ffs(any) - 1;
+                    xn = 32 * (j + l) + __ffs(__shfl_sync(FULL, w, l)) - 1 - x0;
+                } else {
+                    xn = 32 * (j + 32) - x0;
+                }
+                const int p2 = xn >= n ? (n + kStageCols - 1) / kStageCols : xn / kStageCols;
+                if (p2 - p >= kJumpMin) {
+                    [[maybe_unused]] const long long t_j = SEC_NOW();
+                    emit_flat(kStageCols * p, min(n, kStageCols * p2) - kStageCols * p);
+                    if (kStageCols * p2 >= n) {
+                        SEC_ADD(6, t_j);
+                        break;  // the pass ends flat
+                    }
+                    // every chunk in flight lands before the ring is re-based
+                    for (int k = kwaited + 1; k <= kissued; ++k) wait(k);
+                    // chunk p2 (the column step 16 p2 removes) takes the next
+                    // slot in issue order: q0 + p2 = the next q, up to a multiple
+                    // of 2 kSlots (slot and parity of a q repeat with that period)
+                    const unsigned qn = q0 + static_cast<unsigned>(kissued + 1);
+                    const unsigned per = 2u * kSlots;
+                    q0 = qn + (static_cast<unsigned>(p2) + per - 1) / per * per - static_cast<unsigned>(p2);
+                    pos0 = kChunk * static_cast<int>(q0 % kSlots) - B;
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    // (chunks p2 .. p2 + kSlots - 2: phase p2 requests the next one itself)
+                    kissued = min(kmax, p2 + kSlots - 2);
+                    if (lane == 0) {
+                        for (int k = p2; k <= kissued; ++k) issue(k);
+                    }
+                    kwaited = min(kmax, p2 + K0);
+                    for (int k = p2; k <= kwaited; ++k) wait(k);
+                    cin = ringp(kStageCols * p2 + 2 * r);
+                    cout = ringp(kStageCols * p2 - 1);
+                    p = p2 - 1;
+                    nf_load(p2);
+                    SEC_ADD(6, t_j);
+                    continue;
+                }
+            }
+#endif
+            [[maybe_unused]] const long long t_top = SEC_NOW();
             if (p > 0) {
                 // phase p enters chunk p + K0; the slot of chunk p - 1 is free:
                 // request chunk p + kSlots - 1
@@ -722,85 +960,8 @@ __global__ void __launch_bounds__(kWarps * 32)
                     kissued = p + kSlots - 1;
                 }
             }
+            SEC_ADD(8, t_top);
             const int xend = min(n, kStageCols * p + kStageCols);
-            // A block of 16 columns of one colour (a flat run covering a whole
-            // output block): every row of the out tile is the 3-word pattern of
-            // rgb repeated -- packed from the register, no staging.
-            auto flush_flat = [&](const int xb) {
-                if (lane == 0) bulk_wait_read0();  // the previous store has read the tile
-                __syncwarp();
-                const std::uint32_t w0 = rgb | (rgb << 24), w1 = (rgb >> 8) | (rgb << 16),
-                                    w2_ = (rgb >> 16) | (rgb << 8);
-                uint4* orow = reinterpret_cast<uint4*>(otile + lane * 48);
-                orow[0] = make_uint4(w0, w1, w2_, w0);
-                orow[1] = make_uint4(w1, w2_, w0, w1);
-                orow[2] = make_uint4(w2_, w0, w1, w2_);
-                fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) {
-                    tma_store_3d(&tout, otile, 3 * xb, yb - a.out_row0, f);
-                    bulk_commit();
-                }
-                __syncwarp();
-            };
-            // Flush of the output block holding image column xa, its last
-            // staged column (x = the pass column of xa).  Output blocks are 16
-            // image columns [16m, 16m + 15] (a TMA store box must start 16-byte
-            // aligned: 48m bytes); the partial blocks at the ends of a pass are
-            // written with byte stores.
-            auto flush = [&](const int xa) {
-                const int xb = xa & ~(kStageCols - 1);      // image column of stage column 0
-                if (TMA_OUT && xa - xb == kStageCols - 1 && flat_from <= xb && xb >= xs) {
-                    flush_flat(xb);  // no step changed the window since the block began
-                    return;
-                }
-                __syncwarp();
-                const int c_lo = max(xs, xb) - xb;          // valid stage columns [c_lo, c_hi]
-                const int c_hi = xa - xb;
-                if (TMA_OUT && c_lo == 0 && c_hi == kStageCols - 1) {
-                    // lane t packs row t's 16 pixels into 48 bytes of the out
-                    // tile; one TMA store writes the 32 x 48-byte box (rows
-                    // past the band end are clipped by the tensor map)
-                    if (lane == 0) bulk_wait_read0();  // the previous store has read the tile
-                    __syncwarp();
-                    const std::uint32_t* srow = stage + lane * kStageStride;
-                    std::uint32_t wv[12];
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {  // pixels 4j .. 4j+3 -> words 3j .. 3j+2
-                        const std::uint32_t p0 = srow[4 * j], p1 = srow[4 * j + 1],
-                                            p2 = srow[4 * j + 2], p3 = srow[4 * j + 3];
-                        wv[3 * j] = p0 | (p1 << 24);
-                        wv[3 * j + 1] = (p1 >> 8) | (p2 << 16);
-                        wv[3 * j + 2] = (p2 >> 16) | (p3 << 8);
-                    }
-                    uint4* orow = reinterpret_cast<uint4*>(otile + lane * 48);
-                    orow[0] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-                    orow[1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
-                    orow[2] = make_uint4(wv[8], wv[9], wv[10], wv[11]);
-                    fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) {
-                        tma_store_3d(&tout, otile, 3 * xb, yb - a.out_row0, f);
-                        bulk_commit();
-                    }
-                } else {
-                    const int c = lane & (kStageCols - 1);
-                    for (int f0 = 0; f0 < 32; f0 += 32 / kStageCols) {  // 2 rows per store
-                        const int fr = f0 + lane / kStageCols;
-                        if (yb + f0 >= a.y_hi) break;
-                        if (c >= c_lo && c <= c_hi && yb + fr < a.y_hi) {
-                            const std::uint32_t v = stage[fr * kStageStride + c];
-                            std::uint8_t* o = out +
-                                              static_cast<std::size_t>(yb + fr - a.out_row0) * stride +
-                                              static_cast<std::size_t>(xb + c) * 3;
-                            o[0] = static_cast<std::uint8_t>(v);
-                            o[1] = static_cast<std::uint8_t>(v >> 8);
-                            o[2] = static_cast<std::uint8_t>(v >> 16);
-                        }
-                    }
-                }
-                __syncwarp();
-            };
             int x = kStageCols * p;
             while (x < xend) {
                 // Flat steps ahead of x (the work plan's nonflat bits; step 0
@@ -823,24 +984,9 @@ __global__ void __launch_bounds__(kWarps * 32)
                     run = __any_sync(FULL, diff) ? 0 : 1;
                 }
                 if (run > 0) {
-                    tally(kOpSteps, static_cast<unsigned long long>(run - (x == 0 ? 1 : 0)));
-                    if (row_ok) tally(kOpPixels, static_cast<unsigned long long>(run));
-                    for (int done = 0; done < run;) {  // at most two output blocks
-                        const int xa = xs + x + done;
-                        const int c0 = xa & (kStageCols - 1);
-                        const int seg = min(run - done, kStageCols - c0);
-                        if (TMA_OUT && seg == kStageCols) {
-                            flush_flat(xa);
-                        } else {
-                            std::uint32_t* sp = stage + lane * kStageStride + c0;
-#pragma unroll
-                            for (int i = 0; i < kStageCols; ++i) {
-                                if (i < seg) sp[i] = rgb;
-                            }
-                            if (c0 + seg == kStageCols || x + done + seg == n) flush(xa + seg - 1);
-                        }
-                        done += seg;
-                    }
+                    [[maybe_unused]] const long long t_f = SEC_NOW();
+                    emit_flat(x, run);
+                    SEC_ADD(5, t_f);
                     cin += run * RR;
                     cout += run * RR;
                     if (cout >= ring_end) cout -= kRingCols * RR;
@@ -849,10 +995,10 @@ __global__ void __launch_bounds__(kWarps * 32)
                     continue;
                 }
                 // A step that changes the window (x > 0).
+                [[maybe_unused]] const long long t_s1 = SEC_NOW();
                 // Slide: add ring column x + 2r (image x + r), remove x - 1 (image x - r - 1).
                 tally(kOpSteps, 1);
                 {
-                tally(kOpUpdates, 2ull * w2);
                 if (lane == 0) tally(kOpNonFlatSteps, 1);
                 const int best0 = best;
                 int cand_c = -1;  // the largest post-increment count of another bin
@@ -869,11 +1015,21 @@ __global__ void __launch_bounds__(kWarps * 32)
                 const unsigned csh = (lane & 1) * 16;
 #if OPC_SLIDE_PACKED_SUMS
                 // The winner's channel sums change by the masked entering
-                // minus leaving pixels.  They are accumulated packed: R and
-                // B as the 16-bit fields of one word, G (times 256) in a
-                // second -- plain 32-bit adds; every field total is within
-                // +-31 * 255, so the low field is the sign-extended low
-                // half and the high field what is left.
+                // minus leaving pixels.  They are accumulated packed: the
+                // whole 24-bit words in one accumulator (one add per row) and
+                // G alone in a second (two dot products per row); every
+                // channel total is within +-31 * 255, so the packed total
+                // decodes exactly after the loop.
+                //
+                // Count updates: a shared-memory atomic costs ~2 cycles per
+                // lane, so 2(2r+1) of them are most of a step.  The rows of a
+                // step are first walked without touching the counts (bins,
+                // sums, and the rows where the (entering, leaving) bin pair
+                // changes); when every lane sees at most one such change --
+                // an edge that crosses the window's rows, with at most one
+                // corner or horizontal edge in them -- the step is two
+                // weighted updates per lane (rows above / below the change)
+                // instead of one per row.  Other steps update row by row.
                 const unsigned incs = inc << csh;
                 // (32-bit shared-window addresses: one multiply-add per
                 // count word instead of a 64-bit generic address)
@@ -882,11 +1038,7 @@ __global__ void __launch_bounds__(kWarps * 32)
                 std::uint32_t dall = 0;  // R + 256 G + 65536 B differences, summed
                 std::int32_t dg = 0;     // the G differences alone
                 std::uint32_t cand_k = 0;  // largest post-increment key of another bin
-#pragma unroll kUnrollUpdate
-                for (int k = 0; k < w2; ++k) {
-                    const std::uint32_t ei = cin[k], eo = cout[k];
-                    const std::uint32_t bi = bin_of(ei, bm), bo = bin_of(eo, bm);
-                    const unsigned d = bi != bo ? incs : 0u;
+                auto move = [&](const std::uint32_t bi, const std::uint32_t bo, const unsigned d) {
                     std::uint32_t old;
                     asm volatile("atom.shared.add.u32 %0, [%1], %2;"
                                  : "=r"(old)
@@ -895,18 +1047,58 @@ __global__ void __launch_bounds__(kWarps * 32)
                     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(cw_s + bo * 64u), "r"(0u - d)
                                  : "memory");
                     // this lane's key of bin bi after the update (a count
-                    // never overflows its half: no carry to drop; keys
-                    // order like their counts).  A bin whose count did
-                    // not move (d = 0) is already bounded by ub, so it
-                    // may join the candidates.
+                    // never overflows its half -- the pixels leaving are in
+                    // other bins -- so there is no carry to drop; keys order
+                    // like their counts).  A bin whose count did not move
+                    // (d = 0) is already bounded by ub, so it may join the
+                    // candidates; so may a count a later update lowers again.
                     const std::uint32_t key = __byte_perm(old + d, 0u, half);
                     cand_k = max(cand_k, bi != static_cast<std::uint32_t>(best0) ? key : 0u);
+                };
+                std::uint32_t pair0 = 0, prev = 0;  // bi | bo << 16 of row 0 / of the previous row
+                int ncp = 0, split = 0;             // rows k >= 1 whose pair differs from row k - 1; the last one
+#pragma unroll kUnrollUpdate
+                for (int k = 0; k < w2; ++k) {
+                    const std::uint32_t ei = cin[k], eo = cout[k];
+                    const std::uint32_t bi = bin_of(ei, bm), bo = bin_of(eo, bm);
+                    const std::uint32_t pair = bi | (bo << 16);
+                    if (k == 0) pair0 = pair;
+                    const bool cp = k > 0 && pair != prev;
+                    ncp += cp ? 1 : 0;
+                    split = cp ? k : split;
+                    prev = pair;
                     const std::uint32_t a = bi == static_cast<std::uint32_t>(best0) ? ei : 0u;
                     const std::uint32_t b = bo == static_cast<std::uint32_t>(best0) ? eo : 0u;
-                    dall += a - b;                           // (plane words: top byte 0)
+                    dall += a - b;                     // (plane words: top byte 0)
                     dg = dp4a_us(a, 0x00000100u, dg);  // + G(a)
                     dg = dp4a_us(b, 0x0000FF00u, dg);  // - G(b): byte 1 of the multiplier = -1
                 }
+                SEC_ADD(1, t_s1);
+                [[maybe_unused]] const long long t_s2 = SEC_NOW();
+                if (OPC_SLIDE_RUNS && __all_sync(FULL, ncp <= 1)) {
+                    const int n1 = ncp ? split : w2;  // rows of the first run
+                    tally(kOpUpdates, ncp ? 4 : 2);
+                    {
+                        const std::uint32_t bi = pair0 & 0xFFFFu, bo = pair0 >> 16;
+                        move(bi, bo, bi != bo ? static_cast<unsigned>(n1) * incs : 0u);
+                    }
+                    if (__any_sync(FULL, ncp != 0)) {
+                        const std::uint32_t bi = prev & 0xFFFFu, bo = prev >> 16;
+                        move(bi, bo, bi != bo ? static_cast<unsigned>(w2 - n1) * incs : 0u);
+                    }
+                } else {
+                    // Branch-free form: every row pays two count updates (of
+                    // zero when the pixel does not change bin), so lanes whose
+                    // changes sit at different rows do not diverge.
+                    tally(kOpUpdates, 2ull * w2);
+#pragma unroll kUnrollUpdate
+                    for (int k = 0; k < w2; ++k) {
+                        const std::uint32_t bi = bin_of(cin[k], bm), bo = bin_of(cout[k], bm);
+                        move(bi, bo, bi != bo ? incs : 0u);
+                    }
+                }
+                SEC_ADD(2, t_s2);
+                [[maybe_unused]] const long long t_s3 = SEC_NOW();
                 cand_c = static_cast<int>(cand_k >> kb_);  // (0 when no other bin was touched: ub >= 0)
                 {
                     // dall - 256 dg = dR + 65536 dB with |dR|, |dB| <= 31 * 255:
@@ -961,19 +1153,80 @@ __global__ void __launch_bounds__(kWarps * 32)
                         changed = best != best0;
                     }
                 }
-                if (changed) {
-                    tally(kOpSumPixels, static_cast<unsigned long long>(w2) * w2);
-                    tally(kOpWinnerChanges, 1);
-                }
+                if (changed) tally(kOpWinnerChanges, 1);
                 // Winner changed: the new winner's window sums, one lane's
                 // window at a time with lane c < 2r+1 summing its column c
                 // (2r+1 loads per lane instead of (2r+1)^2 on one lane
                 // while the others wait).
+                SEC_ADD(3, t_s3);
+                [[maybe_unused]] const long long t_s4 = SEC_NOW();
                 const unsigned chg = __ballot_sync(FULL, changed);
-                if (__popc(chg) >= OPC_SLIDE_PAR_SUMS) {
-                    // many lanes changed at once (an edge crossing all
-                    // rows): each sums its own window, in parallel
-                    if (changed) {
+                unsigned todo = chg;
+#if OPC_SLIDE_ROW_SUMS
+                // Several lanes with one new winner (an edge crossing the
+                // band): their windows are rows t .. t + 2r of the same 2r + 1
+                // columns, so the warp sums that bin once per ring row (lane t:
+                // rows t and 32 + t) and every lane takes the difference of
+                // two prefix sums over the rows -- 2(2r + 1) loads per lane
+                // instead of (2r + 1)^2.  R, G, B travel as 21-bit fields of
+                // one 64-bit word (a prefix is at most 62 rows x 31 x 255).
+                while (__popc(todo) >= OPC_SLIDE_PAR_SUMS) {
+                    const int bj = __shfl_sync(FULL, best, __ffs(todo) - 1);
+                    const unsigned grp = __ballot_sync(FULL, ((todo >> lane) & 1u) != 0u && best == bj);
+                    if (2 * __popc(grp) < __popc(todo)) break;  // many winners: own windows, below
+                    std::uint32_t rb0 = 0, g0 = 0, rb1 = 0, g1 = 0;
+                    const std::uint32_t* colb = ringp(x) - lane;  // row 0 of column x
+                    const bool two = lane < 2 * r;
+                    tally(kOpSumPixels, static_cast<unsigned long long>(two ? 2 * w2 : w2));
+#pragma unroll 3
+                    for (int c = 0; c < w2; ++c) {
+                        const std::uint32_t e0 = colb[lane];
+                        const std::uint32_t e1 = two ? colb[lane + 32] : 0u;
+                        const std::uint32_t a0 = static_cast<int>(bin_of(e0, bm)) == bj ? e0 : 0u;
+                        const std::uint32_t a1 = (two && static_cast<int>(bin_of(e1, bm)) == bj) ? e1 : 0u;
+                        rb0 += a0 & 0x00FF00FFu;
+                        g0 += a0 & 0x0000FF00u;
+                        rb1 += a1 & 0x00FF00FFu;
+                        g1 += a1 & 0x0000FF00u;
+                        colb += RR;
+                        if (colb >= ring_end) colb -= kRingCols * RR;
+                    }
+                    auto pack = [](std::uint32_t rb, std::uint32_t g) {
+                        return static_cast<unsigned long long>(rb & 0xFFFFu) |
+                               (static_cast<unsigned long long>(g >> 8) << 21) |
+                               (static_cast<unsigned long long>(rb >> 16) << 42);
+                    };
+                    const unsigned long long v0 = pack(rb0, g0), v1 = pack(rb1, g1);
+                    unsigned long long s0 = v0, s1 = v1;  // inclusive scans over the lanes
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const unsigned long long u0 = __shfl_up_sync(FULL, s0, o);
+                        const unsigned long long u1 = __shfl_up_sync(FULL, s1, o);
+                        if (lane >= o) {
+                            s0 += u0;
+                            s1 += u1;
+                        }
+                    }
+                    // window of lane t = rows [t, t + 2r]: prefix(t + 2r + 1) - prefix(t)
+                    const unsigned long long t0 = __shfl_sync(FULL, s0, 31);
+                    const int jj = lane + w2;
+                    const unsigned long long pa = __shfl_sync(FULL, s0, (jj - 1) & 31);
+                    const unsigned long long pb = __shfl_sync(FULL, s1, (jj - 33) & 31);
+                    const unsigned long long ws = (jj <= 32 ? pa : t0 + pb) - (s0 - v0);
+                    if ((grp >> lane) & 1u) {
+                        sr = static_cast<std::uint32_t>(ws) & 0x1FFFFFu;
+                        sg = static_cast<std::uint32_t>(ws >> 21) & 0x1FFFFFu;
+                        sb = static_cast<std::uint32_t>(ws >> 42);
+                    }
+                    todo &= ~grp;
+                }
+#endif
+                const bool own = __popc(todo) >= OPC_SLIDE_PAR_SUMS;
+                if (own) {
+                    // many lanes with different new winners: each sums its own
+                    // window, in parallel
+                    if ((todo >> lane) & 1u) {
+                        tally(kOpSumPixels, static_cast<unsigned long long>(w2) * w2);
                         std::uint32_t cr = 0, cg = 0, cbb = 0;
                         for (int c = 0; c < w2; ++c) {
                             const std::uint32_t* col = ringp(x + c);
@@ -991,12 +1244,14 @@ __global__ void __launch_bounds__(kWarps * 32)
                         sg = cg;
                         sb = cbb;
                     }
+                    todo = 0u;
                 }
-                for (unsigned todo = __popc(chg) >= OPC_SLIDE_PAR_SUMS ? 0u : chg; todo; todo &= todo - 1) {
+                for (; todo; todo &= todo - 1) {
                     const int j = __ffs(todo) - 1;
                     const int bj = __shfl_sync(FULL, best, j);
                     std::uint32_t cr = 0, cg = 0, cbb = 0;
                     if (lane < w2) {
+                        tally(kOpSumPixels, static_cast<unsigned long long>(w2));
                         const std::uint32_t* col = ringp(x + lane) - lane + j;
 #pragma unroll kUnrollChange
                         for (int k = 0; k < w2; ++k) {
@@ -1018,7 +1273,9 @@ __global__ void __launch_bounds__(kWarps * 32)
                     }
                 }
                 rgb = quotient();
+                SEC_ADD(4, t_s4);
                 }
+                [[maybe_unused]] const long long t_s7 = SEC_NOW();
                 if (row_ok) tally(kOpPixels, 1);
                 {
                     const int xa = xs + x;
@@ -1030,6 +1287,7 @@ __global__ void __launch_bounds__(kWarps * 32)
                 cout += RR;
                 if (cout >= ring_end) cout -= kRingCols * RR;
                 if (cin >= ring_end) cin -= kRingCols * RR;
+                SEC_ADD(7, t_s7);
                 ++x;
             }
         }
@@ -1042,6 +1300,13 @@ __global__ void __launch_bounds__(kWarps * 32)
     if constexpr (TMA_OUT) {
         if (lane == 0) bulk_wait0();
     }
+#if OPC_SLIDE_TRACE
+    if (lane == 0) {
+        for (int k = 0; k < 16; ++k) {
+            if (sec_acc[k]) atomicAdd(g_sec + k, static_cast<unsigned long long>(sec_acc[k]));
+        }
+    }
+#endif
     if constexpr (COUNT) {
 #pragma unroll
         for (int k = 0; k < kOpCountN; ++k) {
@@ -1181,6 +1446,12 @@ cudaError_t launch_slide(const BandArgs& a, int* counter, void* scratch, int num
 }  // namespace opc
 
 #if OPC_SLIDE_TRACE
+extern "C" void opc_debug_slide_sections(unsigned long long* out16) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out16, opc::g_sec, 16 * sizeof(unsigned long long));
+    const unsigned long long zero[16] = {};
+    cudaMemcpyToSymbol(opc::g_sec, zero, sizeof(zero));
+}
 extern "C" int opc_debug_slide_trace(unsigned long long* out, int max) {
     int n = 0;
     cudaDeviceSynchronize();

@@ -88,6 +88,7 @@ def main() -> int:
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--max-w", type=int, default=700)
     ap.add_argument("--max-h", type=int, default=500)
+    ap.add_argument("--only", default="", help="restrict the runs to one kernel family (e.g. slide)")
     args = ap.parse_args()
     rng = np.random.default_rng(args.seed)
     t0 = time.time()
@@ -111,7 +112,12 @@ def main() -> int:
         p = opc.FilterParams(r, L, opc.BorderPolicy(border))
         tag = f"w={w} h={h} r={r} L={L} border={border} content={kind}"
         cases += 1
-        for k in families(r, L):
+        fams = families(r, L)
+        if args.only:
+            fams = [k for k in fams if NAMES[k] == args.only]
+            if not fams:
+                continue
+        for k in fams:
             got = opc.apply_cuda(img, p, opc.CudaConfig(kernel=k, allow_levels_256=allow))
             runs += 1
             per_family[k] += 1
@@ -121,7 +127,7 @@ def main() -> int:
         if h >= 2 and rng.random() < 0.5:
             n = int(rng.integers(2, min(h, 9) + 1))
             out = np.empty_like(img)
-            k = int(rng.choice(families(r, L)))
+            k = int(rng.choice(fams))
             for j in range(n):
                 y0, y1 = opc.band_begin(h, n, j), opc.band_begin(h, n, j + 1)
                 if y1 <= y0:
@@ -136,7 +142,7 @@ def main() -> int:
         if rng.random() < 0.25 and w * h <= 120_000:
             nf = int(rng.integers(2, 6))
             fr = np.stack([np.roll(img, 7 * f, axis=1) for f in range(nf)])
-            k = int(rng.choice(families(r, L)))
+            k = int(rng.choice(fams))
             got = opc.apply_cuda_batch(fr, p, opc.CudaConfig(kernel=k, allow_levels_256=allow))
             batches += 1
             for f in range(nf):

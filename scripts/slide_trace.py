@@ -52,3 +52,13 @@ act = [int(((t0 <= a) & (t1 > a)).sum()) for a in tl[:-1]]
 print("passes in flight at 24 sample times:", act)
 if len(sys.argv) > 1:  # per-pass table for offline cost-model fits
     np.savez_compressed(sys.argv[1], sm=sm, kb=kb, x0=x0, x1=x1, t0=t0, t1=t1)
+if hasattr(LIB, "opc_debug_slide_sections"):
+    sec = (ct.c_ulonglong * 16)()
+    LIB.opc_debug_slide_sections.argtypes = [ct.c_void_p]
+    LIB.opc_debug_slide_sections(sec)
+    names = ["pass start", "step walk", "count updates", "winner resolution", "winner-change sums + quotient",
+             "flat emission", "jumps", "column emit + flush", "phase top"]
+    tot = sum(sec[:9])
+    print("section clocks over 3 launches (lane 0 of every warp), share of the instrumented time:")
+    for i, nm in enumerate(names):
+        print(f"  {nm:32s} {sec[i]/3/1.965e3:10.0f} us warp-time  {sec[i]/max(tot,1):6.1%}")
