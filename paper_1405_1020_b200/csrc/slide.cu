@@ -71,6 +71,9 @@ namespace {
 #ifndef OPC_SLIDE_ROW_SUMS
 #define OPC_SLIDE_ROW_SUMS 1  // winner changes of several lanes to one bin: shared row sums + prefix differences
 #endif
+#ifndef OPC_SLIDE_STRIPED_START
+#define OPC_SLIDE_STRIPED_START 1  // pass starts on horizontal / vertical stripes: 2r + 1 weighted count updates
+#endif
 #ifndef OPC_SLIDE_JUMP
 #define OPC_SLIDE_JUMP 1  // flat stretches of kJumpMin phases or more: no ring loads, the stretch is emitted at once
 #endif
@@ -652,8 +655,6 @@ __global__ void __launch_bounds__(kWarps * 32)
             for (int k = 0; k <= kfirst; ++k) issue(k);
         }
         int kissued = kfirst;
-        for (int k = 0; k <= min(K0, kmax); ++k) wait(k);
-        int kwaited = min(K0, kmax);
 
         // Counts are kept as keys count << kb_ | (G-1 - b mod G), G = 2^kb_ bins,
         // so within a group of G bins the largest key is the lowest-index
@@ -664,21 +665,58 @@ __global__ void __launch_bounds__(kWarps * 32)
             const std::uint32_t v2 = v | (v << 16);
             reinterpret_cast<uint4*>(cnt)[q] = make_uint4(v2, v2, v2, v2);
         }
+        // (the first chunks were requested above: their flight covers the reset)
+        for (int k = 0; k <= min(K0, kmax); ++k) wait(k);
+        int kwaited = min(K0, kmax);
         __syncwarp();
         // Fast path: the first windows of all lanes lie in ring columns
         // [0, 2r] x rows [0, 32 + 2r); when that block is one colour (flat
         // content, config 3) every lane's window is (2r+1)^2 copies of it.
-        const std::uint32_t e0 = *(ringp(0) - lane);
-        bool uni = true;
-        for (int c = 0; c < w2; ++c) {
-            const std::uint32_t* col = ringp(c) - lane;
-            for (int k = lane; k < 32 + 2 * r; k += 32) uni &= col[k] == e0;
+        // Striped starts (an edge through the first windows, no corner): when
+        // every column of the block equals column 0 (horizontal stripes) or
+        // every column is one colour down the block's rows (vertical stripes)
+        // a window is 2r + 1 representative pixels taken 2r + 1 times each.
+        const std::uint32_t* const col0 = ringp(0) - lane;  // row 0 of column 0
+        const std::uint32_t e0 = col0[0];
+        bool uni = true, rows_eq = true, cols_eq = true;
+        {
+            const bool two = lane < 2 * r;
+            const std::uint32_t f0 = col0[lane], f1 = two ? col0[lane + 32] : 0u;
+            const std::uint32_t* cb = col0;
+            for (int c = 0; c < w2; ++c) {
+                const std::uint32_t top = cb[0];
+                const std::uint32_t v0 = cb[lane], v1 = two ? cb[lane + 32] : top;
+                uni &= v0 == e0 && v1 == e0;
+                rows_eq &= v0 == f0 && (!two || v1 == f1);
+                cols_eq &= v0 == top && v1 == top;
+                cb += RR;
+                if (cb >= ring_end) cb -= kRingCols * RR;
+            }
         }
         const bool flat0 = __all_sync(FULL, uni);
+        const int stripes = flat0 || !OPC_SLIDE_STRIPED_START ? 0
+                            : __all_sync(FULL, rows_eq)       ? 1
+                            : __all_sync(FULL, cols_eq)       ? 2
+                                                              : 0;
+        // representative pixel i of a striped start: row lane + i of column 0
+        // (horizontal stripes) or row 0 of column i (vertical stripes)
+        auto stripe_px = [&](const int i) {
+            if (stripes == 1) return col0[lane + i];
+            const std::uint32_t* cb = col0 + i * RR;
+            if (cb >= ring_end) cb -= kRingCols * RR;
+            return cb[0];
+        };
         if (flat0) {
             const int b0 = static_cast<int>(bin_of(e0, bm));
             cnt[b0 * 32 + lane] = static_cast<std::uint16_t>(cnt[b0 * 32 + lane] + w2 * w2 * inc);
             tally(kOpUpdates, 1);
+        } else if (stripes) {
+            tally(kOpUpdates, static_cast<unsigned long long>(w2));
+            std::uint32_t* const cw32 = reinterpret_cast<std::uint32_t*>(cnt) + (lane >> 1);
+            const unsigned add = (static_cast<unsigned>(w2) * inc) << ((lane & 1) * 16);
+#pragma unroll 7
+            for (int i = 0; i < w2; ++i) atomicAdd(cw32 + bin_of(stripe_px(i), bm) * 16, add);
+            __syncwarp();
         } else {
             tally(kOpUpdates, static_cast<unsigned long long>(w2) * w2);
             // (shared-memory atomics on the word holding this lane's u16 count:
@@ -744,6 +782,22 @@ __global__ void __launch_bounds__(kWarps * 32)
             sr = n0 * (e0 & 0xFFu);
             sg = n0 * ((e0 >> 8) & 0xFFu);
             sb = n0 * ((e0 >> 16) & 0xFFu);
+        } else if (stripes) {
+            rescan(best, bc, ub);
+            tally(kOpSumPixels, static_cast<unsigned long long>(w2));
+            sr = sg = sb = 0;
+#pragma unroll 7
+            for (int i = 0; i < w2; ++i) {
+                const std::uint32_t e = stripe_px(i);
+                if (static_cast<int>(bin_of(e, bm)) == best) {
+                    sr += e & 0xFFu;
+                    sg += (e >> 8) & 0xFFu;
+                    sb += (e >> 16) & 0xFFu;
+                }
+            }
+            sr *= static_cast<std::uint32_t>(w2);
+            sg *= static_cast<std::uint32_t>(w2);
+            sb *= static_cast<std::uint32_t>(w2);
         } else {
             rescan(best, bc, ub);
             tally(kOpSumPixels, static_cast<unsigned long long>(w2) * w2);
