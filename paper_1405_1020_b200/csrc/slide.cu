@@ -74,6 +74,9 @@ namespace {
 #ifndef OPC_SLIDE_STRIPED_START
 #define OPC_SLIDE_STRIPED_START 1  // pass starts on horizontal / vertical stripes: 2r + 1 weighted count updates
 #endif
+#ifndef OPC_SLIDE_COST_COLS
+#define OPC_SLIDE_COST_COLS 32  // columns per unit of the work plan (32, 16 or 8; A/B on C3: 137 / 138 / 142 us -- finer chunks start more passes inside busy regions)
+#endif
 #ifndef OPC_SLIDE_JUMP
 #define OPC_SLIDE_JUMP 1  // flat stretches of kJumpMin phases or more: no ring loads, the stretch is emitted at once
 #endif
@@ -119,6 +122,8 @@ constexpr int kUnrollSums = OPC_SLIDE_UNROLL_SUMS;
 constexpr int kUnrollChange = OPC_SLIDE_UNROLL_CHANGE;
 constexpr int kUnrollUpdate = OPC_SLIDE_UNROLL_UPDATE;
 constexpr int kJumpMin = OPC_SLIDE_JUMP_MIN;
+constexpr int kCostCols = OPC_SLIDE_COST_COLS;
+static_assert(kCostCols == 32 || kCostCols == 16 || kCostCols == 8, "cost blocks divide the 32-column nonflat words");
 constexpr int kStageCols = 16;   // output columns staged per flush (== kChunk)
 constexpr int kStageStride = 17;
 constexpr int kRecipBytes = 1024 * 4;
@@ -156,13 +161,14 @@ struct TGeom {
     int ncols;    // plane columns: W + 64
     int ntr;      // 32-row tiles per column: Hs / 32
     int nbands;   // 32-row bands of the launch
-    int nblk;     // 32-column blocks per band: ceil((x_hi - x_lo) / 32)
+    int nblk;     // 32-column blocks (nonflat words) per band: ceil((x_hi - x_lo) / 32)
+    int ncb;      // cost blocks (the plan's units, kCostCols columns) per band: nblk * 32 / kCostCols
     int nch;      // chunks of the cost-balanced split
     std::uint32_t* dmask;  // [frame][ntr][ncols]: bit y of (tile, column c) = plane rows
                            // 32 tile + y of columns c and c - (2r + 1) differ
     std::uint32_t* nf;     // [frame][nband][nblk]: bit x = step at interior column
                            // 32 blk + x changes the window (not flat)
-    std::uint32_t* bc;     // [frame][nband][nblk]: cost of the block's columns
+    std::uint32_t* bc;     // [frame][nband][ncb]: cost of the cost block's columns
     int* cs;               // [nch + 1]: first block of each chunk
     int* perm;             // [frames x nbands]: the plan's band order (position -> band), costliest first
     // Decreasing chunk sizes (OPC_SLIDE_PLAN_K > 0): chunk j covers the cost
@@ -187,7 +193,9 @@ __host__ inline TGeom tgeom(const BandArgs& a, void* scratch = nullptr, long lon
     g.ntr = g.Hs / 32;
     g.frame_elems = static_cast<std::size_t>(g.ncols) * g.Hs;
     g.nblk = (a.x_hi - a.x_lo + 31) / 32;
-    const long long blocks = static_cast<long long>(a.frames) * g.nbands * g.nblk;
+    g.ncb = g.nblk * (32 / kCostCols);
+    const long long words = static_cast<long long>(a.frames) * g.nbands * g.nblk;
+    const long long blocks = static_cast<long long>(a.frames) * g.nbands * g.ncb;
     g.nch = plan_chunks(blocks, resident);
     if (OPC_SLIDE_PLAN_K > 0 && resident > 0) {
         const double R = static_cast<double>(resident), K = OPC_SLIDE_PLAN_K, M = OPC_SLIDE_PLAN_M;
@@ -210,7 +218,7 @@ __host__ inline TGeom tgeom(const BandArgs& a, void* scratch = nullptr, long lon
         g.dmask = p;
         p += static_cast<std::size_t>(a.frames) * g.ntr * g.ncols;
         g.nf = p;
-        p += blocks;
+        p += words;
         g.bc = p;
         p += blocks;
         g.cs = reinterpret_cast<int*>(p);
@@ -221,10 +229,11 @@ __host__ inline TGeom tgeom(const BandArgs& a, void* scratch = nullptr, long lon
 
 __host__ inline std::size_t tgeom_bytes(const BandArgs& a) {
     const TGeom g = tgeom(a);
-    const long long blocks = static_cast<long long>(a.frames) * g.nbands * g.nblk;
+    const long long words = static_cast<long long>(a.frames) * g.nbands * g.nblk;
+    const long long blocks = static_cast<long long>(a.frames) * g.nbands * g.ncb;
     // plan_chunks never exceeds the block count (+1 for the end marker)
     return (g.frame_elems * a.frames + static_cast<std::size_t>(a.frames) * g.ntr * g.ncols +
-            2 * static_cast<std::size_t>(blocks) + static_cast<std::size_t>(blocks) + 2 +
+            static_cast<std::size_t>(words) + 2 * static_cast<std::size_t>(blocks) + 2 +
             static_cast<std::size_t>(a.frames) * g.nbands) *
            sizeof(std::uint32_t);
 }
@@ -363,9 +372,15 @@ __global__ void __launch_bounds__(kPlanThreads) slide_plan_kernel(BandArgs a, TG
             const int j = kCostBlocksPerWarp * q + i;
             const std::uint32_t word = __ballot_sync(0xFFFFFFFFu, m[i] != 0u);
             if (lane == 0 && j < g.nblk) {
-                const std::size_t o = static_cast<std::size_t>(band) * g.nblk + j;
-                g.nf[o] = word;
-                g.bc[o] = static_cast<std::uint32_t>(min(32, iw - 32 * j)) + OPC_SLIDE_COST_K * __popc(word);
+                g.nf[static_cast<std::size_t>(band) * g.nblk + j] = word;
+                constexpr int per = 32 / kCostCols;
+#pragma unroll
+                for (int sb = 0; sb < per; ++sb) {
+                    const int cols = max(0, min(kCostCols, iw - 32 * j - kCostCols * sb));
+                    const std::uint32_t bits = (word >> (kCostCols * sb)) & (0xFFFFFFFFu >> (32 - kCostCols));
+                    g.bc[static_cast<std::size_t>(band) * g.ncb + per * j + sb] =
+                        static_cast<std::uint32_t>(cols) + OPC_SLIDE_COST_K * __popc(bits);
+                }
             }
         }
     }
@@ -400,7 +415,7 @@ __global__ void __launch_bounds__(kPlanThreads) slide_plan_kernel(BandArgs a, TG
     if (ordered) {
         if (t < nb) {
             std::uint32_t c = 0;
-            for (int j = 0; j < g.nblk; ++j) c += __ldcg(g.bc + static_cast<long long>(t) * g.nblk + j);
+            for (int j = 0; j < g.ncb; ++j) c += __ldcg(g.bc + static_cast<long long>(t) * g.ncb + j);
             band_cost[t] = c;
         }
         __syncthreads();
@@ -421,8 +436,8 @@ __global__ void __launch_bounds__(kPlanThreads) slide_plan_kernel(BandArgs a, TG
     // block at position i of the plan's order
     auto block_at = [&](long long i) -> long long {
         if (!ordered) return i;
-        const long long pos = i / g.nblk;
-        return static_cast<long long>(band_at[pos]) * g.nblk + (i - pos * g.nblk);
+        const long long pos = i / g.ncb;
+        return static_cast<long long>(band_at[pos]) * g.ncb + (i - pos * g.ncb);
     };
     const bool staged = nblocks <= smem_cap;
     if (staged) {
@@ -526,7 +541,10 @@ __device__ int g_trace_n;
 // 7 single-column emit + flush, 8 phase top (ring waits / requests).
 __device__ unsigned long long g_sec[16];
 #define SEC_T0() const long long sec_t0_ = clock64()
-#define SEC_ADD(i, t0) do { if (lane == 0) sec_acc[i] += clock64() - (t0); } while (0)
+#ifndef OPC_TRACE_MAXW
+#define OPC_TRACE_MAXW (1 << 30)  // section clocks only in passes at most this wide
+#endif
+#define SEC_ADD(i, t0) do { if (lane == 0 && sec_on) sec_acc[i] += clock64() - (t0); } while (0)
 #define SEC_NOW() clock64()
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
@@ -546,6 +564,7 @@ __global__ void __launch_bounds__(kWarps * 32)
                  const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout) {
     unsigned long long opc_n[kOpCountN] = {};
     [[maybe_unused]] long long sec_acc[16] = {};
+    [[maybe_unused]] bool sec_on = true;
     auto tally = [&](int k, unsigned long long v) {
         if constexpr (COUNT) opc_n[k] += v;
     };
@@ -600,6 +619,8 @@ __global__ void __launch_bounds__(kWarps * 32)
             kb = band - f * tg.nbands;
         }
 #if OPC_SLIDE_TRACE
+        sec_on = x1 - x0 <= OPC_TRACE_MAXW;
+        if (lane == 0 && sec_on) sec_acc[9] += 1;
         int pass_cols = x1 - x0;
         const unsigned long long t_start = gtime();
         struct TraceGuard {
@@ -1458,7 +1479,7 @@ cudaError_t launch_slide(const BandArgs& a, int* counter, void* scratch, int num
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
-    const long long nblocks = static_cast<long long>(a.frames) * tg.nbands * tg.nblk;
+    const long long nblocks = static_cast<long long>(a.frames) * tg.nbands * tg.ncb;  // cost blocks
     {
         const long long nq = (tg.nblk + kCostBlocksPerWarp - 1) / kCostBlocksPerWarp;
         const long long nwarps = static_cast<long long>(a.frames) * tg.nbands * nq;
@@ -1478,7 +1499,7 @@ cudaError_t launch_slide(const BandArgs& a, int* counter, void* scratch, int num
     timing_mark(kIdPrePass, 1, s);
     const WorkSplit g =
         OPC_SLIDE_PLAN
-            ? make_planned_split(a.frames, tg.nbands, a.x_hi - a.x_lo, tg.nblk, 32, tg.nch, tg.cs)
+            ? make_planned_split(a.frames, tg.nbands, a.x_hi - a.x_lo, tg.ncb, kCostCols, tg.nch, tg.cs)
             : make_split(a.frames, tg.nbands, a.x_hi - a.x_lo, resident, OPC_SLIDE_STATIC_PCT,
                          OPC_SLIDE_MIN_CHUNK, OPC_SLIDE_DYN_PER_WARP, OPC_SLIDE_GUIDED_K);
     long long blocks = (g.nchunks + warps - 1) / warps;

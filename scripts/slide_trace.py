@@ -58,7 +58,7 @@ if hasattr(LIB, "opc_debug_slide_sections"):
     LIB.opc_debug_slide_sections(sec)
     names = ["pass start", "step walk", "count updates", "winner resolution", "winner-change sums + quotient",
              "flat emission", "jumps", "column emit + flush", "phase top"]
-    tot = sum(sec[:9])
+    tot = sum(sec[:9]); print("passes with section clocks:", sec[9] / 3)
     print("section clocks over 3 launches (lane 0 of every warp), share of the instrumented time:")
     for i, nm in enumerate(names):
         print(f"  {nm:32s} {sec[i]/3/1.965e3:10.0f} us warp-time  {sec[i]/max(tot,1):6.1%}")
