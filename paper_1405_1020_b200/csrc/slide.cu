@@ -413,10 +413,13 @@ __global__ void __launch_bounds__(kPlanThreads) slide_plan_kernel(BandArgs a, TG
     __shared__ int band_at[kPlanThreads];  // position -> band
     const bool ordered = OPC_SLIDE_BAND_ORDER && nb <= kPlanThreads;
     if (ordered) {
-        if (t < nb) {
+        // (a warp per band: coalesced loads of its block costs, one reduction)
+        for (int b = t >> 5; b < nb; b += kPlanThreads / 32) {
             std::uint32_t c = 0;
-            for (int j = 0; j < g.ncb; ++j) c += __ldcg(g.bc + static_cast<long long>(t) * g.ncb + j);
-            band_cost[t] = c;
+#pragma unroll 4
+            for (int j = lane; j < g.ncb; j += 32) c += __ldcg(g.bc + static_cast<long long>(b) * g.ncb + j);
+            c = __reduce_add_sync(0xFFFFFFFFu, c);
+            if (lane == 0) band_cost[b] = c;
         }
         __syncthreads();
         if (t < nb) {
@@ -436,19 +439,37 @@ __global__ void __launch_bounds__(kPlanThreads) slide_plan_kernel(BandArgs a, TG
     // block at position i of the plan's order
     auto block_at = [&](long long i) -> long long {
         if (!ordered) return i;
-        const long long pos = i / g.ncb;
-        return static_cast<long long>(band_at[pos]) * g.ncb + (i - pos * g.ncb);
+        // (block indices fit 32 bits: the chunk starts are ints)
+        const unsigned ii = static_cast<unsigned>(i), ncb = static_cast<unsigned>(g.ncb);
+        const unsigned pos = ii / ncb;
+        return static_cast<long long>(band_at[pos]) * g.ncb + (ii - pos * ncb);
     };
+    PLAN_TICK(4);
     const bool staged = nblocks <= smem_cap;
     if (staged) {
         // (padded: entry b at b + b / 16, so 16 consecutive blocks per lane
         // read conflict-free)
-        for (long long i = t; i < nblocks; i += kPlanThreads) sbc[i + (i >> 4)] = __ldcg(g.bc + block_at(i));
+        // (batches of 8 loads in flight: one L2 round trip per batch, not per entry)
+        for (long long i0 = t; i0 < nblocks; i0 += 8 * kPlanThreads) {
+            std::uint32_t v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const long long i = i0 + static_cast<long long>(k) * kPlanThreads;
+                v[k] = i < nblocks ? __ldcg(g.bc + block_at(i)) : 0u;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const long long i = i0 + static_cast<long long>(k) * kPlanThreads;
+                if (i < nblocks) sbc[i + (i >> 4)] = v[k];
+            }
+        }
     }
     for (int i = t; i <= g.nch; i += kPlanThreads) g.cs[i] = static_cast<int>(nblocks);
     __syncthreads();
     PLAN_TICK(1);
-    auto cost = [&](long long b) -> std::uint32_t {
+    // (32-bit block indices from here on: the chunk starts are ints)
+    const int nbl = static_cast<int>(nblocks);
+    auto cost = [&](int b) -> std::uint32_t {
         return staged ? sbc[b + (b >> 4)] : __ldcg(g.bc + block_at(b));
     };
     // Thread t owns a contiguous run of blocks [t * per, (t + 1) * per): the
@@ -459,10 +480,10 @@ __global__ void __launch_bounds__(kPlanThreads) slide_plan_kernel(BandArgs a, TG
     // monotone map gives a valid partition.
     __shared__ std::uint32_t wsum[32];
     const int w = t >> 5;
-    const long long per = (nblocks + kPlanThreads - 1) / kPlanThreads;
-    const long long b0 = min(nblocks, per * t), b1 = min(nblocks, b0 + per);
+    const int per = (nbl + kPlanThreads - 1) / kPlanThreads;
+    const int b0 = min(nbl, per * t), b1 = min(nbl, b0 + per);
     std::uint32_t mine = 0;
-    for (long long b = b0; b < b1; ++b) mine += cost(b);
+    for (int b = b0; b < b1; ++b) mine += cost(b);
     std::uint32_t incl = mine;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -489,27 +510,30 @@ __global__ void __launch_bounds__(kPlanThreads) slide_plan_kernel(BandArgs a, TG
     if (total == 0) return;
     const float scale = static_cast<float>(g.nch) / static_cast<float>(total);
     const float inv_total = 1.0f / static_cast<float>(total);
+    const float inv_lnq = g.lnq != 0.0f ? 1.0f / g.lnq : 0.0f;
     auto chunk_of = [&](std::uint32_t e) {
         if (g.lnq == 0.0f) return static_cast<int>(static_cast<float>(e) * scale);
         const float x = static_cast<float>(e) * inv_total;  // cost fraction before the block
-        const int j = x < g.xJ ? static_cast<int>(log1pf(-x) / g.lnq)
+        // (fast logarithm: the walk below keeps the map monotone)
+        const int j = x < g.xJ ? static_cast<int>(__logf(1.0f - x) * inv_lnq)
                                : g.J + static_cast<int>((x - g.xJ) * g.rm);
         return min(j, g.nch - 1);
     };
     std::uint32_t e_b = wsum[w] + incl - mine;  // cost before b0
     int prev = b0 == 0 ? -1 : chunk_of(e_b - cost(b0 - 1));
-    for (long long b = b0; b < b1; ++b) {
+    for (int b = b0; b < b1; ++b) {
         // block b belongs to chunk(E_b), E_b = cost before b; the chunks
         // starting at b are (chunk(E_{b-1}), chunk(E_b)]
-        const int cur = chunk_of(e_b);
-        for (int i = prev + 1; i <= cur && i < g.nch; ++i) g.cs[i] = static_cast<int>(b);
+        const int cur = max(prev, chunk_of(e_b));
+        for (int i = prev + 1; i <= cur && i < g.nch; ++i) g.cs[i] = b;
         prev = cur;
         e_b += cost(b);
     }
     PLAN_TICK(3);
 #if OPC_PLAN_CLOCK
     if (t == 0) {
-        printf("plan clocks: stage %lld sums %lld walk %lld\n", ck[1] - ck[0], ck[2] - ck[1], ck[3] - ck[2]);
+        printf("plan clocks: band order %lld stage %lld sums %lld walk %lld (start %lld)\n", ck[4] - ck[0], ck[1] - ck[4],
+               ck[2] - ck[1], ck[3] - ck[2], ck[0]);
     }
 #endif
 }
