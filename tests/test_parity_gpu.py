@@ -169,6 +169,41 @@ def test_slide_rectangles_and_ties(gpu, L):
         assert np.array_equal(run(gpu, two, r, L, 1, SLIDE, L == 256), want), r
 
 
+@pytest.mark.parametrize("content", ["h_stripes", "v_stripes", "sparse_edges", "thin_stripes", "corners"])
+def test_slide_structured_content(gpu, content):
+    """The content-dependent paths of the slide family: striped pass starts
+    (every column equal / every column one colour), long flat stretches jumped
+    without ring loads, steps whose rows form one, two or many runs of a bin
+    pair, winner changes of many lanes to one bin (shared row sums)."""
+    rng = np.random.default_rng(len(content))
+    h, w = 150, 1300
+    img = np.empty((h, w, 3), np.uint8)
+    img[:] = rng.integers(0, 256, 3, dtype=np.uint8)
+    if content == "h_stripes":
+        for y in range(0, h, 23):
+            img[y:y + int(rng.integers(1, 12))] = rng.integers(0, 256, 3, dtype=np.uint8)
+    elif content == "v_stripes":
+        for x in range(0, w, 57):
+            img[:, x:x + int(rng.integers(1, 30))] = rng.integers(0, 256, 3, dtype=np.uint8)
+    elif content == "sparse_edges":  # a few edges, hundreds of flat columns between them
+        for x in (5, 400, 401, 1000, 1290):
+            img[:, x:] = rng.integers(0, 256, 3, dtype=np.uint8)
+        img[70:, 600:900] = rng.integers(0, 256, 3, dtype=np.uint8)
+    elif content == "thin_stripes":  # many runs inside every window
+        for y in range(0, h, 3):
+            img[y, 200:700] = rng.integers(0, 256, 3, dtype=np.uint8)
+        for x in range(800, 1100, 2):
+            img[:, x] = rng.integers(0, 256, 3, dtype=np.uint8)
+    else:  # corners: small rectangles, several per band
+        for _ in range(120):
+            y0, x0 = int(rng.integers(0, h - 4)), int(rng.integers(0, w - 4))
+            img[y0:y0 + int(rng.integers(2, 40)), x0:x0 + int(rng.integers(2, 60))] = \
+                rng.integers(0, 256, 3, dtype=np.uint8)
+    for r, L in ((10, 256), (8, 255), (15, 40), (3, 100)):
+        want = oracle_lib.oracle_filter(img, r, L, 0, threads=4)
+        assert np.array_equal(run(gpu, img, r, L, 0, SLIDE, L == 256), want), (content, r, L)
+
+
 @pytest.mark.parametrize("content", ["flat", "smooth", "two_tone", "white"])
 def test_skew_tie_heavy_content(gpu, content):
     """Smooth / flat content: single-bin windows, many exact ties, bin L (white)."""
