@@ -204,6 +204,21 @@ def test_slide_structured_content(gpu, content):
         assert np.array_equal(run(gpu, img, r, L, 0, SLIDE, L == 256), want), (content, r, L)
 
 
+def test_slide_more_bands_than_the_plan_orders(gpu):
+    """The work plan orders up to 1024 bands by cost; a taller launch keeps
+    the natural order (identity permutation)."""
+    rng = np.random.default_rng(5)
+    h, w = 33000, 48  # 1031 bands of 32 rows
+    img = np.empty((h, w, 3), np.uint8)
+    img[:] = rng.integers(0, 256, 3, dtype=np.uint8)
+    for _ in range(300):
+        y0, x0 = int(rng.integers(0, h - 4)), int(rng.integers(0, w - 4))
+        img[y0:y0 + int(rng.integers(2, 400)), x0:x0 + int(rng.integers(2, 30))] = \
+            rng.integers(0, 256, 3, dtype=np.uint8)
+    want = oracle_lib.oracle_filter(img, 3, 100, 0, threads=8)
+    assert np.array_equal(run(gpu, img, 3, 100, 0, SLIDE), want)
+
+
 @pytest.mark.parametrize("content", ["flat", "smooth", "two_tone", "white"])
 def test_skew_tie_heavy_content(gpu, content):
     """Smooth / flat content: single-bin windows, many exact ties, bin L (white)."""
