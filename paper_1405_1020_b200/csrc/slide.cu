@@ -763,15 +763,38 @@ __global__ void __launch_bounds__(kWarps * 32)
             for (int i = 0; i < w2; ++i) atomicAdd(cw32 + bin_of(stripe_px(i), bm) * 16, add);
             __syncwarp();
         } else {
-            tally(kOpUpdates, static_cast<unsigned long long>(w2) * w2);
             // (shared-memory atomics on the word holding this lane's u16 count:
             // no read-modify-write chain through the counts)
+            // A column whose rows form at most two runs of one bin in every
+            // lane's window (an edge or a corner in the block) is two weighted
+            // updates; other columns update row by row.
             std::uint32_t* const cw32 = reinterpret_cast<std::uint32_t*>(cnt) + (lane >> 1);
             const unsigned add = inc << ((lane & 1) * 16);
+            const std::uint32_t* col = ringp(0);
             for (int c = 0; c < w2; ++c) {
-                const std::uint32_t* col = ringp(c);
+                const std::uint32_t bfirst = bin_of(col[0], bm);
+                std::uint32_t bprev = bfirst;
+                int ncp = 0, split = 0;
+#pragma unroll 5
+                for (int k = 1; k < w2; ++k) {
+                    const std::uint32_t b = bin_of(col[k], bm);
+                    const bool cp = b != bprev;
+                    ncp += cp ? 1 : 0;
+                    split = cp ? k : split;
+                    bprev = b;
+                }
+                if (__all_sync(FULL, ncp <= 1)) {
+                    const unsigned n1 = static_cast<unsigned>(ncp ? split : w2);
+                    tally(kOpUpdates, ncp ? 2 : 1);
+                    atomicAdd(cw32 + bfirst * 16, n1 * add);
+                    if (__any_sync(FULL, ncp != 0)) atomicAdd(cw32 + bprev * 16, (static_cast<unsigned>(w2) - n1) * add);
+                } else {
+                    tally(kOpUpdates, static_cast<unsigned long long>(w2));
 #pragma unroll 7
-                for (int k = 0; k < w2; ++k) atomicAdd(cw32 + bin_of(col[k], bm) * 16, add);
+                    for (int k = 0; k < w2; ++k) atomicAdd(cw32 + bin_of(col[k], bm) * 16, add);
+                }
+                col += RR;
+                if (col >= ring_end + lane) col -= kRingCols * RR;
             }
             __syncwarp();
         }
@@ -819,6 +842,120 @@ __global__ void __launch_bounds__(kWarps * 32)
         };
         int best, bc, ub;  // winner, its count, an upper bound of every other bin's count
         std::uint32_t sr, sg, sb;
+        // The window sums (sr, sg, sb) of the lanes in `todo`, each for its own
+        // bin `best`, the windows at pass column xw (ring columns xw .. xw + 2r).
+        auto resum = [&](const int xw, unsigned todo) {
+#if OPC_SLIDE_ROW_SUMS
+        // Several lanes with one new winner (an edge crossing the
+        // band): their windows are rows t .. t + 2r of the same 2r + 1
+        // columns, so the warp sums that bin once per ring row (lane t:
+        // rows t and 32 + t) and every lane takes the difference of
+        // two prefix sums over the rows -- 2(2r + 1) loads per lane
+        // instead of (2r + 1)^2.  R, G, B travel as 21-bit fields of
+        // one 64-bit word (a prefix is at most 62 rows x 31 x 255).
+        while (__popc(todo) >= OPC_SLIDE_PAR_SUMS) {
+            const int bj = __shfl_sync(FULL, best, __ffs(todo) - 1);
+            const unsigned grp = __ballot_sync(FULL, ((todo >> lane) & 1u) != 0u && best == bj);
+            if (2 * __popc(grp) < __popc(todo)) break;  // many winners: own windows, below
+            std::uint32_t rb0 = 0, g0 = 0, rb1 = 0, g1 = 0;
+            const std::uint32_t* colb = ringp(xw) - lane;  // row 0 of column x
+            const bool two = lane < 2 * r;
+            tally(kOpSumPixels, static_cast<unsigned long long>(two ? 2 * w2 : w2));
+#pragma unroll 3
+            for (int c = 0; c < w2; ++c) {
+                const std::uint32_t e0 = colb[lane];
+                const std::uint32_t e1 = two ? colb[lane + 32] : 0u;
+                const std::uint32_t a0 = static_cast<int>(bin_of(e0, bm)) == bj ? e0 : 0u;
+                const std::uint32_t a1 = (two && static_cast<int>(bin_of(e1, bm)) == bj) ? e1 : 0u;
+                rb0 += a0 & 0x00FF00FFu;
+                g0 += a0 & 0x0000FF00u;
+                rb1 += a1 & 0x00FF00FFu;
+                g1 += a1 & 0x0000FF00u;
+                colb += RR;
+                if (colb >= ring_end) colb -= kRingCols * RR;
+            }
+            auto pack = [](std::uint32_t rb, std::uint32_t g) {
+                return static_cast<unsigned long long>(rb & 0xFFFFu) |
+                       (static_cast<unsigned long long>(g >> 8) << 21) |
+                       (static_cast<unsigned long long>(rb >> 16) << 42);
+            };
+            const unsigned long long v0 = pack(rb0, g0), v1 = pack(rb1, g1);
+            unsigned long long s0 = v0, s1 = v1;  // inclusive scans over the lanes
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long u0 = __shfl_up_sync(FULL, s0, o);
+                const unsigned long long u1 = __shfl_up_sync(FULL, s1, o);
+                if (lane >= o) {
+                    s0 += u0;
+                    s1 += u1;
+                }
+            }
+            // window of lane t = rows [t, t + 2r]: prefix(t + 2r + 1) - prefix(t)
+            const unsigned long long t0 = __shfl_sync(FULL, s0, 31);
+            const int jj = lane + w2;
+            const unsigned long long pa = __shfl_sync(FULL, s0, (jj - 1) & 31);
+            const unsigned long long pb = __shfl_sync(FULL, s1, (jj - 33) & 31);
+            const unsigned long long ws = (jj <= 32 ? pa : t0 + pb) - (s0 - v0);
+            if ((grp >> lane) & 1u) {
+                sr = static_cast<std::uint32_t>(ws) & 0x1FFFFFu;
+                sg = static_cast<std::uint32_t>(ws >> 21) & 0x1FFFFFu;
+                sb = static_cast<std::uint32_t>(ws >> 42);
+            }
+            todo &= ~grp;
+        }
+#endif
+        const bool own = __popc(todo) >= OPC_SLIDE_PAR_SUMS;
+        if (own) {
+            // many lanes with different new winners: each sums its own
+            // window, in parallel
+            if ((todo >> lane) & 1u) {
+                tally(kOpSumPixels, static_cast<unsigned long long>(w2) * w2);
+                std::uint32_t cr = 0, cg = 0, cbb = 0;
+                for (int c = 0; c < w2; ++c) {
+                    const std::uint32_t* col = ringp(xw + c);
+#pragma unroll kUnrollSums
+                    for (int k = 0; k < w2; ++k) {
+                        const std::uint32_t e = col[k];
+                        if (static_cast<int>(bin_of(e, bm)) == best) {
+                            cr += e & 0xFFu;
+                            cg += (e >> 8) & 0xFFu;
+                            cbb += (e >> 16) & 0xFFu;
+                        }
+                    }
+                }
+                sr = cr;
+                sg = cg;
+                sb = cbb;
+            }
+            todo = 0u;
+        }
+        for (; todo; todo &= todo - 1) {
+            const int j = __ffs(todo) - 1;
+            const int bj = __shfl_sync(FULL, best, j);
+            std::uint32_t cr = 0, cg = 0, cbb = 0;
+            if (lane < w2) {
+                tally(kOpSumPixels, static_cast<unsigned long long>(w2));
+                const std::uint32_t* col = ringp(xw + lane) - lane + j;
+#pragma unroll kUnrollChange
+                for (int k = 0; k < w2; ++k) {
+                    const std::uint32_t e = col[k];
+                    if (static_cast<int>(bin_of(e, bm)) == bj) {
+                        cr += e & 0xFFu;
+                        cg += (e >> 8) & 0xFFu;
+                        cbb += (e >> 16) & 0xFFu;
+                    }
+                }
+            }
+            cr = __reduce_add_sync(FULL, cr);
+            cg = __reduce_add_sync(FULL, cg);
+            cbb = __reduce_add_sync(FULL, cbb);
+            if (lane == j) {
+                sr = cr;
+                sg = cg;
+                sb = cbb;
+            }
+        }
+        };
         if (flat0) {
             const std::uint32_t n0 = static_cast<std::uint32_t>(w2 * w2);
             best = static_cast<int>(bin_of(e0, bm));
@@ -845,20 +982,8 @@ __global__ void __launch_bounds__(kWarps * 32)
             sb *= static_cast<std::uint32_t>(w2);
         } else {
             rescan(best, bc, ub);
-            tally(kOpSumPixels, static_cast<unsigned long long>(w2) * w2);
             sr = sg = sb = 0;
-            for (int c = 0; c < w2; ++c) {
-                const std::uint32_t* col = ringp(c);
-#pragma unroll kUnrollSums
-                for (int k = 0; k < w2; ++k) {
-                    const std::uint32_t e = col[k];
-                    if (static_cast<int>(bin_of(e, bm)) == best) {
-                        sr += e & 0xFFu;
-                        sg += (e >> 8) & 0xFFu;
-                        sb += (e >> 16) & 0xFFu;
-                    }
-                }
-            }
+            resum(0, FULL);
         }
         // the output of the current window (recomputed only after a step
         // that changed the window: a flat step repeats the previous pixel)
@@ -1260,117 +1385,7 @@ __global__ void __launch_bounds__(kWarps * 32)
                 SEC_ADD(3, t_s3);
                 [[maybe_unused]] const long long t_s4 = SEC_NOW();
                 const unsigned chg = __ballot_sync(FULL, changed);
-                unsigned todo = chg;
-#if OPC_SLIDE_ROW_SUMS
-                // Several lanes with one new winner (an edge crossing the
-                // band): their windows are rows t .. t + 2r of the same 2r + 1
-                // columns, so the warp sums that bin once per ring row (lane t:
-                // rows t and 32 + t) and every lane takes the difference of
-                // two prefix sums over the rows -- 2(2r + 1) loads per lane
-                // instead of (2r + 1)^2.  R, G, B travel as 21-bit fields of
-                // one 64-bit word (a prefix is at most 62 rows x 31 x 255).
-                while (__popc(todo) >= OPC_SLIDE_PAR_SUMS) {
-                    const int bj = __shfl_sync(FULL, best, __ffs(todo) - 1);
-                    const unsigned grp = __ballot_sync(FULL, ((todo >> lane) & 1u) != 0u && best == bj);
-                    if (2 * __popc(grp) < __popc(todo)) break;  // many winners: own windows, below
-                    std::uint32_t rb0 = 0, g0 = 0, rb1 = 0, g1 = 0;
-                    const std::uint32_t* colb = ringp(x) - lane;  // row 0 of column x
-                    const bool two = lane < 2 * r;
-                    tally(kOpSumPixels, static_cast<unsigned long long>(two ? 2 * w2 : w2));
-#pragma unroll 3
-                    for (int c = 0; c < w2; ++c) {
-                        const std::uint32_t e0 = colb[lane];
-                        const std::uint32_t e1 = two ? colb[lane + 32] : 0u;
-                        const std::uint32_t a0 = static_cast<int>(bin_of(e0, bm)) == bj ? e0 : 0u;
-                        const std::uint32_t a1 = (two && static_cast<int>(bin_of(e1, bm)) == bj) ? e1 : 0u;
-                        rb0 += a0 & 0x00FF00FFu;
-                        g0 += a0 & 0x0000FF00u;
-                        rb1 += a1 & 0x00FF00FFu;
-                        g1 += a1 & 0x0000FF00u;
-                        colb += RR;
-                        if (colb >= ring_end) colb -= kRingCols * RR;
-                    }
-                    auto pack = [](std::uint32_t rb, std::uint32_t g) {
-                        return static_cast<unsigned long long>(rb & 0xFFFFu) |
-                               (static_cast<unsigned long long>(g >> 8) << 21) |
-                               (static_cast<unsigned long long>(rb >> 16) << 42);
-                    };
-                    const unsigned long long v0 = pack(rb0, g0), v1 = pack(rb1, g1);
-                    unsigned long long s0 = v0, s1 = v1;  // inclusive scans over the lanes
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const unsigned long long u0 = __shfl_up_sync(FULL, s0, o);
-                        const unsigned long long u1 = __shfl_up_sync(FULL, s1, o);
-                        if (lane >= o) {
-                            s0 += u0;
-                            s1 += u1;
-                        }
-                    }
-                    // window of lane t = rows [t, t + 2r]: prefix(t + 2r + 1) - prefix(t)
-                    const unsigned long long t0 = __shfl_sync(FULL, s0, 31);
-                    const int jj = lane + w2;
-                    const unsigned long long pa = __shfl_sync(FULL, s0, (jj - 1) & 31);
-                    const unsigned long long pb = __shfl_sync(FULL, s1, (jj - 33) & 31);
-                    const unsigned long long ws = (jj <= 32 ? pa : t0 + pb) - (s0 - v0);
-                    if ((grp >> lane) & 1u) {
-                        sr = static_cast<std::uint32_t>(ws) & 0x1FFFFFu;
-                        sg = static_cast<std::uint32_t>(ws >> 21) & 0x1FFFFFu;
-                        sb = static_cast<std::uint32_t>(ws >> 42);
-                    }
-                    todo &= ~grp;
-                }
-#endif
-                const bool own = __popc(todo) >= OPC_SLIDE_PAR_SUMS;
-                if (own) {
-                    // many lanes with different new winners: each sums its own
-                    // window, in parallel
-                    if ((todo >> lane) & 1u) {
-                        tally(kOpSumPixels, static_cast<unsigned long long>(w2) * w2);
-                        std::uint32_t cr = 0, cg = 0, cbb = 0;
-                        for (int c = 0; c < w2; ++c) {
-                            const std::uint32_t* col = ringp(x + c);
-#pragma unroll kUnrollSums
-                            for (int k = 0; k < w2; ++k) {
-                                const std::uint32_t e = col[k];
-                                if (static_cast<int>(bin_of(e, bm)) == best) {
-                                    cr += e & 0xFFu;
-                                    cg += (e >> 8) & 0xFFu;
-                                    cbb += (e >> 16) & 0xFFu;
-                                }
-                            }
-                        }
-                        sr = cr;
-                        sg = cg;
-                        sb = cbb;
-                    }
-                    todo = 0u;
-                }
-                for (; todo; todo &= todo - 1) {
-                    const int j = __ffs(todo) - 1;
-                    const int bj = __shfl_sync(FULL, best, j);
-                    std::uint32_t cr = 0, cg = 0, cbb = 0;
-                    if (lane < w2) {
-                        tally(kOpSumPixels, static_cast<unsigned long long>(w2));
-                        const std::uint32_t* col = ringp(x + lane) - lane + j;
-#pragma unroll kUnrollChange
-                        for (int k = 0; k < w2; ++k) {
-                            const std::uint32_t e = col[k];
-                            if (static_cast<int>(bin_of(e, bm)) == bj) {
-                                cr += e & 0xFFu;
-                                cg += (e >> 8) & 0xFFu;
-                                cbb += (e >> 16) & 0xFFu;
-                            }
-                        }
-                    }
-                    cr = __reduce_add_sync(FULL, cr);
-                    cg = __reduce_add_sync(FULL, cg);
-                    cbb = __reduce_add_sync(FULL, cbb);
-                    if (lane == j) {
-                        sr = cr;
-                        sg = cg;
-                        sb = cbb;
-                    }
-                }
+                resum(x, chg);
                 rgb = quotient();
                 SEC_ADD(4, t_s4);
                 }
