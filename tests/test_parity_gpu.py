@@ -204,6 +204,23 @@ def test_slide_structured_content(gpu, content):
         assert np.array_equal(run(gpu, img, r, L, 0, SLIDE, L == 256), want), (content, r, L)
 
 
+def test_slide_wide_image_long_flat_stretches(gpu):
+    """Passes thousands of columns wide: several jumps over flat stretches per
+    pass (the lookahead covers 1024 columns), edges right after a jump, at the
+    ends of the lookahead window and in the last columns."""
+    rng = np.random.default_rng(11)
+    h, w = 96, 16384 + 17
+    img = np.empty((h, w, 3), np.uint8)
+    img[:] = rng.integers(0, 256, 3, dtype=np.uint8)
+    for x in (63, 64, 65, 1023, 1024, 1025, 1087, 2047, 2048, 5000, 5001, 9000, 12287, 12288, w - 12, w - 1):
+        img[:, x:] = rng.integers(0, 256, 3, dtype=np.uint8)
+    img[40:50, 3000:11000] = rng.integers(0, 256, 3, dtype=np.uint8)
+    img[70:, 7000:7003] = rng.integers(0, 256, 3, dtype=np.uint8)
+    for r, L in ((10, 256), (8, 64), (15, 255)):
+        want = oracle_lib.oracle_filter(img, r, L, 0, threads=8)
+        assert np.array_equal(run(gpu, img, r, L, 0, SLIDE, L == 256), want), (r, L)
+
+
 def test_slide_more_bands_than_the_plan_orders(gpu):
     """The work plan orders up to 1024 bands by cost; a taller launch keeps
     the natural order (identity permutation)."""
