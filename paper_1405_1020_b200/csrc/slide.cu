@@ -853,10 +853,18 @@ __global__ void __launch_bounds__(kWarps * 32)
         // two prefix sums over the rows -- 2(2r + 1) loads per lane
         // instead of (2r + 1)^2.  R, G, B travel as 21-bit fields of
         // one 64-bit word (a prefix is at most 62 rows x 31 x 255).
-        while (__popc(todo) >= OPC_SLIDE_PAR_SUMS) {
-            const int bj = __shfl_sync(FULL, best, __ffs(todo) - 1);
-            const unsigned grp = __ballot_sync(FULL, ((todo >> lane) & 1u) != 0u && best == bj);
-            if (2 * __popc(grp) < __popc(todo)) break;  // many winners: own windows, below
+        // (every bin that four or more of the lanes share; lanes with rarer
+        // bins are left for the per-lane forms below)
+        unsigned big = 0;  // lanes of `todo` whose bin four or more of them share
+        if (__popc(todo) >= OPC_SLIDE_PAR_SUMS) {
+            const bool mine = ((todo >> lane) & 1u) != 0u;
+            const unsigned same = __match_any_sync(FULL, mine ? best : -1 - lane);
+            big = __ballot_sync(FULL, mine && __popc(same) >= OPC_SLIDE_PAR_SUMS);
+        }
+        todo &= ~big;
+        while (big) {
+            const int bj = __shfl_sync(FULL, best, __ffs(big) - 1);
+            const unsigned grp = __ballot_sync(FULL, ((big >> lane) & 1u) != 0u && best == bj);
             std::uint32_t rb0 = 0, g0 = 0, rb1 = 0, g1 = 0;
             const std::uint32_t* colb = ringp(xw) - lane;  // row 0 of column x
             const bool two = lane < 2 * r;
@@ -901,7 +909,7 @@ __global__ void __launch_bounds__(kWarps * 32)
                 sg = static_cast<std::uint32_t>(ws >> 21) & 0x1FFFFFu;
                 sb = static_cast<std::uint32_t>(ws >> 42);
             }
-            todo &= ~grp;
+            big &= ~grp;
         }
 #endif
         const bool own = __popc(todo) >= OPC_SLIDE_PAR_SUMS;
