@@ -1145,11 +1145,13 @@ __global__ void __launch_bounds__(kWarps * 32)
                 const int p2 = xn >= n ? (n + kStageCols - 1) / kStageCols : xn / kStageCols;
                 if (p2 - p >= kJumpMin) {
                     [[maybe_unused]] const long long t_j = SEC_NOW();
-                    emit_flat(kStageCols * p, min(n, kStageCols * p2) - kStageCols * p);
                     if (kStageCols * p2 >= n) {
+                        emit_flat(kStageCols * p, n - kStageCols * p);
                         SEC_ADD(6, t_j);
                         break;  // the pass ends flat
                     }
+                    // (the ring is restarted first: its loads fly while the
+                    // stretch is emitted, which touches no ring column)
                     // every chunk in flight lands before the ring is re-based
                     for (int k = kwaited + 1; k <= kissued; ++k) wait(k);
                     // chunk p2 (the column step 16 p2 removes) takes the next
@@ -1166,6 +1168,7 @@ __global__ void __launch_bounds__(kWarps * 32)
                     if (lane == 0) {
                         for (int k = p2; k <= kissued; ++k) issue(k);
                     }
+                    emit_flat(kStageCols * p, kStageCols * (p2 - p));
                     kwaited = min(kmax, p2 + K0);
                     for (int k = p2; k <= kwaited; ++k) wait(k);
                     cin = ringp(kStageCols * p2 + 2 * r);
