@@ -449,18 +449,21 @@ __global__ void __launch_bounds__(kPlanThreads) slide_plan_kernel(BandArgs a, TG
     if (staged) {
         // (padded: entry b at b + b / 16, so 16 consecutive blocks per lane
         // read conflict-free)
-        // (batches of 8 loads in flight: one L2 round trip per batch, not per entry)
-        for (long long i0 = t; i0 < nblocks; i0 += 8 * kPlanThreads) {
-            std::uint32_t v[8];
+        // (a warp per band position: coalesced loads of the band's costs in
+        // batches of 4, no index division)
+        const int nbp = a.frames * g.nbands;
+        for (int pos = t >> 5; pos < nbp; pos += kPlanThreads / 32) {
+            const long long src = static_cast<long long>(ordered ? band_at[pos] : pos) * g.ncb;
+            const int dst = pos * g.ncb;
+            for (int j0 = lane; j0 < g.ncb; j0 += 4 * 32) {
+                std::uint32_t v[4];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const long long i = i0 + static_cast<long long>(k) * kPlanThreads;
-                v[k] = i < nblocks ? __ldcg(g.bc + block_at(i)) : 0u;
-            }
+                for (int k = 0; k < 4; ++k) v[k] = j0 + 32 * k < g.ncb ? __ldcg(g.bc + src + j0 + 32 * k) : 0u;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const long long i = i0 + static_cast<long long>(k) * kPlanThreads;
-                if (i < nblocks) sbc[i + (i >> 4)] = v[k];
+                for (int k = 0; k < 4; ++k) {
+                    const int i = dst + j0 + 32 * k;
+                    if (j0 + 32 * k < g.ncb) sbc[i + (i >> 4)] = v[k];
+                }
             }
         }
     }
@@ -520,14 +523,54 @@ __global__ void __launch_bounds__(kPlanThreads) slide_plan_kernel(BandArgs a, TG
         return min(j, g.nch - 1);
     };
     std::uint32_t e_b = wsum[w] + incl - mine;  // cost before b0
-    int prev = b0 == 0 ? -1 : chunk_of(e_b - cost(b0 - 1));
-    for (int b = b0; b < b1; ++b) {
-        // block b belongs to chunk(E_b), E_b = cost before b; the chunks
-        // starting at b are (chunk(E_{b-1}), chunk(E_b)]
-        const int cur = max(prev, chunk_of(e_b));
-        for (int i = prev + 1; i <= cur && i < g.nch; ++i) g.cs[i] = b;
-        prev = cur;
-        e_b += cost(b);
+    if (staged) {
+        // The staged costs become their exclusive prefixes in place; chunk i
+        // then starts at the first block whose prefix reaches the chunk's cost
+        // threshold (the inverse of the block -> chunk map: 1 - q^i of the
+        // total in the decreasing part, equal steps after it) -- a binary
+        // search per chunk instead of a map evaluation per block.  (Should
+        // rounding ever order two neighbouring thresholds the wrong way, a few
+        // blocks are filtered twice with the same result: every block stays
+        // covered.)
+        for (int b = b0; b < b1; ++b) {
+            const int k = b + (b >> 4);
+            const std::uint32_t c = sbc[k];
+            sbc[k] = e_b;
+            e_b += c;
+        }
+        __syncthreads();
+        for (int i = t; i < g.nch; i += kPlanThreads) {
+            float x;  // cost fraction before chunk i
+            if (g.lnq == 0.0f) {
+                x = static_cast<float>(i) / static_cast<float>(g.nch);
+            } else if (i < g.J) {
+                x = 1.0f - expf(static_cast<float>(i) * g.lnq);
+            } else {
+                x = g.xJ + static_cast<float>(i - g.J) / g.rm;
+            }
+            const float thr_f = x * static_cast<float>(total);
+            const std::uint32_t thr = thr_f >= 4294967040.0f ? 0xFFFFFFFFu : static_cast<std::uint32_t>(thr_f);
+            int lo = 0, hi = nbl;  // first block with prefix >= thr
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (sbc[mid + (mid >> 4)] >= thr) {
+                    hi = mid;
+                } else {
+                    lo = mid + 1;
+                }
+            }
+            g.cs[i] = i == 0 ? 0 : lo;
+        }
+    } else {
+        int prev = b0 == 0 ? -1 : chunk_of(e_b - cost(b0 - 1));
+        for (int b = b0; b < b1; ++b) {
+            // block b belongs to chunk(E_b), E_b = cost before b; the chunks
+            // starting at b are (chunk(E_{b-1}), chunk(E_b)]
+            const int cur = max(prev, chunk_of(e_b));
+            for (int i = prev + 1; i <= cur && i < g.nch; ++i) g.cs[i] = b;
+            prev = cur;
+            e_b += cost(b);
+        }
     }
     PLAN_TICK(3);
 #if OPC_PLAN_CLOCK
