@@ -320,14 +320,22 @@ __global__ void __launch_bounds__(256) transpose_kernel(BandArgs a, std::uint32_
     const int ymax = g.y_base + g.Hs;
     const int w2 = 2 * a.radius + 1;
     std::uint32_t* dm = g.dmask + (static_cast<std::size_t>(frame) * g.ntr + blockIdx.y) * g.ncols;
-    for (int c = warp; c < kTCols; c += 8) {
-        const int x = x0 + c, y = y0 + lane;
-        const std::uint32_t v = tile[lane * kTStride + 32 + c];
-        const std::uint32_t m = __ballot_sync(0xFFFFFFFFu, v != tile[lane * kTStride + 32 + c - w2]);
-        if (x < g.ncols) {
-            if (y < ymax) Tf[static_cast<std::size_t>(x) * g.Hs + (y - g.y_base)] = v;
-            if (lane == 0) dm[x] = m;
-        }
+    // (pointers stepped per column, the plane's column bound hoisted: the
+    // tile rows are all inside the plane -- Hs is a multiple of the tile height)
+    static_cast<void>(ymax);
+    const int cmax = min(kTCols, g.ncols - x0);
+    const std::uint32_t* tl = tile + lane * kTStride + 32 + warp;
+    std::uint32_t* tp = Tf + static_cast<std::size_t>(x0 + warp) * g.Hs + (y0 + lane - g.y_base);
+    std::uint32_t* dp = dm + x0 + warp;
+    const std::size_t tstep = static_cast<std::size_t>(8) * g.Hs;
+    for (int c = warp; c < cmax; c += 8) {
+        const std::uint32_t v = tl[0];
+        const std::uint32_t m = __ballot_sync(0xFFFFFFFFu, v != tl[-w2]);
+        *tp = v;
+        if (lane == 0) *dp = m;
+        tl += 8;
+        tp += tstep;
+        dp += 8;
     }
 }
 
