@@ -8,5 +8,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sli
 for c in c3 c4; do timeout 900 python bench.py --config $c --steps 20 --warmup 3 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; done
 timeout 600 python scripts/band_scaling.py --config c3 1 2 4 8 > gpurun_out/band_scaling_c3.log 2>&1
 if [ -f exp/trace.so ]; then OILPAINT_B200_LIB=$PWD/exp/trace.so timeout 120 python scripts/slide_trace.py > gpurun_out/slide_trace_head.log 2>&1; fi
-timeout 400 python scripts/fuzz_parity.py --seconds 120 --seed 63 > gpurun_out/fuzz_head.log 2>&1
+timeout 400 python scripts/fuzz_parity.py --seconds 60 --seed 64 > gpurun_out/fuzz_head.log 2>&1
 echo done > gpurun_out/refresh_c3.done
