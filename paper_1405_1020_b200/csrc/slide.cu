@@ -16,6 +16,12 @@
 //  * the winner's channel sums are tracked in registers and recomputed from
 //    the window (2r+1)^2 when the winner changes; output = truncating quotient
 //    (filter.cpp:41-43) via the exact reciprocal table.
+// What the content allows is skipped: runs of flat steps are
+// emitted at once and long flat stretches jumped without ring loads; a step
+// whose rows form at most two runs of one (entering, leaving) bin pair is two
+// weighted count updates; winner changes of several lanes to one bin share
+// their row sums; uniform and striped pass starts are set up from 1 or 2r+1
+// pixels.  The work plan (slide_plan_kernel) balances the passes by cost.
 // Pixels come from a transposed (column-major) entry plane written by the
 // shared pre-pass, so a ring column (32+2r rows) is one contiguous run: the
 // ring is filled by TMA (one 2D box of 16 columns x the band's rows per
@@ -317,12 +323,10 @@ __global__ void __launch_bounds__(256) transpose_kernel(BandArgs a, std::uint32_
         }
     }
     __syncthreads();
-    const int ymax = g.y_base + g.Hs;
     const int w2 = 2 * a.radius + 1;
     std::uint32_t* dm = g.dmask + (static_cast<std::size_t>(frame) * g.ntr + blockIdx.y) * g.ncols;
     // (pointers stepped per column, the plane's column bound hoisted: the
     // tile rows are all inside the plane -- Hs is a multiple of the tile height)
-    static_cast<void>(ymax);
     const int cmax = min(kTCols, g.ncols - x0);
     const std::uint32_t* tl = tile + lane * kTStride + 32 + warp;
     std::uint32_t* tp = Tf + static_cast<std::size_t>(x0 + warp) * g.Hs + (y0 + lane - g.y_base);
